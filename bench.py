@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""bench.py — chunk-prefill attention TFLOP/s of the CDSP hot path on B200.
+
+Workload (BASELINE.json configs[1]): 7B-shaped MHA (32 Q / 32 KV heads, d=128), a 32K-token
+prompt as ONE chunk, bf16, synthetic seeded inputs (cdsp_inputs.py).  On N GPUs the chunk
+runs at SP=N (one process per GPU, torchrun): at N=8 this is configs[1] exactly; total work
+is fixed, so scaling is "strong".  ``--weak`` instead holds 32K tokens per GPU (L = 32K*N).
+
+One step = one pass of the whole hot path over the chunk:
+  a1 plan -> partition (host, cdsp_plan_partition)
+  a2 zigzag gather of this rank's q/k/v shard from the full tensors (cdsp_zigzag_gather)
+  a4-a6 cdsp_prefill_chunk: store append, ring KV exchange (s>1), block attention with the
+        LSE merge fused into its epilogue
+  a2 zigzag scatter of the output shard (cdsp_zigzag_scatter)
+  a7 KV transfer into decode paged caches (cdsp_kv_transfer_to_decode)
+(a3 balancing does not occur in a single-chunk plan.)
+
+value = algorithmic attention FLOPs of the chunk, 4*d*Hq*L(L+1)/2, over the
+step time (max over ranks, CUDA events).  Inputs (0.8 GB+) exceed the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "chunk-prefill attention TFLOP/s & latency at SP=1/2/4/8 B200; % of bf16 tensor peak"
+UNIT = "TFLOP/s"
+
+
+def attn_flops(L: int, C: int, Hq: int, D: int) -> float:
+    """Algorithmic FLOPs of one chunk: 4 d Hq (L C + L(L+1)/2) (visible pairs x 2 GEMMs)."""
+    return 4.0 * D * Hq * (L * C + L * (L + 1) / 2.0)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return {"bf16_burst": j["bf16_tflops"], "bf16_sustained": j.get("bf16_tflops_sustained", j["bf16_tflops"]),
+                "hbm_gbs": j["hbm_gbs"], "source": "measured"}
+    except Exception:
+        return {"bf16_burst": 1590.0, "bf16_sustained": 1400.0, "hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                  "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                 stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            return
+        while not self._stop.is_set():
+            line = p.stdout.readline()
+            if not line:
+                break
+            self.rows.append([x.strip() for x in line.split(",")])
+        p.terminate()
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------ CPU oracle
+def oracle_sample(q, k, v, scale, n_rows, seed=11):
+    """Time the oracle on n_rows seeded query rows of the workload (all heads).  Returns
+    (seconds, algorithmic flops of the sample, threads)."""
+    import oracle
+    from cdsp_inputs import sample_rows
+    N, Hq, D = q.shape
+    rows = sample_rows(N, n_rows, seed=seed).numpy()
+    qf = q.float().cpu().numpy()
+    kf = k.float().cpu().numpy()
+    vf = v.float().cpu().numpy()
+    t0 = time.perf_counter()
+    oracle.causal_rows(qf, kf, vf, scale, rows=rows)
+    dt = time.perf_counter() - t0
+    flops = 4.0 * D * Hq * float(np.sum(rows + 1))
+    return dt, flops, oracle.num_threads(), rows
+
+
+def cpu_baseline(q, k, v, scale, target_s=12.0):
+    import oracle
+    oracle.build()
+    dt0, f0, _, _ = oracle_sample(q, k, v, scale, 16, seed=5)
+    rate = f0 / max(dt0, 1e-6)
+    per_row = f0 / 16
+    n = int(max(16, min(4096, target_s * rate / per_row)))
+    dt, fl, thr, rows = oracle_sample(q, k, v, scale, n)
+    return {"value": fl / dt / 1e12, "unit": UNIT, "cores": thr, "kind": "oracle",
+            "sample": f"{len(rows)} seeded query rows x all {q.shape[1]} heads of the {q.shape[0]}-token "
+                      f"workload (f64 C oracle, OpenMP), {dt:.1f} s; value = sample attention FLOPs / time",
+            "seconds": dt}
+
+
+# ------------------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world, cfg):
+    """--impl reference: the CPU oracle is this tier's reference implementation."""
+    if rank != 0:
+        return
+    from cdsp_inputs import qkv
+    import oracle
+    oracle.build()
+    L, Hq, Hkv, D = cfg["L"], cfg["Hq"], cfg["Hkv"], cfg["D"]
+    q, k, v = qkv(L, Hq, Hkv, D, torch.bfloat16, seed=0)
+    scale = 1.0 / math.sqrt(D)
+    n_rows = args.ref_rows
+    times, flops = [], []
+    for i in range(args.warmup + args.steps):
+        dt, fl, thr, _ = oracle_sample(q, k, v, scale, n_rows, seed=100 + i)
+        if i >= args.warmup:
+            times.append(dt)
+            flops.append(fl)
+    value = sum(flops) / sum(times) / 1e12
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True,
+            "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": cfg["config"],
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
+                             "sample": f"{n_rows} seeded query rows x all heads per step (f64 C oracle)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--weak", action="store_true", help="hold 32K tokens per GPU (L = 32K * N)")
+    ap.add_argument("--seq", type=int, default=32768, help="prompt tokens (per GPU with --weak)")
+    ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--kv-heads", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-rows", type=int, default=48)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        world = max(world, 1)
+    s = world
+    L = args.seq * (s if args.weak else 1)
+    Hq, Hkv, D = args.heads, args.kv_heads, 128
+    cfg = {"L": L, "Hq": Hq, "Hkv": Hkv, "D": D, "scaling": "weak" if args.weak else "strong",
+           "config": {"workload": "7B-shaped MHA 32K prompt, single chunk (BASELINE configs[1])"
+                      if not args.weak else f"weak: {args.seq} tokens per GPU, single chunk",
+                      "prompt_tokens": L, "chunks": 1, "sp": s, "q_heads": Hq, "kv_heads": Hkv, "head_dim": D,
+                      "plan": f"[({L}, ranks 0..{s - 1})]", "l2": "inputs larger than L2 (no flush needed)",
+                      "decode_target": "paged K/V, block 16, tp=min(8,Hkv), seeded block table"}}
+    if args.impl == "reference":
+        run_reference(args, rank, world, cfg)
+        return
+
+    from cdsp_inputs import block_table, qkv
+    from paper_2511_06247_b200 import api
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    stream = torch.cuda.current_stream(dev)
+
+    # synthetic inputs, resident in HBM before the timed region (same seeds on every rank)
+    q, k, v = qkv(L, Hq, Hkv, D, torch.bfloat16, seed=0, device=dev)
+    plan = api.Plan([(L, list(range(s)))])
+    m2 = L // s
+    comm = api.Comm(rank, world, local, api.plan_capacity(plan), Hkv, D, torch.bfloat16)
+    if world > 1:
+        comm.connect_process_group()
+    qs = torch.empty((m2, Hq, D), dtype=torch.bfloat16, device=dev)
+    ks = torch.empty((m2, Hkv, D), dtype=torch.bfloat16, device=dev)
+    vs = torch.empty_like(ks)
+    out_s = torch.empty_like(qs)
+    lse_s = torch.empty((Hq, m2), dtype=torch.float32, device=dev)
+    out_full = torch.empty_like(q)
+    tp = min(8, Hkv)
+    B = 16
+    n_logical = (L + B - 1) // B
+    num_blocks = n_logical + n_logical // 4
+    bt = block_table(n_logical, num_blocks, seed=7).to(dev)
+    kc = [torch.empty((num_blocks, B, Hkv // tp, D), dtype=torch.bfloat16, device=dev) for _ in range(tp)]
+    vc = [torch.empty_like(x) for x in kc]
+    dst = api.DecodeTarget(kc, vc, B, bt)
+    group = api.SpGroup(comm, plan, 0)
+    launches_per_step = 3 + 1 + s + (2 if s > 1 else 0) + 1 + 1
+
+    def step():
+        api.plan_partition(plan, 0) if L <= 65536 else None  # a1 (host)
+        comm.reset(stream)
+        api.zigzag_gather(q, s, rank, qs, stream)
+        api.zigzag_gather(k, s, rank, ks, stream)
+        api.zigzag_gather(v, s, rank, vs, stream)
+        api.prefill_chunk(qs, ks, vs, comm.kvstore(), group, 0.0, out_s, lse_s, stream)
+        api.zigzag_scatter(out_s, s, rank, out_full, stream)
+        api.kv_transfer_to_decode(ks, vs, group, dst, stream)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    comm.check()
+    comm.profile(True)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    attn_ms, attn_n = comm.profile_read()
+    comm.profile(False)
+    comm.check()
+    if dist is not None:
+        t = torch.tensor([ms, attn_ms / max(attn_n, 1)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, attn_avg = t.tolist()
+    else:
+        attn_avg = attn_ms / max(attn_n, 1)
+    ms_step = ms / args.steps
+    flops = attn_flops(L, 0, Hq, D)
+    value = flops / (ms_step * 1e-3) / 1e12
+
+    # e2e through the same public calls: pinned host q/k/v -> HBM, the step, output shard -> host
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        hout = torch.empty(out_s.shape, dtype=out_s.dtype).pin_memory()
+        h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv))
+        d2h = hout.numel() * hout.element_size()
+        n_e2e = max(1, min(args.steps, 5))
+
+        def e2e_step():
+            q.copy_(hq, non_blocking=True)
+            k.copy_(hk, non_blocking=True)
+            v.copy_(hv, non_blocking=True)
+            step()
+            hout.copy_(out_s, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = a0.elapsed_time(a1) / n_e2e
+        if dist is not None:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {"value": flops / (ems * 1e-3) / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems}
+
+    peaks = load_peaks()
+    # dominant kernel: the block-attention launch(es) inside cdsp_prefill_chunk
+    per_launch_flops = flops / s / s if s > 1 else flops
+    achieved = per_launch_flops / (attn_avg * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_attn_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"L{L}_H{Hq}_s{s}")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_sustained"], "unit": UNIT,
+                "frac": achieved / peaks["bf16_sustained"], "traffic": traffic,
+                "kernel": "attn_tc_kernel<128> (tcgen05/TMEM/TMA)", "avg_launch_ms": attn_avg,
+                "launches_timed": attn_n,
+                "peak_note": f"bf16_tflops_sustained of MEASURED_PEAKS.json ({peaks['source']}); kernel runs "
+                             f"back-to-back in a seconds-long loop; burst peak {peaks['bf16_burst']}",
+                "frac_of_burst": achieved / peaks["bf16_burst"], "frac_of_spec_2250": achieved / 2250.0}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": cfg["scaling"],
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": cfg["config"],
+            "roofline": roofline, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(), "chunk_latency_ms": ms_step,
+            "tflops_per_gpu": value / world}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(q, k, v, 1.0 / math.sqrt(D))
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    comm.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

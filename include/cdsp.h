@@ -1,0 +1,287 @@
+/*
+ * cdsp.h — C ABI of the B200-native CDSP chunked-prefill ring-attention library
+ * (libcdsp.so, sm_100a).
+ *
+ * The method: Tetris' Chunkwise Dynamic Sequence Parallelism (arXiv 2511.06247,
+ * /root/reference/PAPER.md, cited "P:<line>").  One prompt chunk's causal attention is
+ * sharded over an SP group of s in {1,2,4,8} GPUs with the zigzag partition; each
+ * rank attends its query shard to all historical KV (prior chunks, re-balanced onto the
+ * current group) and to the current chunk's KV, which circulates around the ring
+ * (P:59); partial results are combined by log-sum-exp merge; the finished KV is scattered
+ * into the decode instance's paged cache.
+ *
+ * Conventions for every call
+ *  - All tensors are caller-owned, contiguous, row-major [T, H, D] (D fastest) device
+ *    memory (cdsp_tensor), unless stated otherwise.  The library never frees caller memory.
+ *  - Every call validates its arguments on the host BEFORE enqueueing anything: on a
+ *    non-OK status nothing was launched.  cdsp_last_error() then returns a thread-local
+ *    message.
+ *  - Device work is asynchronous and stream-ordered after prior work on `cuda_stream`
+ *    (a cudaStream_t; NULL = legacy default stream).  Asynchronous failures surface as
+ *    CDSP_ERR_CUDA / CDSP_ERR_COMM on a later call (or cdsp_comm_check()).
+ *  - Collective calls (cdsp_prefill_chunk, cdsp_kv_transfer_to_decode) must be made by
+ *    every rank of the chunk's group with identical plan and chunk index (NCCL-like).
+ *
+ * Readings of the paper this interface fixes ("R<n>"):
+ *  R1 softmax scale is a parameter (default 1/sqrt(D)); R2 LSE is the natural log, fp32,
+ *  layout [H, T]; R3 merge formula; R4 key j = t is visible; R5 zigzag on chunk-local
+ *  indices, masks on global positions; R6 L % 2s == 0; R8 balancing pairing; R9 group
+ *  nesting; R14 GQA kv head = floor(h / (Hq/Hkv)); R15 paged layout; R16 empty rows
+ *  give lse = -inf, O = 0.
+ */
+#ifndef CDSP_H_
+#define CDSP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define CDSP_API __attribute__((visibility("default")))
+#else
+#define CDSP_API
+#endif
+
+#define CDSP_ABI_VERSION 1
+#define CDSP_IPC_HANDLE_BYTES 64   /* one cudaIpcMemHandle_t */
+#define CDSP_MAX_SP 8
+
+typedef enum {
+    CDSP_OK = 0,
+    CDSP_ERR_INVALID = 1,      /* NULL pointer, bad enum, misuse of a handle */
+    CDSP_ERR_SHAPE = 2,        /* inconsistent T/H/D, D not in {64,128}, Hq % Hkv != 0, L % 2s != 0 */
+    CDSP_ERR_DTYPE = 3,        /* dtype mismatch between q, k, v, out, store */
+    CDSP_ERR_PLAN = 4,         /* illegal plan (R9) or caller not in the chunk's group */
+    CDSP_ERR_CAPACITY = 5,     /* store / block table / work buffer too small */
+    CDSP_ERR_CUDA = 6,         /* a CUDA runtime/driver call failed */
+    CDSP_ERR_COMM = 7,         /* peer barrier timed out / IPC failure */
+    CDSP_ERR_UNSUPPORTED = 8   /* e.g. decode tp > Hkv (KV-head replication undefined) */
+} cdsp_status;
+
+typedef enum { CDSP_F32 = 0, CDSP_BF16 = 1 } cdsp_dtype;
+
+/* A contiguous device tensor [T, H, D]; element type `dtype`. */
+typedef struct {
+    void* ptr;
+    int32_t dtype;      /* cdsp_dtype */
+    int64_t T, H, D;
+} cdsp_tensor;
+
+/* One chunk of the CDSP plan A = [a_0 .. a_{l-1}], a_i = (token count, instance group)
+ * (Alg. 1; D1).  ranks[0..sp) is the group's RING ORDER, as instance (world)
+ * ranks.  R9: sp in {1,2,4,8}, non-decreasing over chunks, sp_c / sp_{c-1} integral, the
+ * previous chunk's ranks[] a prefix of this one's ("each chunk's instance group
+ * must include all instances involved in preceding chunks"), ranks distinct, len % (2 sp) == 0. */
+typedef struct {
+    int64_t len;
+    int32_t sp;
+    const int32_t* ranks;   /* host memory */
+} cdsp_chunk;
+
+typedef struct {
+    int32_t n_chunks;
+    const cdsp_chunk* chunks;   /* host memory */
+} cdsp_plan;
+
+/* A cache-balancing transfer: ring rank `src` sends store rows
+ * [src_off, src_off + n_tok) to ring rank `dst` (ring ranks of the chunk's group). */
+typedef struct {
+    int32_t src, dst;
+    int64_t src_off, n_tok;
+} cdsp_move;
+
+/* ---------------------------------------------------------------------------------
+ * Communicator: one per process per GPU ("instance").  It owns the instance's KV store
+ * (history of the current request, in memory its peers can read over NVLink), the ring
+ * receive double buffers, fp32 merge work buffers, an internal comm stream, events and
+ * the peer barrier flags.
+ * ------------------------------------------------------------------------------- */
+typedef struct cdsp_comm_s* cdsp_comm;
+
+/* Create the communicator of instance `rank` of `world` on CUDA device `device`.
+ * store_cap_tokens: capacity (tokens) of this instance's KV store and of each ring
+ * receive buffer; must cover the largest (history + shard) any chunk of any plan will
+ * hold on one rank.  Hkv, D, dtype: KV geometry of every request served.  Allocates
+ * 3 * store_cap_tokens * Hkv * D * sizeof(dtype) (+ small) bytes of device memory.
+ * Errors: CDSP_ERR_INVALID, CDSP_ERR_SHAPE (D not in {64,128}), CDSP_ERR_CUDA. */
+CDSP_API cdsp_status cdsp_comm_create(cdsp_comm* out, int32_t rank, int32_t world, int32_t device,
+                                      int64_t store_cap_tokens, int32_t Hkv, int32_t D, int32_t dtype);
+
+/* Export this instance's shared region as CDSP_IPC_HANDLE_BYTES bytes (host buffer). */
+CDSP_API cdsp_status cdsp_comm_ipc_handle(cdsp_comm c, void* handle_out);
+
+/* Multi-process: open every other instance's region.  handles = world * CDSP_IPC_HANDLE_BYTES
+ * host bytes, handle i from instance i (entry `rank` is ignored).  All instances must use
+ * the same store_cap_tokens / Hkv / D / dtype.  Errors: CDSP_ERR_COMM, CDSP_ERR_CUDA. */
+CDSP_API cdsp_status cdsp_comm_connect(cdsp_comm c, const void* handles);
+
+/* Loopback: `world` communicators created in THIS process on ONE device (comms[i] has
+ * rank i) are linked to each other.  Every virtual rank must then be driven on its own
+ * stream; calls only enqueue, so one host thread can issue them one after the other. */
+CDSP_API cdsp_status cdsp_comm_connect_local(cdsp_comm* comms, int32_t world);
+
+/* Poll for asynchronous errors (peer-barrier timeout -> CDSP_ERR_COMM).  Does not block. */
+CDSP_API cdsp_status cdsp_comm_check(cdsp_comm c);
+
+/* Optional live timing of the block-attention launches this communicator issues inside
+ * cdsp_prefill_chunk: with enable != 0, a CUDA event pair brackets each launch on the
+ * caller's stream (up to 8192 pairs).  _read synchronises on the last event and returns
+ * the summed kernel time (ms) and launch count since the last read, then resets. */
+CDSP_API cdsp_status cdsp_comm_profile(cdsp_comm c, int32_t enable);
+CDSP_API cdsp_status cdsp_comm_profile_read(cdsp_comm c, double* attn_ms, int32_t* n_launches);
+
+/* Destroy (synchronises the device first).  Peers must be done with this instance. */
+CDSP_API cdsp_status cdsp_comm_destroy(cdsp_comm c);
+
+/* Per-instance KV store (D4): the balanced history of the current request followed,
+ * after each chunk, by that chunk's zigzag shard.  A VIEW of comm-owned memory:
+ * k, v [cap, Hkv, D]; pos int32 [cap] global positions; rows [0, n) valid. */
+typedef struct {
+    cdsp_tensor k, v;
+    int32_t* pos;        /* device */
+    int64_t n, cap;
+} cdsp_kvstore;
+
+CDSP_API cdsp_status cdsp_kvstore_get(cdsp_comm c, cdsp_kvstore* out);
+
+/* Start a new request on this instance: its store becomes empty (host-side; stream-ordered
+ * uses of the old content must be complete or on `cuda_stream`, which this call joins). */
+CDSP_API cdsp_status cdsp_kvstore_reset(cdsp_comm c, void* cuda_stream);
+
+/* The SP group executing one chunk: communicator of the calling instance + plan + chunk. */
+typedef struct {
+    cdsp_comm comm;
+    const cdsp_plan* plan;
+    int32_t chunk;
+} cdsp_sp_group;
+
+/* ---------------------------------------------------------------------------------
+ * The four calls of the hot path
+ * ------------------------------------------------------------------------------- */
+
+/* Host-only and pure: the store capacity (rows per instance) `plan` needs, i.e. the
+ * largest history + shard any ring rank holds over the plan (R8).  Errors: as
+ * cdsp_plan_partition. */
+CDSP_API cdsp_status cdsp_plan_capacity(const cdsp_plan* plan, int64_t* rows);
+
+/* Host-only and pure.  For chunk c of `plan` (L = len, s = sp, m = L / 2s, C = tokens of
+ * earlier chunks) writes (NULL outputs are skipped):
+ *   tok_rank[L], tok_slot[L]: chunk-local token t is row tok_slot[t] of ring rank
+ *       tok_rank[t]'s shard; zigzag: shard S_j = [j m, (j+1) m) belongs to ring rank
+ *       j (j < s) or 2s-1-j, and rank i's shard is S_i followed by S_{2s-1-i};
+ *   rank_pos[s * 2m]: global position (C + local) of each shard row, rank-major;
+ *   moves[<= CDSP_MAX_SP], *n_moves: the balancing transfers executed before chunk c (R8).
+ * Errors: CDSP_ERR_INVALID, CDSP_ERR_PLAN. */
+CDSP_API cdsp_status cdsp_plan_partition(const cdsp_plan* plan, int32_t c, int32_t* tok_rank,
+                                         int32_t* tok_slot, int64_t* rank_pos, cdsp_move* moves,
+                                         int32_t* n_moves);
+
+/* Collective over plan->chunks[chunk].ranks.  The calling instance is ring rank r.
+ *   q [2m, Hq, D], k/v [2m, Hkv, D]: this rank's zigzag shard of the chunk (S_r then
+ *     S_{2s-1-r}), post-projection ("each instance first calculates its local tokens'
+ *     query, key, value"), dtype bf16 or f32 (all equal, = store dtype).
+ *   prev_kv: this instance's store view (cdsp_kvstore_get).  Before the chunk, history is
+ *     re-balanced from the previous group (R8); afterwards k/v are appended and
+ *     prev_kv->n is updated.  prev_kv->n must match the plan (store of chunk `chunk`).
+ *   softmax_scale: sigma of s_tj = sigma <q_t, k_j> (R1); <= 0 selects 1/sqrt(D).
+ *   out [2m, Hq, D] (dtype of q): exact causal attention of the shard's queries over every
+ *     earlier token of the request (history + chunk), RNE-rounded on the final write (R13).
+ *   lse: fp32 [Hq, 2m] device, natural log (R2); may be NULL.
+ * Errors: CDSP_ERR_INVALID/SHAPE/DTYPE/PLAN/CAPACITY (host validation), CDSP_ERR_CUDA. */
+CDSP_API cdsp_status cdsp_prefill_chunk(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
+                                        cdsp_kvstore* prev_kv, const cdsp_sp_group* sp_group,
+                                        float softmax_scale, cdsp_tensor* out, float* lse,
+                                        void* cuda_stream);
+
+/* n >= 1 partial attention results over disjoint key sets -> their combination (R3):
+ *   M = max_i lse_i; lse = M + ln sum_i e^{lse_i - M}; O = sum_i e^{lse_i - M} O_i / sum_i e^{lse_i - M}.
+ * o_parts[i]: fp32 [T, H, D]; lse_parts[i]: fp32 [H, T] device (rows may be -inf);
+ * out [T, H, D] fp32 or bf16 (RNE); lse fp32 [H, T] (may be NULL).  All -inf: O = 0,
+ * lse = -inf.  n <= 16.  Errors: CDSP_ERR_INVALID/SHAPE/DTYPE. */
+CDSP_API cdsp_status cdsp_lse_merge(int32_t n, const cdsp_tensor* const* o_parts,
+                                    const float* const* lse_parts, cdsp_tensor* out, float* lse,
+                                    void* cuda_stream);
+
+/* Decode paged-KV destination (R15).  Decode TP rank t (0 <= t < tp) owns KV heads
+ * [t Hkv/tp, (t+1) Hkv/tp); its K and V caches are each [num_blocks, block_size, Hkv/tp, D]
+ * (dtype of k) at k_cache[t] / v_cache[t] — pointers valid in the caller's address space
+ * (local, or peer memory mapped by the caller).  block_table: device int32
+ * [n_table], logical block -> physical block; position p lives at
+ * (block_table[p / block_size], p mod block_size). */
+typedef struct {
+    int32_t tp, block_size;
+    int64_t num_blocks;
+    void* const* k_cache;         /* host array of tp device pointers */
+    void* const* v_cache;         /* host array of tp device pointers */
+    const int32_t* block_table;   /* device */
+    int64_t n_table;
+} cdsp_decode_target;
+
+/* Collective-free per-rank scatter of this rank's shard of chunk `chunk` (k, v as passed
+ * to cdsp_prefill_chunk) into the decode caches (chunk KV "streamed" to the
+ * decode instance).  Bit-exact byte copy.  Requires Hkv % tp == 0 (else
+ * CDSP_ERR_UNSUPPORTED) and n_table * block_size > every position (else
+ * CDSP_ERR_CAPACITY); block_table entries outside [0, num_blocks) are skipped and counted
+ * (see cdsp_kv_transfer_errors). */
+CDSP_API cdsp_status cdsp_kv_transfer_to_decode(const cdsp_tensor* k, const cdsp_tensor* v,
+                                                const cdsp_sp_group* sp_group,
+                                                const cdsp_decode_target* dst, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------------
+ * Building blocks, exported for tests and benches (same kernels the path uses)
+ * ------------------------------------------------------------------------------- */
+
+/* Segment description of one block-attention launch (one ring step).  Query row i has
+ * global position q_pos0 + i for i < q_len0, else q_pos1 + (i - q_len0).  KV rows
+ * [0, kv_hist) are history (always visible); row kv_hist + j has position
+ * kv_pos0 + j for j < kv_len0, else kv_pos1 + (j - kv_len0).  Key visible iff its
+ * position <= the query's (R4).  Rows >= nq / >= nkv do not exist. */
+typedef struct {
+    int64_t nq, q_len0, q_pos0, q_pos1;
+    int64_t nkv, kv_hist, kv_len0, kv_pos0, kv_pos1;
+} cdsp_segments;
+
+/* Merge mode of cdsp_attention_fwd. */
+typedef enum {
+    CDSP_ATTN_ONLY = 0,   /* final out (+lse) from this block alone                      */
+    CDSP_ATTN_FIRST = 1,  /* o_acc/lse_acc := this block                                 */
+    CDSP_ATTN_MID = 2,    /* o_acc/lse_acc := merge(acc, this block)                     */
+    CDSP_ATTN_LAST = 3    /* out/lse := merge(acc, this block)                           */
+} cdsp_attn_mode;
+
+/* One block-attention launch: q [nq, Hq, D]; k, v [nkv, Hkv, D]; o_acc fp32 [nq, Hq, D] and
+ * lse_acc fp32 [Hq, nq] (FIRST/MID/LAST); out [nq, Hq, D] dtype of q and lse fp32 [Hq, nq]
+ * (ONLY/LAST; lse may be NULL).  bf16 runs the tcgen05/TMEM/TMA kernel, f32 the FFMA kernel. */
+CDSP_API cdsp_status cdsp_attention_fwd(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
+                                        const cdsp_segments* seg, float softmax_scale, int32_t mode,
+                                        float* o_acc, float* lse_acc, cdsp_tensor* out, float* lse,
+                                        void* cuda_stream);
+
+/* Zigzag gather / scatter: full [L, H, D] <-> ring rank r's shard [2m, H, D]
+ * (rows S_r then S_{2s-1-r}).  Bit-exact.  Errors: CDSP_ERR_SHAPE, CDSP_ERR_DTYPE. */
+CDSP_API cdsp_status cdsp_zigzag_gather(const cdsp_tensor* full, int32_t s, int32_t r, cdsp_tensor* shard,
+                                        void* cuda_stream);
+CDSP_API cdsp_status cdsp_zigzag_scatter(const cdsp_tensor* shard, int32_t s, int32_t r, cdsp_tensor* full,
+                                         void* cuda_stream);
+
+/* Device zigzag maps: tok_rank / tok_slot int32 [L] device. */
+CDSP_API cdsp_status cdsp_zigzag_map_device(int64_t L, int32_t s, int32_t* tok_rank, int32_t* tok_slot,
+                                            void* cuda_stream);
+
+/* Number of block-table entries the last cdsp_kv_transfer_to_decode on this comm found out
+ * of range (synchronises `cuda_stream`). */
+CDSP_API cdsp_status cdsp_kv_transfer_errors(cdsp_comm c, void* cuda_stream, int64_t* n_bad);
+
+/* Thread-local message of the last non-OK status returned on this thread. */
+CDSP_API const char* cdsp_last_error(void);
+
+/* CDSP_ABI_VERSION of the loaded library. */
+CDSP_API int32_t cdsp_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CDSP_H_ */

@@ -1,0 +1,688 @@
+// cdsp.cu — the C ABI of libcdsp.so: communicator (peer-readable KV store, ring buffers,
+// barriers), the CDSP chunk-prefill orchestration, and the exported building blocks.
+//
+// Per-call procedure of cdsp_prefill_chunk on ring rank r of chunk c (§4.1, Fig. 5;
+// P:59 §2.3 ring attention; §6 "zigzag ring attention for historical tokens"):
+//   B1  peer barrier (previous call's peer reads of every store are finished)
+//   balancing: a rank new to the group pulls its part of an old rank's store (R8);
+//       old ranks keep part 0;                                   then B2 (pulls done)
+//   append this rank's k/v shard (and positions) to its store
+//   B3  peer barrier (every store holds history + shard)
+//   ring, step k = 0..s-1: src = (r - k) mod s (R11: receive from the previous neighbour);
+//       the block = src's whole store (history + shard).  Step 0 reads the own store;
+//       step k >= 1 pulls src's store over NVLink with the copy engines on the internal comm
+//       stream into one of two receive buffers (owner-pull: on NVSwitch every peer is one
+//       hop, so the logical ring needs no store-and-forward), overlapped with step k-1's
+//       attention; each step's attention LSE-merges into fp32 accumulators in its epilogue
+//       and the last step writes the output.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "plan.h"
+
+namespace cdsp {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+const char* last_error() { return g_err; }
+
+}  // namespace cdsp
+
+using namespace cdsp;
+
+namespace {
+constexpr int kMaxWorld = 8;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct PeerView {
+    char* k = nullptr;
+    char* v = nullptr;
+    int32_t* pos = nullptr;
+    unsigned long long* flags = nullptr;
+};
+}  // namespace
+
+struct cdsp_comm_s {
+    int rank = 0, world = 1, device = 0;
+    int64_t cap = 0;
+    int Hkv = 0, D = 0;
+    int32_t dtype = CDSP_BF16;
+    size_t esize = 2, row_bytes = 0;
+    // shared (IPC-exportable) region: K store | V store | positions | barrier flags
+    void* region = nullptr;
+    size_t region_bytes = 0, off_v = 0, off_pos = 0, off_flags = 0;
+    PeerView self;
+    PeerView peers[kMaxWorld];
+    void* ipc_base[kMaxWorld] = {nullptr};
+    bool connected = false;
+    // local buffers
+    void* recv = nullptr;  // 2 x (K, V) receive buffers, cap rows each
+    char* recv_k[2] = {nullptr, nullptr};
+    char* recv_v[2] = {nullptr, nullptr};
+    float* o_acc = nullptr;
+    float* lse_acc = nullptr;
+    size_t acc_elems = 0, lse_elems = 0;
+    unsigned long long sent[kMaxWorld] = {0};
+    int* err_host = nullptr;
+    int* err_dev = nullptr;
+    unsigned long long* bad_count = nullptr;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_done = nullptr, ev_copy[2] = {nullptr, nullptr},
+                ev_comp[2] = {nullptr, nullptr};
+    int64_t n = 0;  // valid store rows
+    // live kernel timing (cdsp_comm_profile)
+    bool profiling = false;
+    std::vector<cudaEvent_t> prof_ev;  // pairs
+    int prof_n = 0;
+};
+
+namespace {
+
+cdsp_status check_tensor(const cdsp_tensor* t, const char* name) {
+    CDSP_REQUIRE(t != nullptr, CDSP_ERR_INVALID, "%s is NULL", name);
+    CDSP_REQUIRE(dtype_ok(t->dtype), CDSP_ERR_DTYPE, "%s: bad dtype %d", name, t->dtype);
+    CDSP_REQUIRE(t->T >= 0 && t->H > 0 && t->D > 0, CDSP_ERR_SHAPE, "%s: bad shape [%lld,%lld,%lld]", name,
+                 static_cast<long long>(t->T), static_cast<long long>(t->H), static_cast<long long>(t->D));
+    CDSP_REQUIRE(t->T == 0 || t->ptr != nullptr, CDSP_ERR_INVALID, "%s: NULL data", name);
+    CDSP_REQUIRE((reinterpret_cast<uintptr_t>(t->ptr) & 15u) == 0, CDSP_ERR_INVALID,
+                 "%s: data must be 16-byte aligned", name);
+    return CDSP_OK;
+}
+
+cdsp_status barrier(cdsp_comm c, const ChunkInfo& ci, cudaStream_t st) {
+    BarrierArgs a;
+    std::memset(&a, 0, sizeof(a));
+    for (int i = 0; i < ci.s; ++i) {
+        const int j = ci.ranks[i];
+        if (j == c->rank) continue;
+        c->sent[j] += 1;
+        a.remote[a.n] = c->peers[j].flags + c->rank;
+        a.local[a.n] = c->self.flags + j;
+        a.target[a.n] = c->sent[j];
+        ++a.n;
+    }
+    a.err = c->err_dev;
+    return launch_peer_barrier(a, st);
+}
+
+cdsp_status ensure_acc(cdsp_comm c, size_t acc_elems, size_t lse_elems, cudaStream_t st) {
+    if (acc_elems > c->acc_elems) {
+        if (c->o_acc) CDSP_CUDA(cudaFreeAsync(c->o_acc, st));
+        CDSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c->o_acc), acc_elems * sizeof(float), st));
+        c->acc_elems = acc_elems;
+    }
+    if (lse_elems > c->lse_elems) {
+        if (c->lse_acc) CDSP_CUDA(cudaFreeAsync(c->lse_acc, st));
+        CDSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c->lse_acc), lse_elems * sizeof(float), st));
+        c->lse_elems = lse_elems;
+    }
+    return CDSP_OK;
+}
+
+cdsp_status run_attention(const void* q, const void* k, const void* v, int32_t dtype, int Hq, int Hkv, int D,
+                          const cdsp_segments& seg, float scale, int mode, float* o_acc, float* lse_acc, void* out,
+                          float* lse, cudaStream_t st) {
+    AttnArgs a;
+    a.q = q;
+    a.k = k;
+    a.v = v;
+    a.dtype = dtype;
+    a.Hq = Hq;
+    a.Hkv = Hkv;
+    a.D = D;
+    a.seg = seg;
+    a.scale = scale;
+    a.mode = mode;
+    a.o_acc = o_acc;
+    a.lse_acc = lse_acc;
+    a.out = out;
+    a.lse = lse;
+    return dtype == CDSP_BF16 ? launch_attention_tc(a, st) : launch_attention_simt(a, st);
+}
+
+// run_attention bracketed by a CUDA event pair when the communicator is profiling.
+cdsp_status run_attention_timed(cdsp_comm c, const void* q, const void* k, const void* v, int32_t dtype, int Hq,
+                                int Hkv, int D, const cdsp_segments& seg, float scale, int mode, float* o_acc,
+                                float* lse_acc, void* out, float* lse, cudaStream_t st) {
+    const bool rec = c->profiling && c->prof_n * 2 + 1 < static_cast<int>(c->prof_ev.size());
+    if (rec) CDSP_CUDA(cudaEventRecord(c->prof_ev[2 * c->prof_n], st));
+    CDSP_CHECK_STATUS(run_attention(q, k, v, dtype, Hq, Hkv, D, seg, scale, mode, o_acc, lse_acc, out, lse, st));
+    if (rec) {
+        CDSP_CUDA(cudaEventRecord(c->prof_ev[2 * c->prof_n + 1], st));
+        ++c->prof_n;
+    }
+    return CDSP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cdsp_last_error(void) { return cdsp::last_error(); }
+int32_t cdsp_abi_version(void) { return CDSP_ABI_VERSION; }
+
+// ------------------------------------------------------------------------------- comm
+cdsp_status cdsp_comm_create(cdsp_comm* out, int32_t rank, int32_t world, int32_t device, int64_t store_cap_tokens,
+                             int32_t Hkv, int32_t D, int32_t dtype) {
+    CDSP_REQUIRE(out != nullptr, CDSP_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    CDSP_REQUIRE(world >= 1 && world <= kMaxWorld, CDSP_ERR_INVALID, "world %d not in [1,%d]", world, kMaxWorld);
+    CDSP_REQUIRE(rank >= 0 && rank < world, CDSP_ERR_INVALID, "rank %d not in [0,%d)", rank, world);
+    CDSP_REQUIRE(store_cap_tokens >= 1 && Hkv >= 1, CDSP_ERR_SHAPE, "bad store geometry");
+    CDSP_REQUIRE(D == 64 || D == 128, CDSP_ERR_SHAPE, "head dim %d not in {64,128}", D);
+    CDSP_REQUIRE(dtype_ok(dtype), CDSP_ERR_DTYPE, "bad dtype %d", dtype);
+    CDSP_CUDA(cudaSetDevice(device));
+    cdsp_comm c = new cdsp_comm_s();
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    c->cap = store_cap_tokens;
+    c->Hkv = Hkv;
+    c->D = D;
+    c->dtype = dtype;
+    c->esize = dtype_size(dtype);
+    c->row_bytes = static_cast<size_t>(Hkv) * D * c->esize;
+    const size_t kv_bytes = align_up(static_cast<size_t>(store_cap_tokens) * c->row_bytes, 256);
+    c->off_v = kv_bytes;
+    c->off_pos = 2 * kv_bytes;
+    c->off_flags = c->off_pos + align_up(static_cast<size_t>(store_cap_tokens) * 4, 256);
+    c->region_bytes = c->off_flags + align_up(kMaxWorld * sizeof(unsigned long long), 256);
+    auto fail = [&](cudaError_t e, const char* what) {
+        set_error("%s failed: %s", what, cudaGetErrorString(e));
+        cdsp_comm_destroy(c);
+        return CDSP_ERR_CUDA;
+    };
+    cudaError_t e = cudaMalloc(&c->region, c->region_bytes);
+    if (e != cudaSuccess) return fail(e, "cudaMalloc(store)");
+    e = cudaMemset(c->region, 0, c->region_bytes);
+    if (e != cudaSuccess) return fail(e, "cudaMemset(store)");
+    char* base = static_cast<char*>(c->region);
+    c->self.k = base;
+    c->self.v = base + c->off_v;
+    c->self.pos = reinterpret_cast<int32_t*>(base + c->off_pos);
+    c->self.flags = reinterpret_cast<unsigned long long*>(base + c->off_flags);
+    c->peers[rank] = c->self;
+    e = cudaMalloc(&c->recv, 4 * kv_bytes);
+    if (e != cudaSuccess) return fail(e, "cudaMalloc(recv)");
+    for (int b = 0; b < 2; ++b) {
+        c->recv_k[b] = static_cast<char*>(c->recv) + (2 * b) * kv_bytes;
+        c->recv_v[b] = static_cast<char*>(c->recv) + (2 * b + 1) * kv_bytes;
+    }
+    e = cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped);
+    if (e != cudaSuccess) return fail(e, "cudaHostAlloc");
+    *c->err_host = 0;
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0);
+    if (e != cudaSuccess) return fail(e, "cudaHostGetDevicePointer");
+    e = cudaMalloc(reinterpret_cast<void**>(&c->bad_count), sizeof(unsigned long long));
+    if (e != cudaSuccess) return fail(e, "cudaMalloc(bad_count)");
+    e = cudaMemset(c->bad_count, 0, sizeof(unsigned long long));
+    if (e != cudaSuccess) return fail(e, "cudaMemset");
+    e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(e, "cudaStreamCreate");
+    cudaEvent_t* evs[6] = {&c->ev_ready, &c->ev_done, &c->ev_copy[0], &c->ev_copy[1], &c->ev_comp[0], &c->ev_comp[1]};
+    for (auto* ev : evs) {
+        e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return fail(e, "cudaEventCreate");
+    }
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return fail(e, "cudaDeviceSynchronize");
+    *out = c;
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_comm_ipc_handle(cdsp_comm c, void* handle_out) {
+    CDSP_REQUIRE(c && handle_out, CDSP_ERR_INVALID, "NULL argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == CDSP_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    CDSP_CUDA(cudaIpcGetMemHandle(&h, c->region));
+    std::memcpy(handle_out, &h, sizeof(h));
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_comm_connect(cdsp_comm c, const void* handles) {
+    CDSP_REQUIRE(c && handles, CDSP_ERR_INVALID, "NULL argument");
+    CDSP_REQUIRE(!c->connected, CDSP_ERR_INVALID, "communicator already connected");
+    const char* hb = static_cast<const char*>(handles);
+    for (int j = 0; j < c->world; ++j) {
+        if (j == c->rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, hb + static_cast<size_t>(j) * CDSP_IPC_HANDLE_BYTES, sizeof(h));
+        void* base = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+        CDSP_REQUIRE(e == cudaSuccess, CDSP_ERR_COMM, "cudaIpcOpenMemHandle(peer %d): %s", j, cudaGetErrorString(e));
+        c->ipc_base[j] = base;
+        char* b = static_cast<char*>(base);
+        c->peers[j].k = b;
+        c->peers[j].v = b + c->off_v;
+        c->peers[j].pos = reinterpret_cast<int32_t*>(b + c->off_pos);
+        c->peers[j].flags = reinterpret_cast<unsigned long long*>(b + c->off_flags);
+    }
+    c->connected = true;
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_comm_connect_local(cdsp_comm* comms, int32_t world) {
+    CDSP_REQUIRE(comms != nullptr && world >= 1 && world <= kMaxWorld, CDSP_ERR_INVALID, "bad comms/world");
+    for (int i = 0; i < world; ++i) {
+        CDSP_REQUIRE(comms[i] != nullptr, CDSP_ERR_INVALID, "comms[%d] is NULL", i);
+        CDSP_REQUIRE(comms[i]->rank == i && comms[i]->world == world, CDSP_ERR_INVALID,
+                     "comms[%d] has rank %d / world %d", i, comms[i]->rank, comms[i]->world);
+        CDSP_REQUIRE(comms[i]->cap == comms[0]->cap && comms[i]->Hkv == comms[0]->Hkv &&
+                         comms[i]->D == comms[0]->D && comms[i]->dtype == comms[0]->dtype &&
+                         comms[i]->device == comms[0]->device,
+                     CDSP_ERR_INVALID, "loopback communicators must share geometry and device");
+    }
+    for (int i = 0; i < world; ++i) {
+        for (int j = 0; j < world; ++j) comms[i]->peers[j] = comms[j]->self;
+        comms[i]->connected = true;
+    }
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_comm_check(cdsp_comm c) {
+    CDSP_REQUIRE(c != nullptr, CDSP_ERR_INVALID, "NULL comm");
+    if (*reinterpret_cast<volatile int*>(c->err_host) != 0)
+        CDSP_FAIL(CDSP_ERR_COMM, "peer barrier timed out on instance %d", c->rank);
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_comm_profile(cdsp_comm c, int32_t enable) {
+    CDSP_REQUIRE(c != nullptr, CDSP_ERR_INVALID, "NULL comm");
+    if (enable && c->prof_ev.empty()) {
+        c->prof_ev.resize(2 * 8192, nullptr);
+        for (auto& ev : c->prof_ev) CDSP_CUDA(cudaEventCreate(&ev));
+    }
+    c->profiling = enable != 0;
+    c->prof_n = 0;
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_comm_profile_read(cdsp_comm c, double* attn_ms, int32_t* n_launches) {
+    CDSP_REQUIRE(c && attn_ms && n_launches, CDSP_ERR_INVALID, "NULL argument");
+    double total = 0.0;
+    if (c->prof_n > 0) CDSP_CUDA(cudaEventSynchronize(c->prof_ev[2 * c->prof_n - 1]));
+    for (int i = 0; i < c->prof_n; ++i) {
+        float ms = 0.f;
+        CDSP_CUDA(cudaEventElapsedTime(&ms, c->prof_ev[2 * i], c->prof_ev[2 * i + 1]));
+        total += ms;
+    }
+    *attn_ms = total;
+    *n_launches = c->prof_n;
+    c->prof_n = 0;
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_comm_destroy(cdsp_comm c) {
+    if (!c) return CDSP_OK;
+    cudaDeviceSynchronize();
+    for (auto ev : c->prof_ev)
+        if (ev) cudaEventDestroy(ev);
+    for (int j = 0; j < kMaxWorld; ++j)
+        if (c->ipc_base[j]) cudaIpcCloseMemHandle(c->ipc_base[j]);
+    if (c->o_acc) cudaFree(c->o_acc);
+    if (c->lse_acc) cudaFree(c->lse_acc);
+    if (c->recv) cudaFree(c->recv);
+    if (c->region) cudaFree(c->region);
+    if (c->bad_count) cudaFree(c->bad_count);
+    if (c->err_host) cudaFreeHost(c->err_host);
+    cudaEvent_t evs[6] = {c->ev_ready, c->ev_done, c->ev_copy[0], c->ev_copy[1], c->ev_comp[0], c->ev_comp[1]};
+    for (auto ev : evs)
+        if (ev) cudaEventDestroy(ev);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    delete c;
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_kvstore_get(cdsp_comm c, cdsp_kvstore* out) {
+    CDSP_REQUIRE(c && out, CDSP_ERR_INVALID, "NULL argument");
+    out->k = cdsp_tensor{c->self.k, c->dtype, c->cap, c->Hkv, c->D};
+    out->v = cdsp_tensor{c->self.v, c->dtype, c->cap, c->Hkv, c->D};
+    out->pos = c->self.pos;
+    out->n = c->n;
+    out->cap = c->cap;
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_kvstore_reset(cdsp_comm c, void* cuda_stream) {
+    CDSP_REQUIRE(c != nullptr, CDSP_ERR_INVALID, "NULL comm");
+    (void)cuda_stream;  // content is overwritten in stream order by the next chunk
+    c->n = 0;
+    return CDSP_OK;
+}
+
+// ------------------------------------------------------------------------------- plan
+cdsp_status cdsp_plan_capacity(const cdsp_plan* plan, int64_t* rows) {
+    CDSP_REQUIRE(rows != nullptr, CDSP_ERR_INVALID, "rows is NULL");
+    ChunkInfo ci;
+    CDSP_CHECK_STATUS(plan_chunk_info(plan, 0, &ci));  // validates the plan
+    *rows = plan_max_store(plan);
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_plan_partition(const cdsp_plan* plan, int32_t c, int32_t* tok_rank, int32_t* tok_slot,
+                                int64_t* rank_pos, cdsp_move* moves, int32_t* n_moves) {
+    ChunkInfo ci;
+    CDSP_CHECK_STATUS(plan_chunk_info(plan, c, &ci));
+    const int64_t m = ci.m;
+    if (tok_rank || tok_slot) {
+        for (int64_t t = 0; t < ci.L; ++t) {
+            const int64_t j = t / m;  // shard S_j
+            const bool first = j < ci.s;
+            if (tok_rank) tok_rank[t] = static_cast<int32_t>(first ? j : 2 * ci.s - 1 - j);
+            if (tok_slot) tok_slot[t] = static_cast<int32_t>(first ? t - j * m : m + (t - j * m));
+        }
+    }
+    if (rank_pos) {
+        for (int r = 0; r < ci.s; ++r) {
+            int64_t* p = rank_pos + static_cast<size_t>(r) * 2 * m;
+            for (int64_t i = 0; i < m; ++i) {
+                p[i] = shard_pos0(ci, r) + i;
+                p[m + i] = shard_pos1(ci, r) + i;
+            }
+        }
+    }
+    if (moves)
+        for (int i = 0; i < ci.n_moves; ++i) moves[i] = ci.moves[i];
+    if (n_moves) *n_moves = ci.n_moves;
+    return CDSP_OK;
+}
+
+// ------------------------------------------------------------------------------- prefill
+cdsp_status cdsp_prefill_chunk(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
+                               cdsp_kvstore* prev_kv, const cdsp_sp_group* sp_group, float softmax_scale,
+                               cdsp_tensor* out, float* lse, void* cuda_stream) {
+    CDSP_REQUIRE(sp_group && sp_group->comm && sp_group->plan && prev_kv, CDSP_ERR_INVALID,
+                 "NULL sp_group/comm/plan/prev_kv");
+    CDSP_CHECK_STATUS(check_tensor(q, "q"));
+    CDSP_CHECK_STATUS(check_tensor(k, "k"));
+    CDSP_CHECK_STATUS(check_tensor(v, "v"));
+    CDSP_CHECK_STATUS(check_tensor(out, "out"));
+    cdsp_comm c = sp_group->comm;
+    ChunkInfo ci;
+    CDSP_CHECK_STATUS(plan_chunk_info(sp_group->plan, sp_group->chunk, &ci));
+    const int r = plan_ring_rank(ci, c->rank);
+    CDSP_REQUIRE(r >= 0, CDSP_ERR_PLAN, "instance %d is not in chunk %d's group", c->rank, ci.c);
+    for (int i = 0; i < ci.s; ++i)
+        CDSP_REQUIRE(ci.ranks[i] < c->world, CDSP_ERR_PLAN, "plan names instance %d >= world %d", ci.ranks[i],
+                     c->world);
+    const int64_t m2 = 2 * ci.m;
+    CDSP_REQUIRE(q->dtype == k->dtype && k->dtype == v->dtype && out->dtype == q->dtype && q->dtype == c->dtype,
+                 CDSP_ERR_DTYPE, "q/k/v/out/store dtypes differ");
+    CDSP_REQUIRE(q->T == m2 && k->T == m2 && v->T == m2 && out->T == m2, CDSP_ERR_SHAPE,
+                 "q/k/v/out must hold the rank's 2m=%lld shard rows", static_cast<long long>(m2));
+    CDSP_REQUIRE(q->D == c->D && k->D == c->D && v->D == c->D && out->D == c->D, CDSP_ERR_SHAPE,
+                 "head dim mismatch");
+    CDSP_REQUIRE(k->H == c->Hkv && v->H == c->Hkv, CDSP_ERR_SHAPE, "k/v heads must equal store Hkv=%d", c->Hkv);
+    CDSP_REQUIRE(q->H % c->Hkv == 0 && out->H == q->H, CDSP_ERR_SHAPE, "Hq %% Hkv != 0 or out heads != Hq");
+    CDSP_REQUIRE(prev_kv->k.ptr == c->self.k && prev_kv->v.ptr == c->self.v, CDSP_ERR_INVALID,
+                 "prev_kv is not this communicator's store (use cdsp_kvstore_get)");
+    CDSP_REQUIRE(c->n == ci.store_before[r], CDSP_ERR_PLAN,
+                 "store holds %lld rows but the plan expects %lld before chunk %d (missing cdsp_kvstore_reset?)",
+                 static_cast<long long>(c->n), static_cast<long long>(ci.store_before[r]), ci.c);
+    for (int i = 0; i < ci.s; ++i)
+        CDSP_REQUIRE(ci.hist[i] + m2 <= c->cap, CDSP_ERR_CAPACITY,
+                     "ring rank %d needs %lld store rows, capacity %lld", i,
+                     static_cast<long long>(ci.hist[i] + m2), static_cast<long long>(c->cap));
+    CDSP_REQUIRE(ci.s == 1 || c->connected, CDSP_ERR_INVALID, "communicator not connected");
+    CDSP_CHECK_STATUS(cdsp_comm_check(c));
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf(static_cast<float>(c->D));
+    const int Hq = static_cast<int>(q->H);
+    if (ci.s > 1) CDSP_CHECK_STATUS(ensure_acc(c, static_cast<size_t>(m2) * Hq * c->D, static_cast<size_t>(Hq) * m2, st));
+
+    // B1
+    if (ci.s > 1) CDSP_CHECK_STATUS(barrier(c, ci, st));
+    // cache balancing (R8)
+    if (ci.s_prev > 0 && ci.s > ci.s_prev) {
+        for (int i = 0; i < ci.n_moves; ++i) {
+            const cdsp_move& mv = ci.moves[i];
+            if (mv.dst != r || mv.n_tok == 0) continue;
+            const PeerView& src = c->peers[ci.ranks[mv.src]];
+            CDSP_CUDA(cudaMemcpyAsync(c->self.k, src.k + mv.src_off * c->row_bytes, mv.n_tok * c->row_bytes,
+                                      cudaMemcpyDeviceToDevice, st));
+            CDSP_CUDA(cudaMemcpyAsync(c->self.v, src.v + mv.src_off * c->row_bytes, mv.n_tok * c->row_bytes,
+                                      cudaMemcpyDeviceToDevice, st));
+            CDSP_CUDA(cudaMemcpyAsync(c->self.pos, src.pos + mv.src_off, mv.n_tok * sizeof(int32_t),
+                                      cudaMemcpyDeviceToDevice, st));
+        }
+        CDSP_CHECK_STATUS(barrier(c, ci, st));  // B2
+    }
+    c->n = ci.hist[r];
+    // append this chunk's shard
+    {
+        AppendArgs a;
+        a.k_src = k->ptr;
+        a.v_src = v->ptr;
+        a.k_dst = c->self.k + c->n * c->row_bytes;
+        a.v_dst = c->self.v + c->n * c->row_bytes;
+        a.pos_dst = c->self.pos + c->n;
+        a.n_rows = m2;
+        a.row_bytes = static_cast<int64_t>(c->row_bytes);
+        a.len0 = ci.m;
+        a.pos0 = shard_pos0(ci, r);
+        a.pos1 = shard_pos1(ci, r);
+        CDSP_CHECK_STATUS(launch_store_append(a, st));
+    }
+    c->n += m2;
+    prev_kv->n = c->n;
+
+    auto segs_for = [&](int src) {
+        cdsp_segments s;
+        s.nq = m2;
+        s.q_len0 = ci.m;
+        s.q_pos0 = shard_pos0(ci, r);
+        s.q_pos1 = shard_pos1(ci, r);
+        s.nkv = ci.hist[src] + m2;
+        s.kv_hist = ci.hist[src];
+        s.kv_len0 = ci.m;
+        s.kv_pos0 = shard_pos0(ci, src);
+        s.kv_pos1 = shard_pos1(ci, src);
+        return s;
+    };
+    if (ci.s == 1) {
+        return run_attention_timed(c, q->ptr, c->self.k, c->self.v, c->dtype, Hq, c->Hkv, c->D, segs_for(0), scale,
+                                   CDSP_ATTN_ONLY, nullptr, nullptr, out->ptr, lse, st);
+    }
+    CDSP_CHECK_STATUS(barrier(c, ci, st));  // B3
+    CDSP_CUDA(cudaEventRecord(c->ev_ready, st));
+    CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+    auto issue_copy = [&](int step) -> cdsp_status {
+        const int src = (r - step + ci.s) % ci.s;
+        const int b = step & 1;
+        if (step >= 3) CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_comp[b], 0));
+        const size_t bytes = static_cast<size_t>(ci.hist[src] + m2) * c->row_bytes;
+        const PeerView& pv = c->peers[ci.ranks[src]];
+        CDSP_CUDA(cudaMemcpyAsync(c->recv_k[b], pv.k, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
+        CDSP_CUDA(cudaMemcpyAsync(c->recv_v[b], pv.v, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
+        CDSP_CUDA(cudaEventRecord(c->ev_copy[b], c->comm_stream));
+        return CDSP_OK;
+    };
+    CDSP_CHECK_STATUS(issue_copy(1));
+    for (int step = 0; step < ci.s; ++step) {
+        if (step + 1 >= 2 && step + 1 < ci.s) CDSP_CHECK_STATUS(issue_copy(step + 1));
+        const int src = (r - step + ci.s) % ci.s;
+        const int b = step & 1;
+        const char* kb = c->self.k;
+        const char* vb = c->self.v;
+        if (step > 0) {
+            CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_copy[b], 0));
+            kb = c->recv_k[b];
+            vb = c->recv_v[b];
+        }
+        const int mode = step == 0 ? CDSP_ATTN_FIRST : (step == ci.s - 1 ? CDSP_ATTN_LAST : CDSP_ATTN_MID);
+        CDSP_CHECK_STATUS(run_attention_timed(c, q->ptr, kb, vb, c->dtype, Hq, c->Hkv, c->D, segs_for(src), scale,
+                                              mode, c->o_acc, c->lse_acc, out->ptr, lse, st));
+        if (step > 0) CDSP_CUDA(cudaEventRecord(c->ev_comp[b], st));
+    }
+    CDSP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
+    CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
+    return CDSP_OK;
+}
+
+// ------------------------------------------------------------------------------- merge
+cdsp_status cdsp_lse_merge(int32_t n, const cdsp_tensor* const* o_parts, const float* const* lse_parts,
+                           cdsp_tensor* out, float* lse, void* cuda_stream) {
+    CDSP_REQUIRE(n >= 1 && n <= kMaxMerge, CDSP_ERR_INVALID, "n=%d not in [1,%d]", n, kMaxMerge);
+    CDSP_REQUIRE(o_parts && lse_parts, CDSP_ERR_INVALID, "NULL parts");
+    CDSP_CHECK_STATUS(check_tensor(out, "out"));
+    const float* ptrs[kMaxMerge];
+    for (int i = 0; i < n; ++i) {
+        CDSP_CHECK_STATUS(check_tensor(o_parts[i], "o_parts[i]"));
+        CDSP_REQUIRE(o_parts[i]->dtype == CDSP_F32, CDSP_ERR_DTYPE, "partials must be fp32");
+        CDSP_REQUIRE(o_parts[i]->T == out->T && o_parts[i]->H == out->H && o_parts[i]->D == out->D, CDSP_ERR_SHAPE,
+                     "part %d shape differs from out", i);
+        CDSP_REQUIRE(lse_parts[i] != nullptr || out->T == 0, CDSP_ERR_INVALID, "lse_parts[%d] is NULL", i);
+        ptrs[i] = static_cast<const float*>(o_parts[i]->ptr);
+    }
+    CDSP_REQUIRE(out->D == 64 || out->D == 128, CDSP_ERR_SHAPE, "head dim %lld not in {64,128}",
+                 static_cast<long long>(out->D));
+    return launch_lse_merge(n, ptrs, lse_parts, out->T, static_cast<int>(out->H), static_cast<int>(out->D),
+                            out->ptr, out->dtype, lse, static_cast<cudaStream_t>(cuda_stream));
+}
+
+// ------------------------------------------------------------------------------- KV transfer
+cdsp_status cdsp_kv_transfer_to_decode(const cdsp_tensor* k, const cdsp_tensor* v, const cdsp_sp_group* sp_group,
+                                       const cdsp_decode_target* dst, void* cuda_stream) {
+    CDSP_REQUIRE(sp_group && sp_group->comm && sp_group->plan && dst, CDSP_ERR_INVALID, "NULL argument");
+    CDSP_CHECK_STATUS(check_tensor(k, "k"));
+    CDSP_CHECK_STATUS(check_tensor(v, "v"));
+    cdsp_comm c = sp_group->comm;
+    ChunkInfo ci;
+    CDSP_CHECK_STATUS(plan_chunk_info(sp_group->plan, sp_group->chunk, &ci));
+    const int r = plan_ring_rank(ci, c->rank);
+    CDSP_REQUIRE(r >= 0, CDSP_ERR_PLAN, "instance %d is not in chunk %d's group", c->rank, ci.c);
+    CDSP_REQUIRE(k->dtype == v->dtype, CDSP_ERR_DTYPE, "k/v dtypes differ");
+    CDSP_REQUIRE(k->T == 2 * ci.m && v->T == k->T && v->H == k->H && v->D == k->D, CDSP_ERR_SHAPE,
+                 "k/v must be this rank's [2m, Hkv, D] shard");
+    CDSP_REQUIRE(dst->tp >= 1 && dst->tp <= 8, CDSP_ERR_INVALID, "decode tp %d not in [1,8]", dst->tp);
+    CDSP_REQUIRE(k->H % dst->tp == 0, CDSP_ERR_UNSUPPORTED,
+                 "Hkv=%lld not divisible by decode tp=%d (KV-head replication is not defined)",
+                 static_cast<long long>(k->H), dst->tp);
+    CDSP_REQUIRE(dst->block_size >= 1 && dst->num_blocks >= 1 && dst->block_table && dst->k_cache && dst->v_cache,
+                 CDSP_ERR_INVALID, "bad decode target");
+    CDSP_REQUIRE(dst->n_table * dst->block_size >= ci.C + ci.L, CDSP_ERR_CAPACITY,
+                 "block table covers %lld positions, chunk ends at %lld",
+                 static_cast<long long>(dst->n_table * dst->block_size), static_cast<long long>(ci.C + ci.L));
+    PagedArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.k = k->ptr;
+    a.v = v->ptr;
+    a.n_tok = k->T;
+    a.Hkv = static_cast<int>(k->H);
+    a.D = static_cast<int>(k->D);
+    a.esize = static_cast<int>(dtype_size(k->dtype));
+    a.len0 = ci.m;
+    a.pos0 = shard_pos0(ci, r);
+    a.pos1 = shard_pos1(ci, r);
+    a.tp = dst->tp;
+    a.block_size = dst->block_size;
+    a.num_blocks = dst->num_blocks;
+    a.n_table = dst->n_table;
+    a.block_table = dst->block_table;
+    for (int t = 0; t < dst->tp; ++t) {
+        CDSP_REQUIRE(dst->k_cache[t] && dst->v_cache[t], CDSP_ERR_INVALID, "NULL cache pointer for tp rank %d", t);
+        a.k_cache[t] = dst->k_cache[t];
+        a.v_cache[t] = dst->v_cache[t];
+    }
+    a.bad_count = c->bad_count;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    CDSP_CUDA(cudaMemsetAsync(c->bad_count, 0, sizeof(unsigned long long), st));
+    return launch_paged_scatter(a, st);
+}
+
+cdsp_status cdsp_kv_transfer_errors(cdsp_comm c, void* cuda_stream, int64_t* n_bad) {
+    CDSP_REQUIRE(c && n_bad, CDSP_ERR_INVALID, "NULL argument");
+    unsigned long long h = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    CDSP_CUDA(cudaMemcpyAsync(&h, c->bad_count, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CDSP_CUDA(cudaStreamSynchronize(st));
+    *n_bad = static_cast<int64_t>(h);
+    return CDSP_OK;
+}
+
+// ------------------------------------------------------------------------------- blocks
+cdsp_status cdsp_attention_fwd(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
+                               const cdsp_segments* seg, float softmax_scale, int32_t mode, float* o_acc,
+                               float* lse_acc, cdsp_tensor* out, float* lse, void* cuda_stream) {
+    CDSP_REQUIRE(seg != nullptr, CDSP_ERR_INVALID, "NULL segments");
+    CDSP_CHECK_STATUS(check_tensor(q, "q"));
+    CDSP_CHECK_STATUS(check_tensor(k, "k"));
+    CDSP_CHECK_STATUS(check_tensor(v, "v"));
+    CDSP_REQUIRE(mode >= CDSP_ATTN_ONLY && mode <= CDSP_ATTN_LAST, CDSP_ERR_INVALID, "bad mode %d", mode);
+    CDSP_REQUIRE(q->dtype == k->dtype && k->dtype == v->dtype, CDSP_ERR_DTYPE, "q/k/v dtypes differ");
+    CDSP_REQUIRE(q->D == k->D && k->D == v->D && (q->D == 64 || q->D == 128), CDSP_ERR_SHAPE,
+                 "head dim must match and be 64 or 128");
+    CDSP_REQUIRE(k->H == v->H && q->H % k->H == 0, CDSP_ERR_SHAPE, "Hq %% Hkv != 0");
+    CDSP_REQUIRE(seg->nq == q->T && seg->nkv <= k->T && seg->nkv <= v->T && seg->nkv >= 0, CDSP_ERR_SHAPE,
+                 "segments do not match tensor rows");
+    CDSP_REQUIRE(seg->q_len0 >= 0 && seg->q_len0 <= seg->nq && seg->kv_hist >= 0 && seg->kv_len0 >= 0 &&
+                     seg->kv_hist + seg->kv_len0 <= seg->nkv,
+                 CDSP_ERR_SHAPE, "inconsistent segments");
+    const bool final_out = mode == CDSP_ATTN_ONLY || mode == CDSP_ATTN_LAST;
+    if (final_out) {
+        CDSP_CHECK_STATUS(check_tensor(out, "out"));
+        CDSP_REQUIRE(out->dtype == q->dtype && out->T == q->T && out->H == q->H && out->D == q->D, CDSP_ERR_SHAPE,
+                     "out must match q");
+    }
+    CDSP_REQUIRE(mode == CDSP_ATTN_ONLY || (o_acc && lse_acc) || q->T == 0, CDSP_ERR_INVALID,
+                 "accumulator buffers required for mode %d", mode);
+    const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf(static_cast<float>(q->D));
+    return run_attention(q->ptr, k->ptr, v->ptr, q->dtype, static_cast<int>(q->H), static_cast<int>(k->H),
+                         static_cast<int>(q->D), *seg, scale, mode, o_acc, lse_acc, final_out ? out->ptr : nullptr,
+                         lse, static_cast<cudaStream_t>(cuda_stream));
+}
+
+static cdsp_status zigzag_copy(const cdsp_tensor* full, int32_t s, int32_t r, cdsp_tensor* shard, bool gather,
+                               cudaStream_t st) {
+    CDSP_CHECK_STATUS(check_tensor(full, "full"));
+    CDSP_CHECK_STATUS(check_tensor(shard, "shard"));
+    CDSP_REQUIRE(s == 1 || s == 2 || s == 4 || s == 8, CDSP_ERR_PLAN, "s=%d not in {1,2,4,8}", s);
+    CDSP_REQUIRE(r >= 0 && r < s, CDSP_ERR_INVALID, "rank %d not in [0,%d)", r, s);
+    CDSP_REQUIRE(full->dtype == shard->dtype, CDSP_ERR_DTYPE, "dtype mismatch");
+    CDSP_REQUIRE(full->H == shard->H && full->D == shard->D, CDSP_ERR_SHAPE, "H/D mismatch");
+    CDSP_REQUIRE(full->T % (2 * s) == 0, CDSP_ERR_SHAPE, "L=%lld not a multiple of 2s", static_cast<long long>(full->T));
+    const int64_t m = full->T / (2 * s);
+    CDSP_REQUIRE(shard->T == 2 * m, CDSP_ERR_SHAPE, "shard must have 2m=%lld rows", static_cast<long long>(2 * m));
+    const int64_t row_bytes = full->H * full->D * static_cast<int64_t>(dtype_size(full->dtype));
+    RowCopy segs[2];
+    const int64_t f0 = static_cast<int64_t>(r) * m, f1 = static_cast<int64_t>(2 * s - 1 - r) * m;
+    if (gather) {
+        segs[0] = RowCopy{full->ptr, shard->ptr, f0, 0, m};
+        segs[1] = RowCopy{full->ptr, shard->ptr, f1, m, m};
+    } else {
+        segs[0] = RowCopy{shard->ptr, full->ptr, 0, f0, m};
+        segs[1] = RowCopy{shard->ptr, full->ptr, m, f1, m};
+    }
+    return launch_row_copy(segs, 2, row_bytes, st);
+}
+
+cdsp_status cdsp_zigzag_gather(const cdsp_tensor* full, int32_t s, int32_t r, cdsp_tensor* shard, void* cuda_stream) {
+    return zigzag_copy(full, s, r, shard, true, static_cast<cudaStream_t>(cuda_stream));
+}
+
+cdsp_status cdsp_zigzag_scatter(const cdsp_tensor* shard, int32_t s, int32_t r, cdsp_tensor* full,
+                                void* cuda_stream) {
+    return zigzag_copy(full, s, r, const_cast<cdsp_tensor*>(shard), false, static_cast<cudaStream_t>(cuda_stream));
+}
+
+cdsp_status cdsp_zigzag_map_device(int64_t L, int32_t s, int32_t* tok_rank, int32_t* tok_slot, void* cuda_stream) {
+    CDSP_REQUIRE(s == 1 || s == 2 || s == 4 || s == 8, CDSP_ERR_PLAN, "s=%d not in {1,2,4,8}", s);
+    CDSP_REQUIRE(L >= 0 && L % (2 * s) == 0, CDSP_ERR_SHAPE, "L=%lld not a multiple of 2s", static_cast<long long>(L));
+    return launch_zigzag_map(L, s, tok_rank, tok_slot, static_cast<cudaStream_t>(cuda_stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// internal.h — launchers shared between the libcdsp.so translation units (not exported).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "cdsp.h"
+
+namespace cdsp {
+
+// One block-attention launch (see cdsp_attention_fwd in cdsp.h).
+struct AttnArgs {
+    const void* q;
+    const void* k;
+    const void* v;
+    int32_t dtype;
+    int Hq, Hkv, D;
+    cdsp_segments seg;
+    float scale;   // softmax scale sigma
+    int mode;      // cdsp_attn_mode
+    float* o_acc;
+    float* lse_acc;
+    void* out;
+    float* lse;
+};
+
+cdsp_status launch_attention_tc(const AttnArgs& a, cudaStream_t st);    // bf16, tcgen05/TMEM/TMA
+cdsp_status launch_attention_simt(const AttnArgs& a, cudaStream_t st);  // fp32, FFMA
+
+// n-way LSE merge.  parts[i] fp32 [T,H,D], lses[i] fp32 [H,T].
+constexpr int kMaxMerge = 16;
+cdsp_status launch_lse_merge(int n, const float* const* parts, const float* const* lses, int64_t T, int H,
+                             int D, void* out, int32_t out_dtype, float* lse, cudaStream_t st);
+
+// Row-segment copy: dst rows [dst_row0 + i] = src rows [src_row0 + i], i < n_rows, for up to
+// two (src, dst) segment pairs; rows are `row_bytes` long (multiple of 16).
+struct RowCopy {
+    const void* src;
+    void* dst;
+    int64_t src_row0, dst_row0, n_rows;
+};
+cdsp_status launch_row_copy(const RowCopy* segs, int n_segs, int64_t row_bytes, cudaStream_t st);
+
+// Store append: k/v rows + int32 positions (two contiguous position segments).
+struct AppendArgs {
+    const void* k_src;
+    const void* v_src;
+    void* k_dst;
+    void* v_dst;
+    int32_t* pos_dst;
+    int64_t n_rows, row_bytes;
+    int64_t len0, pos0, pos1;  // row i < len0 -> pos0 + i, else pos1 + (i - len0)
+};
+cdsp_status launch_store_append(const AppendArgs& a, cudaStream_t st);
+
+cdsp_status launch_zigzag_map(int64_t L, int s, int32_t* tok_rank, int32_t* tok_slot, cudaStream_t st);
+
+// Paged-KV scatter (R15).
+struct PagedArgs {
+    const void* k;
+    const void* v;
+    int64_t n_tok;
+    int Hkv, D, esize;
+    int64_t len0, pos0, pos1;  // row -> position, as AppendArgs
+    int tp, block_size;
+    int64_t num_blocks, n_table;
+    const int32_t* block_table;
+    void* k_cache[8];
+    void* v_cache[8];
+    unsigned long long* bad_count;
+};
+cdsp_status launch_paged_scatter(const PagedArgs& a, cudaStream_t st);
+
+// Peer barrier: signal every listed peer, wait for each peer's matching signal.
+struct BarrierArgs {
+    int n;
+    unsigned long long* remote[8];  // peer j's flag slot for this instance (peer memory)
+    unsigned long long* local[8];   // this instance's flag slot for peer j
+    unsigned long long target[8];
+    int* err;                       // host-mapped error word
+};
+cdsp_status launch_peer_barrier(const BarrierArgs& a, cudaStream_t st);
+
+}  // namespace cdsp

@@ -1,0 +1,279 @@
+// mem_kernels.cu — the HBM-bound kernels of the path:
+//   K*3 n-way LSE merge (warp per row-head, shuffle-free: lanes own disjoint D slices)
+//   K*4 zigzag gather / scatter and store append (16-byte vectorised row copies)
+//   K*5 zigzag partition map
+//   K*6 paged-KV scatter into decode caches
+//   the peer barrier used by the ring (flags in peer memory over NVLink)
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace cdsp {
+namespace {
+
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ------------------------------------------------------------------ K*3 LSE merge (R3)
+struct MergeParams {
+    int n;
+    const float* parts[kMaxMerge];
+    const float* lses[kMaxMerge];
+    int64_t T;
+    int H, D;
+    void* out;
+    int32_t out_dtype;
+    float* lse;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) lse_merge_kernel(const MergeParams p) {
+    constexpr int PER = D / 32;  // elements per lane (2 or 4)
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t rows = p.T * p.H;
+    if (gw >= rows) return;
+    const int64_t t = gw / p.H;
+    const int h = static_cast<int>(gw % p.H);
+    const size_t li = static_cast<size_t>(h) * p.T + t;
+    float M = -INFINITY;
+    float a[kMaxMerge];
+#pragma unroll
+    for (int i = 0; i < kMaxMerge; ++i) {
+        if (i < p.n) {
+            a[i] = p.lses[i][li];
+            M = fmaxf(M, a[i]);
+        }
+    }
+    float acc[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+    float den = 0.f;
+    if (M != -INFINITY) {
+        const size_t base = static_cast<size_t>(gw) * D + lane * PER;
+#pragma unroll
+        for (int i = 0; i < kMaxMerge; ++i) {
+            if (i < p.n && a[i] != -INFINITY) {
+                const float w = expf(a[i] - M);
+                den += w;
+                if constexpr (PER == 4) {
+                    const float4 x = *reinterpret_cast<const float4*>(p.parts[i] + base);
+                    acc[0] = fmaf(w, x.x, acc[0]);
+                    acc[1] = fmaf(w, x.y, acc[1]);
+                    acc[2] = fmaf(w, x.z, acc[2]);
+                    acc[3] = fmaf(w, x.w, acc[3]);
+                } else {
+                    const float2 x = *reinterpret_cast<const float2*>(p.parts[i] + base);
+                    acc[0] = fmaf(w, x.x, acc[0]);
+                    acc[1] = fmaf(w, x.y, acc[1]);
+                }
+            }
+        }
+    }
+    const float inv = den > 0.f ? 1.0f / den : 0.f;
+    const size_t ob = static_cast<size_t>(gw) * D + lane * PER;
+    if (p.out_dtype == CDSP_F32) {
+        float* o = static_cast<float*>(p.out) + ob;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) o[e] = acc[e] * inv;
+    } else {
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + ob;
+#pragma unroll
+        for (int e = 0; e < PER; e += 2)
+            *reinterpret_cast<__nv_bfloat162*>(o + e) = __floats2bfloat162_rn(acc[e] * inv, acc[e + 1] * inv);
+    }
+    if (p.lse && lane == 0) p.lse[li] = (M == -INFINITY) ? -INFINITY : M + logf(den);
+}
+
+// ------------------------------------------------------------------ K*4 row copies
+struct RowCopyParams {
+    RowCopy seg[2];
+    int n_segs;
+    int64_t row_vec;  // 16-byte vectors per row
+    int64_t total;    // vectors over all segments
+    int64_t seg0_vec;
+};
+
+__global__ void __launch_bounds__(256) row_copy_kernel(const RowCopyParams p) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < p.total; i += stride) {
+        const int s = (i < p.seg0_vec) ? 0 : 1;
+        const int64_t j = s == 0 ? i : i - p.seg0_vec;
+        const int64_t r = j / p.row_vec, c = j % p.row_vec;
+        const void* sp = s ? p.seg[1].src : p.seg[0].src;
+        void* dp = s ? p.seg[1].dst : p.seg[0].dst;
+        const int64_t sr0 = s ? p.seg[1].src_row0 : p.seg[0].src_row0;
+        const int64_t dr0 = s ? p.seg[1].dst_row0 : p.seg[0].dst_row0;
+        const uint4* src = static_cast<const uint4*>(sp) + (sr0 + r) * p.row_vec + c;
+        uint4* dst = static_cast<uint4*>(dp) + (dr0 + r) * p.row_vec + c;
+        *dst = __ldg(src);
+    }
+}
+
+__global__ void __launch_bounds__(256) store_append_kernel(const AppendArgs a) {
+    const int64_t row_vec = a.row_bytes / 16;
+    const int64_t total = a.n_rows * row_vec;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        static_cast<uint4*>(a.k_dst)[i] = __ldg(static_cast<const uint4*>(a.k_src) + i);
+        static_cast<uint4*>(a.v_dst)[i] = __ldg(static_cast<const uint4*>(a.v_src) + i);
+        if (i < a.n_rows) a.pos_dst[i] = static_cast<int32_t>(i < a.len0 ? a.pos0 + i : a.pos1 + (i - a.len0));
+    }
+}
+
+// ------------------------------------------------------------------ K*5 zigzag map
+__global__ void zigzag_map_kernel(int64_t L, int s, int64_t m, int32_t* tok_rank, int32_t* tok_slot) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= L) return;
+    const int64_t shard = t / m, off = t - shard * m;
+    const bool first = shard < s;
+    if (tok_rank) tok_rank[t] = static_cast<int32_t>(first ? shard : 2 * s - 1 - shard);
+    if (tok_slot) tok_slot[t] = static_cast<int32_t>(first ? off : m + off);
+}
+
+// ------------------------------------------------------------------ K*6 paged scatter (R15)
+__global__ void __launch_bounds__(256) paged_scatter_kernel(const PagedArgs a) {
+    const int row_vec = a.D * a.esize / 16;  // 16-byte vectors per head row
+    const int hl = a.Hkv / a.tp;
+    const int64_t per_tensor = a.n_tok * a.Hkv * row_vec;
+    const int64_t total = 2 * per_tensor;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int which = i >= per_tensor;  // 0: K, 1: V
+        const int64_t j = which ? i - per_tensor : i;
+        const int c = static_cast<int>(j % row_vec);
+        const int64_t rh = j / row_vec;
+        const int h = static_cast<int>(rh % a.Hkv);
+        const int64_t tok = rh / a.Hkv;
+        const int64_t pos = tok < a.len0 ? a.pos0 + tok : a.pos1 + (tok - a.len0);
+        const int64_t lb = pos / a.block_size;
+        const int32_t blk = lb < a.n_table ? a.block_table[lb] : -1;
+        if (blk < 0 || blk >= a.num_blocks) {
+            if (c == 0 && which == 0 && h == 0) atomicAdd(a.bad_count, 1ull);
+            continue;
+        }
+        const int t = h / hl;
+        const int hloc = h - t * hl;
+        const uint4* src = static_cast<const uint4*>(which ? a.v : a.k) + rh * row_vec + c;
+        uint4* dst = static_cast<uint4*>(which ? a.v_cache[t] : a.k_cache[t]) +
+                     ((static_cast<int64_t>(blk) * a.block_size + pos % a.block_size) * hl + hloc) * row_vec + c;
+        *dst = __ldg(src);
+    }
+}
+
+// ------------------------------------------------------------------ peer barrier
+__global__ void peer_barrier_kernel(const BarrierArgs a) {
+    const int j = threadIdx.x;
+    if (j >= a.n) return;
+    __threadfence_system();  // this stream's prior writes before the signal
+    atomicAdd_system(a.remote[j], 1ull);
+    const uint64_t t0 = gtimer();
+    while (true) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.local[j]) : "memory");
+        if (v >= a.target[j]) break;
+        if (gtimer() - t0 > 8000000000ull) {  // 8 s: a peer never arrived
+            atomicExch(a.err, 1);
+            break;
+        }
+        __nanosleep(64);
+    }
+    __threadfence_system();
+}
+
+unsigned grid_for(int64_t work, int per_block = 256) {
+    int64_t b = (work + per_block - 1) / per_block;
+    const int64_t cap = 148 * 16;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return static_cast<unsigned>(b);
+}
+
+}  // namespace
+
+cdsp_status launch_lse_merge(int n, const float* const* parts, const float* const* lses, int64_t T, int H, int D,
+                             void* out, int32_t out_dtype, float* lse, cudaStream_t st) {
+    CDSP_REQUIRE(n >= 1 && n <= kMaxMerge, CDSP_ERR_INVALID, "merge count %d not in [1,%d]", n, kMaxMerge);
+    MergeParams p;
+    p.n = n;
+    for (int i = 0; i < kMaxMerge; ++i) {
+        p.parts[i] = i < n ? parts[i] : nullptr;
+        p.lses[i] = i < n ? lses[i] : nullptr;
+    }
+    p.T = T;
+    p.H = H;
+    p.D = D;
+    p.out = out;
+    p.out_dtype = out_dtype;
+    p.lse = lse;
+    const int64_t warps = T * H;
+    if (warps == 0) return CDSP_OK;
+    const int64_t blocks = (warps * 32 + 255) / 256;
+    CDSP_REQUIRE(blocks < (1ll << 31), CDSP_ERR_SHAPE, "merge too large");
+    if (D == 128)
+        lse_merge_kernel<128><<<static_cast<unsigned>(blocks), 256, 0, st>>>(p);
+    else if (D == 64)
+        lse_merge_kernel<64><<<static_cast<unsigned>(blocks), 256, 0, st>>>(p);
+    else
+        CDSP_FAIL(CDSP_ERR_SHAPE, "head dim %d not supported", D);
+    CDSP_CUDA(cudaGetLastError());
+    return CDSP_OK;
+}
+
+cdsp_status launch_row_copy(const RowCopy* segs, int n_segs, int64_t row_bytes, cudaStream_t st) {
+    CDSP_REQUIRE(n_segs >= 1 && n_segs <= 2, CDSP_ERR_INVALID, "row copy: 1 or 2 segments");
+    CDSP_REQUIRE(row_bytes % 16 == 0, CDSP_ERR_SHAPE, "row bytes %lld not a multiple of 16",
+                 static_cast<long long>(row_bytes));
+    RowCopyParams p;
+    p.n_segs = n_segs;
+    p.row_vec = row_bytes / 16;
+    p.seg[0] = segs[0];
+    p.seg[1] = n_segs > 1 ? segs[1] : RowCopy{nullptr, nullptr, 0, 0, 0};
+    p.seg0_vec = segs[0].n_rows * p.row_vec;
+    p.total = p.seg0_vec + (n_segs > 1 ? segs[1].n_rows * p.row_vec : 0);
+    if (p.total == 0) return CDSP_OK;
+    row_copy_kernel<<<grid_for(p.total), 256, 0, st>>>(p);
+    CDSP_CUDA(cudaGetLastError());
+    return CDSP_OK;
+}
+
+cdsp_status launch_store_append(const AppendArgs& a, cudaStream_t st) {
+    CDSP_REQUIRE(a.row_bytes % 16 == 0, CDSP_ERR_SHAPE, "row bytes not a multiple of 16");
+    const int64_t work = a.n_rows * (a.row_bytes / 16);
+    if (a.n_rows == 0) return CDSP_OK;
+    store_append_kernel<<<grid_for(work > a.n_rows ? work : a.n_rows), 256, 0, st>>>(a);
+    CDSP_CUDA(cudaGetLastError());
+    return CDSP_OK;
+}
+
+cdsp_status launch_zigzag_map(int64_t L, int s, int32_t* tok_rank, int32_t* tok_slot, cudaStream_t st) {
+    if (L == 0) return CDSP_OK;
+    const int64_t m = L / (2 * s);
+    const int64_t blocks = (L + 255) / 256;
+    zigzag_map_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(L, s, m, tok_rank, tok_slot);
+    CDSP_CUDA(cudaGetLastError());
+    return CDSP_OK;
+}
+
+cdsp_status launch_paged_scatter(const PagedArgs& a, cudaStream_t st) {
+    CDSP_REQUIRE((a.D * a.esize) % 16 == 0, CDSP_ERR_SHAPE, "head row not a multiple of 16 bytes");
+    const int64_t work = 2 * a.n_tok * a.Hkv * (a.D * a.esize / 16);
+    if (work == 0) return CDSP_OK;
+    paged_scatter_kernel<<<grid_for(work), 256, 0, st>>>(a);
+    CDSP_CUDA(cudaGetLastError());
+    return CDSP_OK;
+}
+
+cdsp_status launch_peer_barrier(const BarrierArgs& a, cudaStream_t st) {
+    if (a.n == 0) return CDSP_OK;
+    peer_barrier_kernel<<<1, 32, 0, st>>>(a);
+    CDSP_CUDA(cudaGetLastError());
+    return CDSP_OK;
+}
+
+}  // namespace cdsp

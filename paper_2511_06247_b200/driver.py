@@ -1,0 +1,126 @@
+"""Drivers that run a whole CDSP plan through the C ABI.
+
+``run_plan_loopback``: every instance of the plan is a virtual rank on THIS GPU, each with
+its own communicator and stream (cdsp_comm_connect_local).  The library calls only enqueue
+work, so one host thread issues all ranks' calls in turn; the device-side peer barriers and
+copy-engine pulls are the same code the multi-process path runs over NVLink.
+
+``run_plan_distributed``: one process per GPU (torch.distributed for the IPC handle
+exchange only); this process executes the chunks whose group contains its rank.
+
+Input sharding (cdsp_zigzag_gather) and output reassembly (cdsp_zigzag_scatter) use the
+library's kernels; the LSE reassembly for tests is harness code (index_copy).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import api
+
+
+def _rank_lse_index(plan: api.Plan, c: int, r: int, device) -> torch.Tensor:
+    _, _, rank_pos, _ = api.plan_partition(plan, c)
+    return torch.as_tensor(rank_pos[r], device=device)
+
+
+def make_loopback_comms(plan: api.Plan, Hkv: int, D: int, dtype, device: int = 0, cap: Optional[int] = None):
+    world = max(r for _, ranks in plan.chunks for r in ranks) + 1
+    cap = cap or api.plan_capacity(plan)
+    comms = [api.Comm(i, world, device, cap, Hkv, D, dtype) for i in range(world)]
+    if world > 1:
+        api.connect_local(comms)
+    return comms
+
+
+def run_plan_loopback(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: api.Plan,
+                      softmax_scale: float = 0.0, comms: Optional[List[api.Comm]] = None,
+                      streams: Optional[Sequence[torch.cuda.Stream]] = None, want_lse: bool = True,
+                      shards=None, out_shards=None):
+    """Full-prompt q [N,Hq,D], k/v [N,Hkv,D] on one device -> (out [N,Hq,D], lse [Hq,N] or None).
+
+    ``shards`` (optional, reused across calls): per chunk, per ring rank, (q, k, v) shards
+    prepared by :func:`prepare_shards`."""
+    device = q.device
+    N, Hq, D = q.shape
+    Hkv = k.shape[1]
+    assert sum(L for L, _ in plan.chunks) == N, "plan does not cover the prompt"
+    if comms is None:
+        comms = make_loopback_comms(plan, Hkv, D, q.dtype, device.index or 0)
+    world = len(comms)
+    if streams is None:
+        streams = [torch.cuda.Stream(device=device) for _ in range(world)]
+    cur = torch.cuda.current_stream(device)
+    for s in streams:
+        s.wait_stream(cur)
+    for cm in comms:
+        cm.reset(cur)
+    if shards is None:
+        shards = prepare_shards(q, k, v, plan, streams=None)
+        for s in streams:
+            s.wait_stream(cur)
+    out = torch.empty_like(q)
+    lse = torch.empty((Hq, N), dtype=torch.float32, device=device) if want_lse else None
+    outs = out_shards if out_shards is not None else alloc_out_shards(plan, Hq, D, q.dtype, device, want_lse)
+    for c, (L, ranks) in enumerate(plan.chunks):
+        C = plan.chunk_start(c)
+        for r, inst in enumerate(ranks):
+            qs, ks, vs = shards[c][r]
+            o_r, l_r = outs[c][r]
+            api.prefill_chunk(qs, ks, vs, comms[inst].kvstore(), api.SpGroup(comms[inst], plan, c),
+                              softmax_scale, o_r, l_r, stream=streams[inst])
+        for r, inst in enumerate(ranks):
+            with torch.cuda.stream(streams[inst]):
+                o_r, l_r = outs[c][r]
+                api.zigzag_scatter(o_r, len(ranks), r, out[C:C + L], stream=streams[inst])
+                if want_lse:
+                    idx = _rank_lse_index(plan, c, r, device)
+                    lse.index_copy_(1, idx, l_r)
+    for s in streams:
+        cur.wait_stream(s)
+    for cm in comms:
+        cm.check()
+    return out, lse
+
+
+def prepare_shards(q, k, v, plan: api.Plan, streams=None):
+    """Per chunk, per ring rank: (q, k, v) zigzag shards (cdsp_zigzag_gather)."""
+    shards = []
+    for c, (L, ranks) in enumerate(plan.chunks):
+        C = plan.chunk_start(c)
+        s = len(ranks)
+        per = []
+        for r in range(s):
+            per.append((api.zigzag_gather(q[C:C + L], s, r), api.zigzag_gather(k[C:C + L], s, r),
+                        api.zigzag_gather(v[C:C + L], s, r)))
+        shards.append(per)
+    return shards
+
+
+def alloc_out_shards(plan: api.Plan, Hq: int, D: int, dtype, device, want_lse=True):
+    outs = []
+    for L, ranks in plan.chunks:
+        m2 = L // len(ranks)
+        outs.append([(torch.empty((m2, Hq, D), dtype=dtype, device=device),
+                      torch.empty((Hq, m2), dtype=torch.float32, device=device) if want_lse else None)
+                     for _ in ranks])
+    return outs
+
+
+def run_plan_distributed(q_shards, k_shards, v_shards, plan: api.Plan, comm: api.Comm, softmax_scale=0.0,
+                         out_shards=None, lse_shards=None, stream=None):
+    """Execute, on this process's instance, every chunk whose group contains it.
+    *_shards[c] = this rank's zigzag shard of chunk c (or None if not in the group)."""
+    comm.reset(stream)
+    outs = []
+    for c, (L, ranks) in enumerate(plan.chunks):
+        if comm.rank not in ranks:
+            outs.append(None)
+            continue
+        o = out_shards[c] if out_shards is not None else torch.empty_like(q_shards[c])
+        l = lse_shards[c] if lse_shards is not None else None
+        api.prefill_chunk(q_shards[c], k_shards[c], v_shards[c], comm.kvstore(), api.SpGroup(comm, plan, c),
+                          softmax_scale, o, l, stream=stream)
+        outs.append(o)
+    return outs

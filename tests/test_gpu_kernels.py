@@ -1,0 +1,191 @@
+"""GPU parity of the individual kernels (through the C ABI) against the CPU oracle.
+
+Tolerances (north_star): attention out max-abs 2e-2 (bf16 path) / 1e-4 (fp32 path), LSE
+1e-3; partition maps and KV layout bit-exact."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from cdsp_inputs import qkv, sample_rows
+from paper_2511_06247_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.bfloat16: 2e-2, torch.float32: 1e-4}
+LSE_TOL = 1e-3
+
+
+def _np(x):
+    return x.detach().float().cpu().numpy()
+
+
+def _check(out, lse, o_ref, l_ref, dtype, what=""):
+    err = np.abs(_np(out).astype(np.float64) - o_ref).max() if o_ref.size else 0.0
+    lerr = np.abs(_np(lse).astype(np.float64) - l_ref)
+    lerr = lerr[np.isfinite(l_ref)].max() if np.isfinite(l_ref).any() else 0.0
+    assert np.array_equal(np.isfinite(_np(lse)), np.isfinite(l_ref)), f"{what}: -inf pattern differs"
+    assert err <= TOL[dtype], f"{what}: out max-abs {err:.3e} > {TOL[dtype]}"
+    assert lerr <= LSE_TOL, f"{what}: lse max-abs {lerr:.3e}"
+    return err, lerr
+
+
+CASES = [
+    (1, 2, 2, 64, torch.bfloat16), (77, 2, 2, 128, torch.bfloat16), (128, 4, 4, 128, torch.bfloat16),
+    (300, 4, 1, 128, torch.bfloat16), (513, 8, 2, 64, torch.bfloat16), (1000, 2, 2, 128, torch.bfloat16),
+    (1, 2, 1, 64, torch.float32), (100, 4, 4, 64, torch.float32), (257, 2, 1, 128, torch.float32),
+    (700, 3, 3, 64, torch.bfloat16),
+]
+
+
+@pytest.mark.parametrize("N,Hq,Hkv,D,dtype", CASES)
+@pytest.mark.parametrize("sharp", [False, True])
+def test_causal_attention_all_rows(N, Hq, Hkv, D, dtype, sharp):
+    q, k, v = qkv(N, Hq, Hkv, D, dtype, seed=N + D, sharp=sharp)
+    scale = 1.0 / math.sqrt(D)
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    out = torch.empty_like(qd)
+    lse = torch.empty((Hq, N), dtype=torch.float32, device="cuda")
+    api.attention_fwd(qd, kd, vd, api.causal_segments(N, N), scale, api.ATTN_ONLY, out=out, lse=lse)
+    torch.cuda.synchronize()
+    o_ref, l_ref = oracle.causal_rows(q.float().numpy(), k.float().numpy(), v.float().numpy(), scale)
+    _check(out, lse, o_ref, l_ref, dtype, f"N={N} Hq={Hq} Hkv={Hkv} D={D} {dtype}")
+
+
+def _zigzag_block_case(s, r, src, m, h, Hq, Hkv, D, dtype, C=1000, seed=0):
+    """Q = rank r's shard of a chunk at C; KV = src's history (h rows) + src's shard."""
+    L = 2 * s * m
+    q, k, v = qkv(L, Hq, Hkv, D, dtype, seed=seed)
+    hk, hv = qkv(max(h, 1), Hkv, Hkv, D, dtype, seed=seed + 50)[1:]
+    hk, hv = hk[:h], hv[:h]
+    pos = oracle.rank_positions(L, s, C)
+    qs, ks, vs = q[pos[r] - C], k[pos[src] - C], v[pos[src] - C]
+    kk = torch.cat([hk, ks]).contiguous()
+    vv = torch.cat([hv, vs]).contiguous()
+    kpos = np.concatenate([np.arange(h) + C - h - 7, pos[src]])
+    seg = api.segments(2 * m, m, C + r * m, C + (2 * s - 1 - r) * m, h + 2 * m, h, m, C + src * m,
+                       C + (2 * s - 1 - src) * m)
+    return qs.contiguous(), kk, vv, pos[r], kpos, seg
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("s,r,src,m,h", [(2, 0, 0, 64, 0), (2, 1, 0, 96, 50), (4, 1, 3, 130, 257),
+                                         (8, 5, 2, 128, 384), (8, 2, 6, 40, 1), (4, 3, 3, 200, 130)])
+def test_block_with_history_and_zigzag_segments(dtype, s, r, src, m, h):
+    Hq, Hkv, D = (4, 2, 128) if dtype == torch.bfloat16 else (2, 2, 64)
+    qs, kk, vv, qpos, kpos, seg = _zigzag_block_case(s, r, src, m, h, Hq, Hkv, D, dtype, seed=s * 10 + r)
+    scale = 1.0 / math.sqrt(D)
+    out = torch.empty_like(qs).cuda()
+    lse = torch.empty((Hq, 2 * m), dtype=torch.float32, device="cuda")
+    api.attention_fwd(qs.cuda(), kk.cuda(), vv.cuda(), seg, scale, api.ATTN_ONLY, out=out, lse=lse)
+    torch.cuda.synchronize()
+    o_ref, l_ref = oracle.attention(qs.float().numpy(), qpos, kk.float().numpy(), vv.float().numpy(), kpos, scale)
+    _check(out, lse, o_ref, l_ref, dtype, f"s={s} r={r} src={src} m={m} h={h}")
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_merge_modes_chain_equals_single_block(dtype):
+    """FIRST / MID / LAST over three KV blocks == ONLY over their union (R3 in the epilogue)."""
+    N, Hq, Hkv, D = 640, 4, 4, 128 if dtype == torch.bfloat16 else 64
+    q, k, v = (t.cuda() for t in qkv(N, Hq, Hkv, D, dtype, seed=3))
+    scale = 1.0 / math.sqrt(D)
+    cuts = [0, 200, 300, N]
+    o_acc = torch.empty((N, Hq, D), dtype=torch.float32, device="cuda")
+    l_acc = torch.empty((Hq, N), dtype=torch.float32, device="cuda")
+    out = torch.empty_like(q)
+    lse = torch.empty((Hq, N), dtype=torch.float32, device="cuda")
+    modes = [api.ATTN_FIRST, api.ATTN_MID, api.ATTN_LAST]
+    for (a, b), mode in zip(zip(cuts[:-1], cuts[1:]), modes):
+        seg = api.segments(N, N, 0, 0, b - a, 0, b - a, a, 0)
+        api.attention_fwd(q, k[a:b].contiguous(), v[a:b].contiguous(), seg, scale, mode, o_acc, l_acc, out, lse)
+    torch.cuda.synchronize()
+    o_ref, l_ref = oracle.causal_rows(_np(q), _np(k), _np(v), scale)
+    _check(out, lse, o_ref, l_ref, dtype, "merge chain")
+
+
+def test_fully_masked_block_is_identity():
+    """A block invisible to every query (src > r, first half) leaves the accumulator exact."""
+    m, Hq, D = 128, 2, 128
+    q = torch.randn(2 * m, Hq, D, device="cuda").to(torch.bfloat16)
+    k = torch.randn(2 * m, Hq, D, device="cuda").to(torch.bfloat16)
+    o_acc = torch.randn(2 * m, Hq, D, device="cuda")
+    l_acc = torch.randn(Hq, 2 * m, device="cuda")
+    o0, l0 = o_acc.clone(), l_acc.clone()
+    seg = api.segments(2 * m, 2 * m, 0, 0, 2 * m, 0, 2 * m, 10000, 10000)  # keys all in the future
+    api.attention_fwd(q, k, k, seg, 0.1, api.ATTN_MID, o_acc, l_acc)
+    torch.cuda.synchronize()
+    assert torch.equal(l_acc, l0)
+    assert (o_acc - o0).abs().max().item() <= 1e-6
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 8])
+@pytest.mark.parametrize("D", [64, 128])
+def test_lse_merge_kernel(n, D):
+    T, H = 333, 3
+    g = torch.Generator().manual_seed(n * D)
+    parts = [torch.randn(T, H, D, generator=g) for _ in range(n)]
+    lses = [torch.randn(H, T, generator=g) * 4 for _ in range(n)]
+    lses[0][0, :10] = float("-inf")
+    if n > 1:
+        for l in lses:
+            l[1, 5] = float("-inf")  # a row with every part empty
+    out = torch.empty(T, H, D, device="cuda")
+    lse = torch.empty(H, T, device="cuda")
+    api.lse_merge([p.cuda() for p in parts], [l.cuda() for l in lses], out, lse)
+    outb = torch.empty(T, H, D, device="cuda", dtype=torch.bfloat16)
+    api.lse_merge([p.cuda() for p in parts], [l.cuda() for l in lses], outb)
+    torch.cuda.synchronize()
+    o_ref, l_ref = oracle.lse_merge([p.double().numpy() for p in parts], [l.double().numpy() for l in lses])
+    assert np.abs(_np(out) - o_ref).max() <= 1e-5
+    fin = np.isfinite(l_ref)
+    assert np.array_equal(np.isfinite(_np(lse)), fin)
+    assert np.abs(_np(lse)[fin] - l_ref[fin]).max() <= 1e-5
+    assert not np.isnan(_np(out)).any()
+    assert np.abs(_np(outb) - o_ref).max() <= 2e-2
+
+
+@pytest.mark.parametrize("s", [1, 2, 4, 8])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_zigzag_gather_scatter_bit_exact(s, dtype):
+    L, H, D = 2 * s * 37, 3, 64
+    full = torch.randn(L, H, D, device="cuda").to(dtype)
+    tr, ts = oracle.zigzag_map(L, s)
+    back = torch.zeros_like(full)
+    for r in range(s):
+        sh = api.zigzag_gather(full, s, r)
+        idx = np.nonzero(tr == r)[0]
+        expect = torch.empty_like(sh)
+        expect[torch.as_tensor(ts[idx], device="cuda").long()] = full[torch.as_tensor(idx, device="cuda")]
+        assert torch.equal(sh, expect)
+        api.zigzag_scatter(sh, s, r, back)
+    torch.cuda.synchronize()
+    assert torch.equal(back, full)
+
+
+@pytest.mark.parametrize("s", [1, 2, 4, 8])
+def test_device_zigzag_map_bit_exact(s):
+    L = 2 * s * 1000
+    tr, ts = api.zigzag_map_device(L, s)
+    otr, ots = oracle.zigzag_map(L, s)
+    assert np.array_equal(tr.cpu().numpy(), otr) and np.array_equal(ts.cpu().numpy(), ots)
+
+
+def test_bench_config_sampled_rows():
+    """BASELINE configs[1] shape (7B MHA, 32 heads, d=128, 32K) at SP=1 through
+    cdsp_prefill_chunk, the launch the bench times; sampled rows incl. tile edges."""
+    N, Hq, Hkv, D = 32768, 32, 32, 128
+    q, k, v = qkv(N, Hq, Hkv, D, torch.bfloat16, seed=0)
+    plan = api.Plan([(N, [0])])
+    comm = api.Comm(0, 1, 0, N, Hkv, D, torch.bfloat16)
+    out = torch.empty(N, Hq, D, dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty(Hq, N, dtype=torch.float32, device="cuda")
+    api.prefill_chunk(q.cuda(), k.cuda(), v.cuda(), comm.kvstore(), api.SpGroup(comm, plan, 0), 0.0, out, lse)
+    torch.cuda.synchronize()
+    rows = sample_rows(N, 48, seed=1, edges=[0, 1, 127, 128, 255, 256, 16383, 16384, N - 129, N - 1]).numpy()
+    o_ref, l_ref = oracle.causal_rows(q.float().numpy(), k.float().numpy(), v.float().numpy(),
+                                      1.0 / math.sqrt(D), rows=rows)
+    _check(out[torch.as_tensor(rows, device="cuda")], lse[:, torch.as_tensor(rows, device="cuda")], o_ref, l_ref,
+           torch.bfloat16, "32K sampled")
+    comm.close()
