@@ -217,6 +217,8 @@ def main():
     m2 = L // s
     comm = api.Comm(rank, world, local, api.plan_capacity(plan), Hkv, D, torch.bfloat16)
     if world > 1:
+        from paper_2511_06247_b200 import dist_utils
+        dist_utils.check_plan_consistent(plan.chunks)
         comm.connect_process_group()
     qs = torch.empty((m2, Hq, D), dtype=torch.bfloat16, device=dev)
     ks = torch.empty((m2, Hkv, D), dtype=torch.bfloat16, device=dev)

@@ -245,11 +245,8 @@ class Comm:
 
     def connect_process_group(self, group=None):
         """Exchange IPC handles over torch.distributed (plumbing) and open the peers."""
-        import torch.distributed as dist
-        mine = self.ipc_handle()
-        allh = [None] * dist.get_world_size(group)
-        dist.all_gather_object(allh, mine, group=group)
-        self.connect(allh)
+        from .dist_utils import exchange_bytes
+        self.connect(exchange_bytes(self.ipc_handle(), group))
 
     def check(self):
         _check(lib().cdsp_comm_check(self.h))

@@ -42,6 +42,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
+        if os.environ.get("CDSP_KTRACE"):
+            cmd.insert(1, "-DCDSP_KTRACE")
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     failed = []
