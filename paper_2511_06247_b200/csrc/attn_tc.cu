@@ -41,6 +41,10 @@
 #include "internal.h"
 #include "ptx.cuh"
 
+#ifndef CDSP_EMU_MASK
+#define CDSP_EMU_MASK 0x52
+#endif
+
 namespace cdsp {
 using namespace ptx;
 
@@ -427,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 16; ++i) {
                 const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc, nm);
                 float2 pp;
-                if ((0x52 >> (i % 8)) & 1) {  // 3/8 of the exponentials on the FMA pipe (pairs 1, 4, 6 of 8)
+                if ((CDSP_EMU_MASK >> (i % 8)) & 1) {  // pairs on the FMA pipe (default 3/8: pairs 1, 4, 6 of 8)
                     pp = ex2_fma2(x);
                 } else {
                     pp.x = ex2(x.x);

@@ -59,20 +59,20 @@ def analyze_ctas(path, n_cta):
 def analyze_iters(path):
     raw = np.fromfile(path, dtype=np.uint64)
     t = raw[65536 * 8:].reshape(4, 512, 16).astype(np.int64)
-    names = {0: "w4 S", 1: "w4 bar", 2: "w4 exp", 3: "w4 P", 4: "w19 S", 5: "w19 P", 8: "preQK", 9: "postQK",
-             10: "prePV", 11: "postPV"}
+    names = {0: "t0 S", 1: "t0 bar", 2: "t0 P", 4: "t1 S", 5: "t1 P", 8: "t0 prePV", 9: "t0 postQK"}
     d = t[0]
     base = d[0, 0]
     print("it  " + " ".join(f"{names[k]:>8}" for k in names))
     for it in range(0, 14):
         print(f"{it:3d} " + " ".join(f"{(d[it, k] - base) if d[it, k] else -1:8d}" for k in names))
     x = d[8:200]
-    print("period (w4 S->S)", np.median(np.diff(x[:, 0])))
-    for nm, a_, b_ in (("w4 S->bar", 0, 1), ("w4 bar->exp", 1, 2), ("w4 exp->P", 2, 3), ("w19 S->P", 4, 5),
-                       ("w4 P->prePV", 3, 10), ("w19 P->prePV", 5, 10), ("prePV->postPV", 10, 11),
-                       ("preQK->postQK", 8, 9)):
+    print("period (t0 S->S)", np.median(np.diff(x[:, 0])), " t1:", np.median(np.diff(x[:, 4])))
+    for nm, a_, b_ in (("t0 S->bar", 0, 1), ("t0 bar->P", 1, 2), ("t1 S->P", 4, 5), ("t0 P->prePV", 2, 8),
+                       ("t0 prePV->postQK", 8, 9)):
         v = x[:, b_] - x[:, a_]
         print(f"{nm:16s} median {np.median(v):7.0f} p90 {np.percentile(v, 90):7.0f}")
+    v = d[9:201, 0] - x[:, 9]
+    print(f"t0 postQK->S(next) median {np.median(v):7.0f}")
 
 
 def analyze(path):
