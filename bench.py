@@ -203,11 +203,19 @@ def main():
     from cdsp_inputs import block_table, qkv
     from paper_2511_06247_b200 import api
 
+    # CDSP_BENCH_DEVICE pins every rank to one device (functional test of the N>1 path on a
+    # 1-GPU box; ranks then time-share the GPU, so such numbers are not performance data)
+    shared = os.environ.get("CDSP_BENCH_DEVICE")
+    if shared is not None:
+        local = int(shared)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if shared is not None:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.current_stream(dev)
 
@@ -216,8 +224,8 @@ def main():
     plan = api.Plan([(L, list(range(s)))])
     m2 = L // s
     comm = api.Comm(rank, world, local, api.plan_capacity(plan), Hkv, D, torch.bfloat16)
+    from paper_2511_06247_b200 import dist_utils
     if world > 1:
-        from paper_2511_06247_b200 import dist_utils
         dist_utils.check_plan_consistent(plan.chunks)
         comm.connect_process_group()
     qs = torch.empty((m2, Hq, D), dtype=torch.bfloat16, device=dev)
@@ -271,9 +279,8 @@ def main():
     comm.profile(False)
     comm.check()
     if dist is not None:
-        t = torch.tensor([ms, attn_ms / max(attn_n, 1)], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, attn_avg = t.tolist()
+        ms, attn_avg = dist_utils.max_over_ranks([ms, attn_ms / max(attn_n, 1)],
+                                                 device=None if shared is not None else dev)
     else:
         attn_avg = attn_ms / max(attn_n, 1)
     ms_step = ms / args.steps
@@ -308,9 +315,7 @@ def main():
         barrier()
         ems = a0.elapsed_time(a1) / n_e2e
         if dist is not None:
-            t = torch.tensor([ems], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = t.item()
+            ems = dist_utils.max_over_ranks([ems], device=None if shared is not None else dev)[0]
         e2e = {"value": flops / (ems * 1e-3) / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems}
 

@@ -89,3 +89,22 @@ def test_two_processes_ipc_ring_matches_oracle():
             idx = np.searchsorted(pos, sel) if np.all(np.diff(pos) > 0) else np.array([list(pos).index(x) for x in sel])
             assert np.abs(o[idx] - o_ref).max() <= 2e-2
             assert np.abs(lse[:, idx] - l_ref).max() <= 1e-3
+
+
+def test_bench_torchrun_two_ranks_one_gpu():
+    """bench.py's N>1 path (torchrun, IPC ring, max-over-ranks timing) runs end to end and
+    prints one JSON line from rank 0 (both ranks pinned to GPU 0: functional check only)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CDSP_BENCH_DEVICE="0", CUDA_DEVICE_MAX_CONNECTIONS="32")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "1", "--seq", "4096", "--no-e2e"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["sp"] == 2 and d["value"] > 0
