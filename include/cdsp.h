@@ -119,8 +119,10 @@ CDSP_API cdsp_status cdsp_comm_ipc_handle(cdsp_comm c, void* handle_out);
 CDSP_API cdsp_status cdsp_comm_connect(cdsp_comm c, const void* handles);
 
 /* Loopback: `world` communicators created in THIS process on ONE device (comms[i] has
- * rank i) are linked to each other.  Every virtual rank must then be driven on its own
- * stream; calls only enqueue, so one host thread can issue them one after the other. */
+ * rank i) are linked into a group.  cdsp_prefill_chunk then acts as a deferred collective
+ * (like an NCCL group call): each ring rank's call is validated and recorded, and the call
+ * that completes the chunk's group enqueues every rank's work on the ranks' own streams,
+ * ordered by CUDA events (no device-side spinning).  One host thread issues all calls. */
 CDSP_API cdsp_status cdsp_comm_connect_local(cdsp_comm* comms, int32_t world);
 
 /* Poll for asynchronous errors (peer-barrier timeout -> CDSP_ERR_COMM).  Does not block. */

@@ -54,6 +54,26 @@ struct PeerView {
     int32_t* pos = nullptr;
     unsigned long long* flags = nullptr;
 };
+
+// Loopback groups (cdsp_comm_connect_local): every instance lives in this process; a chunk's
+// cdsp_prefill_chunk calls are collected and issued together, ordered by CUDA events.
+struct PendingCall {
+    cdsp_tensor q, k, v, out;
+    float* lse;
+    cdsp_kvstore* prev_kv;
+    float scale;
+    cudaStream_t st;
+    bool set;
+};
+struct LocalGroup {
+    int world = 0;
+    cdsp_comm comms[kMaxWorld] = {};
+    PendingCall calls[kMaxWorld] = {};
+    int pending = 0;
+    const cdsp_plan* plan = nullptr;
+    int chunk = -1;
+    int refs = 0;
+};
 }  // namespace
 
 struct cdsp_comm_s {
@@ -88,6 +108,10 @@ struct cdsp_comm_s {
     bool profiling = false;
     std::vector<cudaEvent_t> prof_ev;  // pairs
     int prof_n = 0;
+    // loopback group and its ordering events
+    LocalGroup* lg = nullptr;
+    cudaEvent_t ev_bal = nullptr, ev_app = nullptr, ev_fin = nullptr;
+    bool fin_recorded = false;
 };
 
 namespace {
@@ -168,6 +192,134 @@ cdsp_status run_attention_timed(cdsp_comm c, const void* q, const void* k, const
     return CDSP_OK;
 }
 
+// Segments of ring rank r's query shard against src's block (history + src's shard).
+cdsp_segments segments_for(const ChunkInfo& ci, int r, int src) {
+    cdsp_segments sgm;
+    sgm.nq = 2 * ci.m;
+    sgm.q_len0 = ci.m;
+    sgm.q_pos0 = shard_pos0(ci, r);
+    sgm.q_pos1 = shard_pos1(ci, r);
+    sgm.nkv = ci.hist[src] + 2 * ci.m;
+    sgm.kv_hist = ci.hist[src];
+    sgm.kv_len0 = ci.m;
+    sgm.kv_pos0 = shard_pos0(ci, src);
+    sgm.kv_pos1 = shard_pos1(ci, src);
+    return sgm;
+}
+
+// Cache balancing (R8): a ring rank new to the group pulls its part of an old rank's
+// store (copy engines, NVLink when the peer is another GPU).
+cdsp_status phase_balance(cdsp_comm c, const ChunkInfo& ci, int r, cudaStream_t st) {
+    for (int i = 0; i < ci.n_moves; ++i) {
+        const cdsp_move& mv = ci.moves[i];
+        if (mv.dst != r || mv.n_tok == 0) continue;
+        const PeerView& src = c->peers[ci.ranks[mv.src]];
+        CDSP_CUDA(cudaMemcpyAsync(c->self.k, src.k + mv.src_off * c->row_bytes, mv.n_tok * c->row_bytes,
+                                  cudaMemcpyDeviceToDevice, st));
+        CDSP_CUDA(cudaMemcpyAsync(c->self.v, src.v + mv.src_off * c->row_bytes, mv.n_tok * c->row_bytes,
+                                  cudaMemcpyDeviceToDevice, st));
+        CDSP_CUDA(cudaMemcpyAsync(c->self.pos, src.pos + mv.src_off, mv.n_tok * sizeof(int32_t),
+                                  cudaMemcpyDeviceToDevice, st));
+    }
+    return CDSP_OK;
+}
+
+// Append this rank's shard (k, v and global positions) after its balanced history.
+cdsp_status phase_append(cdsp_comm c, const ChunkInfo& ci, int r, const cdsp_tensor* k, const cdsp_tensor* v,
+                         cudaStream_t st) {
+    c->n = ci.hist[r];
+    AppendArgs a;
+    a.k_src = k->ptr;
+    a.v_src = v->ptr;
+    a.k_dst = c->self.k + c->n * c->row_bytes;
+    a.v_dst = c->self.v + c->n * c->row_bytes;
+    a.pos_dst = c->self.pos + c->n;
+    a.n_rows = 2 * ci.m;
+    a.row_bytes = static_cast<int64_t>(c->row_bytes);
+    a.len0 = ci.m;
+    a.pos0 = shard_pos0(ci, r);
+    a.pos1 = shard_pos1(ci, r);
+    CDSP_CHECK_STATUS(launch_store_append(a, st));
+    c->n += 2 * ci.m;
+    return CDSP_OK;
+}
+
+// The ring (R10, R11): step k attends to src = (r - k) mod s's whole store; steps >= 1
+// read it through a copy-engine pull on the comm stream into receive buffer k & 1, overlapped
+// with step k-1.  g != NULL (loopback): each pull waits for src's append event.
+cdsp_status phase_ring(cdsp_comm c, const ChunkInfo& ci, int r, const void* q, int Hq, void* out, float* lse,
+                       float scale, cudaStream_t st, LocalGroup* g) {
+    const int64_t m2 = 2 * ci.m;
+    CDSP_CUDA(cudaEventRecord(c->ev_ready, st));  // recv buffers are free after st's earlier work
+    CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+    auto issue_copy = [&](int step) -> cdsp_status {
+        const int src = (r - step + ci.s) % ci.s;
+        const int b = step & 1;
+        if (step >= 3) CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_comp[b], 0));
+        if (g) CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, g->comms[ci.ranks[src]]->ev_app, 0));
+        const size_t bytes = static_cast<size_t>(ci.hist[src] + m2) * c->row_bytes;
+        const PeerView& pv = c->peers[ci.ranks[src]];
+        CDSP_CUDA(cudaMemcpyAsync(c->recv_k[b], pv.k, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
+        CDSP_CUDA(cudaMemcpyAsync(c->recv_v[b], pv.v, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
+        CDSP_CUDA(cudaEventRecord(c->ev_copy[b], c->comm_stream));
+        return CDSP_OK;
+    };
+    CDSP_CHECK_STATUS(issue_copy(1));
+    for (int step = 0; step < ci.s; ++step) {
+        if (step + 1 >= 2 && step + 1 < ci.s) CDSP_CHECK_STATUS(issue_copy(step + 1));
+        const int src = (r - step + ci.s) % ci.s;
+        const int b = step & 1;
+        const char* kb = c->self.k;
+        const char* vb = c->self.v;
+        if (step > 0) {
+            CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_copy[b], 0));
+            kb = c->recv_k[b];
+            vb = c->recv_v[b];
+        }
+        const int mode = step == 0 ? CDSP_ATTN_FIRST : (step == ci.s - 1 ? CDSP_ATTN_LAST : CDSP_ATTN_MID);
+        CDSP_CHECK_STATUS(run_attention_timed(c, q, kb, vb, c->dtype, Hq, c->Hkv, c->D, segments_for(ci, r, src),
+                                              scale, mode, c->o_acc, c->lse_acc, out, lse, st));
+        if (step > 0) CDSP_CUDA(cudaEventRecord(c->ev_comp[b], st));
+    }
+    CDSP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
+    CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
+    return CDSP_OK;
+}
+
+// Loopback execution of one chunk by all its ranks, ordered by events:
+//   previous calls finished -> balancing pulls -> (old ranks wait for their pullers) append ->
+//   ring (each pull waits for the source's append) -> finish event.
+cdsp_status run_group_local(LocalGroup* g, const ChunkInfo& ci) {
+    auto comm_of = [&](int r) { return g->comms[ci.ranks[r]]; };
+    for (int r = 0; r < ci.s; ++r)
+        for (int j = 0; j < ci.s; ++j)
+            if (comm_of(j)->fin_recorded) CDSP_CUDA(cudaStreamWaitEvent(g->calls[r].st, comm_of(j)->ev_fin, 0));
+    if (ci.s_prev > 0 && ci.s > ci.s_prev) {
+        for (int r = 0; r < ci.s; ++r) {
+            CDSP_CHECK_STATUS(phase_balance(comm_of(r), ci, r, g->calls[r].st));
+            CDSP_CUDA(cudaEventRecord(comm_of(r)->ev_bal, g->calls[r].st));
+        }
+        for (int i = 0; i < ci.n_moves; ++i)  // an old rank overwrites its moved parts only after the pull
+            CDSP_CUDA(cudaStreamWaitEvent(g->calls[ci.moves[i].src].st, comm_of(ci.moves[i].dst)->ev_bal, 0));
+    }
+    for (int r = 0; r < ci.s; ++r) {
+        PendingCall& pc = g->calls[r];
+        CDSP_CHECK_STATUS(phase_append(comm_of(r), ci, r, &pc.k, &pc.v, pc.st));
+        CDSP_CUDA(cudaEventRecord(comm_of(r)->ev_app, pc.st));
+        pc.prev_kv->n = comm_of(r)->n;
+    }
+    for (int r = 0; r < ci.s; ++r) {
+        PendingCall& pc = g->calls[r];
+        CDSP_CHECK_STATUS(phase_ring(comm_of(r), ci, r, pc.q.ptr, static_cast<int>(pc.q.H), pc.out.ptr, pc.lse,
+                                     pc.scale, pc.st, g));
+    }
+    for (int r = 0; r < ci.s; ++r) {
+        CDSP_CUDA(cudaEventRecord(comm_of(r)->ev_fin, g->calls[r].st));
+        comm_of(r)->fin_recorded = true;
+    }
+    return CDSP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -233,7 +385,8 @@ cdsp_status cdsp_comm_create(cdsp_comm* out, int32_t rank, int32_t world, int32_
     if (e != cudaSuccess) return fail(e, "cudaMemset");
     e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return fail(e, "cudaStreamCreate");
-    cudaEvent_t* evs[6] = {&c->ev_ready, &c->ev_done, &c->ev_copy[0], &c->ev_copy[1], &c->ev_comp[0], &c->ev_comp[1]};
+    cudaEvent_t* evs[9] = {&c->ev_ready,   &c->ev_done,   &c->ev_copy[0], &c->ev_copy[1], &c->ev_comp[0],
+                           &c->ev_comp[1], &c->ev_bal,    &c->ev_app,     &c->ev_fin};
     for (auto* ev : evs) {
         e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
         if (e != cudaSuccess) return fail(e, "cudaEventCreate");
@@ -285,10 +438,17 @@ cdsp_status cdsp_comm_connect_local(cdsp_comm* comms, int32_t world) {
                          comms[i]->D == comms[0]->D && comms[i]->dtype == comms[0]->dtype &&
                          comms[i]->device == comms[0]->device,
                      CDSP_ERR_INVALID, "loopback communicators must share geometry and device");
+        CDSP_REQUIRE(!comms[i]->connected && comms[i]->lg == nullptr, CDSP_ERR_INVALID,
+                     "comms[%d] is already connected", i);
     }
+    LocalGroup* g = new LocalGroup();
+    g->world = world;
+    g->refs = world;
     for (int i = 0; i < world; ++i) {
+        g->comms[i] = comms[i];
         for (int j = 0; j < world; ++j) comms[i]->peers[j] = comms[j]->self;
         comms[i]->connected = true;
+        comms[i]->lg = g;
     }
     return CDSP_OK;
 }
@@ -339,7 +499,9 @@ cdsp_status cdsp_comm_destroy(cdsp_comm c) {
     if (c->region) cudaFree(c->region);
     if (c->bad_count) cudaFree(c->bad_count);
     if (c->err_host) cudaFreeHost(c->err_host);
-    cudaEvent_t evs[6] = {c->ev_ready, c->ev_done, c->ev_copy[0], c->ev_copy[1], c->ev_comp[0], c->ev_comp[1]};
+    if (c->lg && --c->lg->refs == 0) delete c->lg;
+    cudaEvent_t evs[9] = {c->ev_ready,   c->ev_done, c->ev_copy[0], c->ev_copy[1], c->ev_comp[0],
+                          c->ev_comp[1], c->ev_bal,  c->ev_app,     c->ev_fin};
     for (auto ev : evs)
         if (ev) cudaEventDestroy(ev);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
@@ -444,93 +606,58 @@ cdsp_status cdsp_prefill_chunk(const cdsp_tensor* q, const cdsp_tensor* k, const
     const int Hq = static_cast<int>(q->H);
     if (ci.s > 1) CDSP_CHECK_STATUS(ensure_acc(c, static_cast<size_t>(m2) * Hq * c->D, static_cast<size_t>(Hq) * m2, st));
 
+    if (ci.s > 1 && c->lg != nullptr) {
+        // loopback: a deferred collective (like an NCCL group) — record this rank's call; the
+        // call that completes the group issues every rank's phases in dependency order, with
+        // CUDA events instead of device-side peer barriers
+        LocalGroup* g = c->lg;
+        CDSP_REQUIRE(g->pending == 0 || (g->plan == sp_group->plan && g->chunk == sp_group->chunk), CDSP_ERR_INVALID,
+                     "loopback group has a pending call for another chunk");
+        CDSP_REQUIRE(!g->calls[r].set, CDSP_ERR_INVALID, "ring rank %d already called chunk %d", r, ci.c);
+        g->plan = sp_group->plan;
+        g->chunk = sp_group->chunk;
+        g->calls[r] = PendingCall{*q, *k, *v, *out, lse, prev_kv, scale, st, true};
+        if (++g->pending < ci.s) return CDSP_OK;
+        g->pending = 0;
+        cdsp_status rc = run_group_local(g, ci);
+        for (int i = 0; i < ci.s; ++i) g->calls[i].set = false;
+        return rc;
+    }
+
     // B1
     if (ci.s > 1) CDSP_CHECK_STATUS(barrier(c, ci, st));
     // cache balancing (R8)
     if (ci.s_prev > 0 && ci.s > ci.s_prev) {
-        for (int i = 0; i < ci.n_moves; ++i) {
-            const cdsp_move& mv = ci.moves[i];
-            if (mv.dst != r || mv.n_tok == 0) continue;
-            const PeerView& src = c->peers[ci.ranks[mv.src]];
-            CDSP_CUDA(cudaMemcpyAsync(c->self.k, src.k + mv.src_off * c->row_bytes, mv.n_tok * c->row_bytes,
-                                      cudaMemcpyDeviceToDevice, st));
-            CDSP_CUDA(cudaMemcpyAsync(c->self.v, src.v + mv.src_off * c->row_bytes, mv.n_tok * c->row_bytes,
-                                      cudaMemcpyDeviceToDevice, st));
-            CDSP_CUDA(cudaMemcpyAsync(c->self.pos, src.pos + mv.src_off, mv.n_tok * sizeof(int32_t),
-                                      cudaMemcpyDeviceToDevice, st));
-        }
+        CDSP_CHECK_STATUS(phase_balance(c, ci, r, st));
         CDSP_CHECK_STATUS(barrier(c, ci, st));  // B2
     }
     c->n = ci.hist[r];
-    // append this chunk's shard
-    {
-        AppendArgs a;
-        a.k_src = k->ptr;
-        a.v_src = v->ptr;
-        a.k_dst = c->self.k + c->n * c->row_bytes;
-        a.v_dst = c->self.v + c->n * c->row_bytes;
-        a.pos_dst = c->self.pos + c->n;
-        a.n_rows = m2;
-        a.row_bytes = static_cast<int64_t>(c->row_bytes);
-        a.len0 = ci.m;
-        a.pos0 = shard_pos0(ci, r);
-        a.pos1 = shard_pos1(ci, r);
-        CDSP_CHECK_STATUS(launch_store_append(a, st));
+    if (ci.s == 1 && c->n == 0) {
+        // single instance, no history: the attention reads this call's k/v directly while the
+        // copy engines append them to the store on the comm stream (no SMs taken from it)
+        CDSP_CUDA(cudaEventRecord(c->ev_ready, st));
+        CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+        CDSP_CUDA(cudaMemcpyAsync(c->self.k, k->ptr, m2 * c->row_bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
+        CDSP_CUDA(cudaMemcpyAsync(c->self.v, v->ptr, m2 * c->row_bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
+        CDSP_CHECK_STATUS(launch_fill_positions(c->self.pos, m2, ci.m, shard_pos0(ci, r), shard_pos1(ci, r),
+                                                c->comm_stream));
+        c->n = m2;
+        prev_kv->n = c->n;
+        CDSP_CHECK_STATUS(run_attention_timed(c, q->ptr, k->ptr, v->ptr, c->dtype, Hq, c->Hkv, c->D,
+                                              segments_for(ci, r, 0), scale, CDSP_ATTN_ONLY, nullptr, nullptr,
+                                              out->ptr, lse, st));
+        CDSP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
+        CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
+        return CDSP_OK;
     }
-    c->n += m2;
+    CDSP_CHECK_STATUS(phase_append(c, ci, r, k, v, st));
     prev_kv->n = c->n;
-
-    auto segs_for = [&](int src) {
-        cdsp_segments s;
-        s.nq = m2;
-        s.q_len0 = ci.m;
-        s.q_pos0 = shard_pos0(ci, r);
-        s.q_pos1 = shard_pos1(ci, r);
-        s.nkv = ci.hist[src] + m2;
-        s.kv_hist = ci.hist[src];
-        s.kv_len0 = ci.m;
-        s.kv_pos0 = shard_pos0(ci, src);
-        s.kv_pos1 = shard_pos1(ci, src);
-        return s;
-    };
     if (ci.s == 1) {
-        return run_attention_timed(c, q->ptr, c->self.k, c->self.v, c->dtype, Hq, c->Hkv, c->D, segs_for(0), scale,
-                                   CDSP_ATTN_ONLY, nullptr, nullptr, out->ptr, lse, st);
+        return run_attention_timed(c, q->ptr, c->self.k, c->self.v, c->dtype, Hq, c->Hkv, c->D,
+                                   segments_for(ci, r, 0), scale, CDSP_ATTN_ONLY, nullptr, nullptr, out->ptr, lse, st);
     }
     CDSP_CHECK_STATUS(barrier(c, ci, st));  // B3
-    CDSP_CUDA(cudaEventRecord(c->ev_ready, st));
-    CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-    auto issue_copy = [&](int step) -> cdsp_status {
-        const int src = (r - step + ci.s) % ci.s;
-        const int b = step & 1;
-        if (step >= 3) CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_comp[b], 0));
-        const size_t bytes = static_cast<size_t>(ci.hist[src] + m2) * c->row_bytes;
-        const PeerView& pv = c->peers[ci.ranks[src]];
-        CDSP_CUDA(cudaMemcpyAsync(c->recv_k[b], pv.k, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
-        CDSP_CUDA(cudaMemcpyAsync(c->recv_v[b], pv.v, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
-        CDSP_CUDA(cudaEventRecord(c->ev_copy[b], c->comm_stream));
-        return CDSP_OK;
-    };
-    CDSP_CHECK_STATUS(issue_copy(1));
-    for (int step = 0; step < ci.s; ++step) {
-        if (step + 1 >= 2 && step + 1 < ci.s) CDSP_CHECK_STATUS(issue_copy(step + 1));
-        const int src = (r - step + ci.s) % ci.s;
-        const int b = step & 1;
-        const char* kb = c->self.k;
-        const char* vb = c->self.v;
-        if (step > 0) {
-            CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_copy[b], 0));
-            kb = c->recv_k[b];
-            vb = c->recv_v[b];
-        }
-        const int mode = step == 0 ? CDSP_ATTN_FIRST : (step == ci.s - 1 ? CDSP_ATTN_LAST : CDSP_ATTN_MID);
-        CDSP_CHECK_STATUS(run_attention_timed(c, q->ptr, kb, vb, c->dtype, Hq, c->Hkv, c->D, segs_for(src), scale,
-                                              mode, c->o_acc, c->lse_acc, out->ptr, lse, st));
-        if (step > 0) CDSP_CUDA(cudaEventRecord(c->ev_comp[b], st));
-    }
-    CDSP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
-    CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
-    return CDSP_OK;
+    return phase_ring(c, ci, r, q->ptr, Hq, out->ptr, lse, scale, st, nullptr);
 }
 
 // ------------------------------------------------------------------------------- merge

@@ -52,6 +52,8 @@ struct AppendArgs {
     int64_t len0, pos0, pos1;  // row i < len0 -> pos0 + i, else pos1 + (i - len0)
 };
 cdsp_status launch_store_append(const AppendArgs& a, cudaStream_t st);
+// Store positions only: dst[i] = i < len0 ? pos0 + i : pos1 + (i - len0).
+cdsp_status launch_fill_positions(int32_t* dst, int64_t n, int64_t len0, int64_t pos0, int64_t pos1, cudaStream_t st);
 
 cdsp_status launch_zigzag_map(int64_t L, int s, int32_t* tok_rank, int32_t* tok_slot, cudaStream_t st);
 
@@ -68,6 +70,7 @@ struct PagedArgs {
     void* k_cache[8];
     void* v_cache[8];
     unsigned long long* bad_count;
+    int seg_vec, seg_shift;  // set by the launcher: 16-B vectors per TP slice, log2 (or -1)
 };
 cdsp_status launch_paged_scatter(const PagedArgs& a, cudaStream_t st);
 

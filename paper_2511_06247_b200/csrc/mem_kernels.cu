@@ -126,6 +126,11 @@ __global__ void __launch_bounds__(256) store_append_kernel(const AppendArgs a) {
     }
 }
 
+__global__ void fill_positions_kernel(int32_t* dst, int64_t n, int64_t len0, int64_t pos0, int64_t pos1) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = static_cast<int32_t>(i < len0 ? pos0 + i : pos1 + (i - len0));
+}
+
 // ------------------------------------------------------------------ K*5 zigzag map
 __global__ void zigzag_map_kernel(int64_t L, int s, int64_t m, int32_t* tok_rank, int32_t* tok_slot) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -137,32 +142,32 @@ __global__ void zigzag_map_kernel(int64_t L, int s, int64_t m, int32_t* tok_rank
 }
 
 // ------------------------------------------------------------------ K*6 paged scatter (R15)
+// One warp per (token, K|V) row: the token's position and physical block are resolved once;
+// the row [Hkv, D] splits into tp contiguous slices (one per decode TP rank), each copied to a
+// contiguous slot [blk][p % B][Hkv/tp][D] of that rank's cache in 16-byte vectors.
 __global__ void __launch_bounds__(256) paged_scatter_kernel(const PagedArgs a) {
-    const int row_vec = a.D * a.esize / 16;  // 16-byte vectors per head row
-    const int hl = a.Hkv / a.tp;
-    const int64_t per_tensor = a.n_tok * a.Hkv * row_vec;
-    const int64_t total = 2 * per_tensor;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const int which = i >= per_tensor;  // 0: K, 1: V
-        const int64_t j = which ? i - per_tensor : i;
-        const int c = static_cast<int>(j % row_vec);
-        const int64_t rh = j / row_vec;
-        const int h = static_cast<int>(rh % a.Hkv);
-        const int64_t tok = rh / a.Hkv;
-        const int64_t pos = tok < a.len0 ? a.pos0 + tok : a.pos1 + (tok - a.len0);
-        const int64_t lb = pos / a.block_size;
-        const int32_t blk = lb < a.n_table ? a.block_table[lb] : -1;
-        if (blk < 0 || blk >= a.num_blocks) {
-            if (c == 0 && which == 0 && h == 0) atomicAdd(a.bad_count, 1ull);
-            continue;
-        }
-        const int t = h / hl;
-        const int hloc = h - t * hl;
-        const uint4* src = static_cast<const uint4*>(which ? a.v : a.k) + rh * row_vec + c;
-        uint4* dst = static_cast<uint4*>(which ? a.v_cache[t] : a.k_cache[t]) +
-                     ((static_cast<int64_t>(blk) * a.block_size + pos % a.block_size) * hl + hloc) * row_vec + c;
-        *dst = __ldg(src);
+    const int warps = blockDim.x >> 5;
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * warps + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (w >= 2 * a.n_tok) return;
+    const int which = w >= a.n_tok;  // 0: K, 1: V
+    const int64_t tok = which ? w - a.n_tok : w;
+    const int64_t pos = tok < a.len0 ? a.pos0 + tok : a.pos1 + (tok - a.len0);
+    const int64_t lb = pos / a.block_size;
+    const int32_t blk = lb < a.n_table ? __ldg(a.block_table + lb) : -1;
+    if (blk < 0 || blk >= a.num_blocks) {
+        if (lane == 0 && which == 0) atomicAdd(a.bad_count, 1ull);
+        return;
+    }
+    const int seg_vec = a.seg_vec;                  // 16-byte vectors per TP slice (Hkv/tp heads)
+    const int row_vec = seg_vec * a.tp;             // per token row
+    const int64_t slot = static_cast<int64_t>(blk) * a.block_size + pos % a.block_size;
+    const uint4* src = static_cast<const uint4*>(which ? a.v : a.k) + tok * row_vec;
+    for (int c = lane; c < row_vec; c += 32) {
+        const int t = a.seg_shift >= 0 ? (c >> a.seg_shift) : c / seg_vec;
+        const int cl = c - t * seg_vec;
+        uint4* dst = static_cast<uint4*>(which ? a.v_cache[t] : a.k_cache[t]) + slot * seg_vec + cl;
+        *dst = __ldg(src + c);
     }
 }
 
@@ -251,6 +256,13 @@ cdsp_status launch_store_append(const AppendArgs& a, cudaStream_t st) {
     return CDSP_OK;
 }
 
+cdsp_status launch_fill_positions(int32_t* dst, int64_t n, int64_t len0, int64_t pos0, int64_t pos1, cudaStream_t st) {
+    if (n == 0) return CDSP_OK;
+    fill_positions_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(dst, n, len0, pos0, pos1);
+    CDSP_CUDA(cudaGetLastError());
+    return CDSP_OK;
+}
+
 cdsp_status launch_zigzag_map(int64_t L, int s, int32_t* tok_rank, int32_t* tok_slot, cudaStream_t st) {
     if (L == 0) return CDSP_OK;
     const int64_t m = L / (2 * s);
@@ -260,11 +272,18 @@ cdsp_status launch_zigzag_map(int64_t L, int s, int32_t* tok_rank, int32_t* tok_
     return CDSP_OK;
 }
 
-cdsp_status launch_paged_scatter(const PagedArgs& a, cudaStream_t st) {
+cdsp_status launch_paged_scatter(const PagedArgs& a_in, cudaStream_t st) {
+    PagedArgs a = a_in;
     CDSP_REQUIRE((a.D * a.esize) % 16 == 0, CDSP_ERR_SHAPE, "head row not a multiple of 16 bytes");
-    const int64_t work = 2 * a.n_tok * a.Hkv * (a.D * a.esize / 16);
-    if (work == 0) return CDSP_OK;
-    paged_scatter_kernel<<<grid_for(work), 256, 0, st>>>(a);
+    a.seg_vec = (a.Hkv / a.tp) * a.D * a.esize / 16;
+    a.seg_shift = -1;
+    for (int sh = 0; sh < 30; ++sh)
+        if ((1 << sh) == a.seg_vec) a.seg_shift = sh;
+    const int64_t rows = 2 * a.n_tok;  // one warp per (token, K|V)
+    if (rows == 0) return CDSP_OK;
+    const int64_t blocks = (rows + 7) / 8;
+    CDSP_REQUIRE(blocks < (1ll << 31), CDSP_ERR_SHAPE, "transfer too large");
+    paged_scatter_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(a);
     CDSP_CUDA(cudaGetLastError());
     return CDSP_OK;
 }
