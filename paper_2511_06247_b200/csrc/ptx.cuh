@@ -43,17 +43,26 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint: the thread sleeps until the phase completes (or the
+// hint expires) instead of re-issuing, so waiting warps do not steal issue slots.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000000u)
+        : "memory");
+    return ok != 0;
+}
 // Wait for the phase with parity `parity` to complete.  A watchdog traps after ~4 s so a
 // protocol bug fails the launch instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
-    uint64_t t0 = globaltimer();
-    uint32_t n = 0;
-    while (!mbar_try_wait(bar, parity)) {
-        if (++n == 4096) {
-            n = 0;
-            if (globaltimer() - t0 > 4000000000ull) __trap();
-        }
+    const uint64_t t0 = globaltimer();
+    while (!mbar_try_wait_sleep(bar, parity)) {
+        if (globaltimer() - t0 > 4000000000ull) __trap();
     }
 }
 
