@@ -7,28 +7,33 @@
 // tensors"), extended to historical tokens as Tetris does (§6: "we extend Flash
 // Attention [7] to support zigzag ring attention for historical tokens").
 //
-// B200 design (not the paper's A100 FlashAttention-2), measured on the box:
+// B200 design (not the paper's A100 FlashAttention-2), from measurements on the box:
 //  * tcgen05.mma M=128 reaches the full 8192 FLOP/clk/SM only for N >= 128 (N=64: ~48 clk
 //    per K=16 step instead of 32; tools/mma_rate.cu), so S = Q K^T uses 128-key tiles.
-//  * one CTA = one 128-row query tile of one head; 20 warps:
-//      warps 0, 2  TMA producers: Q once; K (3 stages) and V (2 stages) in 128-key tiles
-//      warp 1      TMEM allocator + tcgen05.mma issuer (warp-uniform loop, one lane issues)
-//      warps 2-3   build the CTA's KV-tile schedule (tile kinds) in shared memory first
-//      warps 4-19  softmax + epilogue: warp w owns TMEM lanes 32*(w%4).. (32 query rows)
-//                  and key columns 32*cg.. of the tile, cg = (w-4)/4; the four warps of a
-//                  lane quadrant exchange their row maxima through shared memory.
-//  * TMEM (512 cols): O [0,128), S double buffer [128,256) [256,384), P (bf16) double
-//    buffer [384,448) [448,512).  The MMA warp issues S(j+2) = Q K_{j+2}^T as soon as the
-//    softmax warps have copied S(j) to registers, and O += P(j) V_j once P(j) is in TMEM,
-//    so the tensor core computes scores two tiles ahead of the exponentials; P is the A
-//    operand of PV straight from TMEM.
-//  * four softmax warps per SMSP keep MUFU / FMA / issue busy (two per SMSP left them
-//    latency-bound); packed fp32x2 FFMA2/FADD2; 3/8 of the exponentials run as a cubic
-//    on the FMA pipe (rel. error 7.5e-5 << bf16's 2^-9) to relieve MUFU.
+//  * MUFU.EX2 issues 16 lanes/clk/SM (tools/exp_rate.cu): the 16384 exponentials of a
+//    128x128 tile take 1024 clk, exactly the two MMAs of that tile.  3/8 of them therefore
+//    run as a cubic on the FMA pipe, and the softmax must spend almost no issue slots on
+//    anything else.  One thread owns one query row (all 128 columns of S in registers):
+//    the row max needs no cross-warp exchange and per-tile bookkeeping (waits, arrives,
+//    TMEM addressing) is paid by 4 warps per tile instead of 16.
+//  * one CTA = two 128-row query tiles (Q0, Q1) of one head, 11 warps:
+//      warps 0-3   softmax + epilogue of Q0 (warp w owns TMEM lanes 32*(w%4)..)
+//      warps 4-7   softmax + epilogue of Q1
+//      warp 8      TMA producer: Q0, Q1 once, then K tiles (2 stages)
+//      warp 9      TMA producer: V tiles (2 stages)
+//      warp 10     TMEM allocator + tcgen05.mma issuer (warp-uniform loop, one lane issues)
+//    The tensor pipe alternates [O0 += P0 V_{j-1}, S0 = Q0 K_j^T] and [O1 += P1 V_{j-1},
+//    S1 = Q1 K_j^T]: while it works for one query tile the other tile's softmax runs, so
+//    each softmax group has a full half-period (two MMAs) for its 128x128 tile.
+//  * TMEM (512 cols): O0 [0,128), O1 [128,256), S0 [256,384), S1 [384,512).  P (bf16) is
+//    written over its own S columns and is the A operand of PV straight from TMEM; the
+//    next S into those columns is issued after that PV on the same in-order tensor pipe.
+//    S_t(j) is committed after PV_t(j-1), so when the softmax sees S_t(j), O_t is stable.
 //  * lazy rescaling: the running max only moves when it grows by > 8 (log2 units); O is
-//    rescaled in TMEM after PV(j-1) completed.
-//  * masks from segment descriptors: empty tiles are skipped, full tiles run mask-free,
-//    only diagonal / ragged tiles evaluate per-element positions.
+//    rescaled in TMEM after P is stored (registers of S are dead by then).
+//  * masks from segment descriptors: empty tiles are skipped per query tile, full tiles run
+//    mask-free, diagonal / ragged tiles build per-row 32-bit column masks from the three
+//    visible intervals (history, segment 0, segment 1).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -50,35 +55,36 @@ using namespace ptx;
 
 namespace {
 
-constexpr int kThreads = 640;
-constexpr int kSoftmaxWarps = 16;
-constexpr int BM = 128;                 // query rows per CTA (TMEM lanes)
+constexpr int kThreads = 352;           // 11 warps
+constexpr int BQ = 128;                 // rows per query tile (TMEM lanes)
+constexpr int NQT = 2;                  // query tiles per CTA
+constexpr int BM = BQ * NQT;            // query rows per CTA
 constexpr int BN = 128;                 // KV rows per tile
 constexpr int kBox = 128 * 128;         // TMA box: 128 rows x 64 bf16 (128-byte swizzle rows)
 constexpr int kSchedMax = 8192;         // KV tiles per launch (1M keys)
+constexpr int W_K = 8, W_V = 9, W_MMA = 10;
+constexpr int kSchedWarps = 8;          // warps 0-7 classify the KV tiles at setup
 
 template <int HD>
 struct Layout {
     static constexpr int NBOX = HD / 64;
     static constexpr int TILE = kBox * NBOX;  // one 128-row tile of Q, K or V
-    static constexpr int KST = 3, VST = 2;
+    static constexpr int KST = 2, VST = 2;
     static constexpr int OFF_Q = 0;
-    static constexpr int OFF_K = OFF_Q + TILE;
+    static constexpr int OFF_K = OFF_Q + NQT * TILE;
     static constexpr int OFF_V = OFF_K + KST * TILE;
-    static constexpr int OFF_RED = OFF_V + VST * TILE;  // [2 parity][4 quad][32 lanes][4 cg] float
-    static constexpr int OFF_BAR = OFF_RED + 2 * 4 * 4 * 32 * 4;
-    // q_full, k_full[KST], k_empty[KST], v_full[VST], v_empty[VST],
-    // s_full[2], s_free[2], p_full[2], p_free[2], o_full
-    static constexpr int B_Q = 0, B_KF = 1, B_KE = B_KF + KST, B_VF = B_KE + KST, B_VE = B_VF + VST,
-                         B_SF = B_VE + VST, B_SE = B_SF + 2, B_PF = B_SE + 2, B_PE = B_PF + 2, B_O = B_PE + 2,
-                         NBAR = B_O + 1;
+    static constexpr int OFF_BAR = OFF_V + VST * TILE;
+    // q_full[2], k_full[KST], k_empty[KST], v_full[VST], v_empty[VST], s_full[2], p_full[2], o_full[2]
+    static constexpr int B_Q = 0, B_KF = B_Q + NQT, B_KE = B_KF + KST, B_VF = B_KE + KST, B_VE = B_VF + VST,
+                         B_SF = B_VE + VST, B_PF = B_SF + NQT, B_OF = B_PF + NQT, NBAR = B_OF + NQT;
     static constexpr int OFF_TMEM_SLOT = OFF_BAR + NBAR * 8;
-    static constexpr int OFF_JR = OFF_TMEM_SLOT + 16;   // used-tile range: 2 x (min, max+1)
-    static constexpr int OFF_SCHED = OFF_JR + 16;
+    static constexpr int OFF_JR = OFF_TMEM_SLOT + 16;   // used-tile range per setup warp: (min, max+1)
+    static constexpr int OFF_SCHED = OFF_JR + 8 * kSchedWarps;
     static constexpr int SMEM = OFF_SCHED + kSchedMax + 1024;  // + alignment slack
 };
 
-constexpr uint32_t COL_O = 0, COL_S = 128, COL_P = 384;  // S buffer b at COL_S + 128 b, P at COL_P + 64 b
+__host__ __device__ constexpr uint32_t col_o(int t) { return 128u * t; }
+__host__ __device__ constexpr uint32_t col_s(int t) { return 256u + 128u * t; }
 
 struct TcParams {
     cdsp_segments seg;
@@ -156,12 +162,63 @@ __device__ __forceinline__ float2 ex2_fma2(float2 x) {
                        __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
 }
 
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+// Registers loaded by tcgen05.ld are only valid after tcgen05.wait::ld; tying them to an
+// (empty) volatile asm after the wait keeps their uses below it.
+__device__ __forceinline__ void reg_tie32(uint32_t* r) {
+    asm volatile(""
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                   "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                   "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
+}
+__device__ __forceinline__ void tmem_ld32p(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ int clamp_bn(int64_t x) { return x < 0 ? 0 : (x > BN ? BN : static_cast<int>(x)); }
+// bits [lo, hi) of the 32 columns starting at `base`
+__device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
+    const int l = max(lo - base, 0), h = min(hi - base, 32);
+    if (l >= h) return 0u;
+    const uint32_t hm = h >= 32 ? 0xFFFFFFFFu : ((1u << h) - 1u);
+    return hm & ~((1u << l) - 1u);
+}
+
+// Mask a partial tile: the KV rows of tile j visible to a query at position qpos are the
+// union of [0, b0) (history), [a1, b1) (segment 0 rows with pos <= qpos) and [a2, b2)
+// (segment 1 rows with pos <= qpos), tile-relative — seg_visible() written as intervals.
+__device__ __forceinline__ void mask_tile(uint32_t* s, const cdsp_segments& sg, int j, int64_t qpos) {
+    const int64_t c0 = static_cast<int64_t>(j) * BN;
+    const int nk = clamp_bn(sg.nkv - c0);
+    const int h = clamp_bn(sg.kv_hist - c0);
+    const int64_t e0abs = sg.kv_hist + sg.kv_len0;
+    const int e0 = clamp_bn(e0abs - c0);
+    const int lim0 = clamp_bn(qpos - sg.kv_pos0 + sg.kv_hist + 1 - c0);
+    const int lim1 = clamp_bn(qpos - sg.kv_pos1 + e0abs + 1 - c0);
+    const int b0 = min(h, nk);
+    const int a1 = h, b1 = min(min(e0, lim0), nk);
+    const int a2 = e0, b2 = min(nk, lim1);
+#pragma unroll
+    for (int w = 0; w < BN / 32; ++w) {
+        const uint32_t mk = range_bits(0, b0, 32 * w) | range_bits(a1, b1, 32 * w) | range_bits(a2, b2, 32 * w);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (!((mk >> i) & 1u)) s[32 * w + i] = __float_as_uint(-INFINITY);
+    }
 }
 
 template <int HD>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __maxnreg__(168)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const TcParams p) {
     using L = Layout<HD>;
@@ -178,57 +235,61 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto bar = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM_SLOT);
     uint8_t* sched = smem + L::OFF_SCHED;
-    float* red = reinterpret_cast<float*>(smem + L::OFF_RED);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const cdsp_segments& sg = p.seg;
 
     // ---- work unit: head-major (the ~148 CTAs in flight share one head's K/V, which stays
-    // L2-resident; head-minor order streamed all heads' K/V from DRAM ~40x over), heavy row
-    // blocks first within a head (causal work grows with the row index)
+    // L2-resident), heavy row blocks first within a head (causal work grows with the row)
     const int head = static_cast<int>(blockIdx.x) / p.n_rb;
     const int rb = p.n_rb - 1 - static_cast<int>(blockIdx.x) % p.n_rb;
     const int kvh = head / p.g;
     const int64_t row0 = static_cast<int64_t>(rb) * BM;
     const int n_kv_tiles = static_cast<int>((sg.nkv + BN - 1) / BN);
+    const bool q1_rows = row0 + BQ < sg.nq;
 
     // ---- setup
-    if (warp == 0 && lane == 0) {
-        mbar_init(bar(L::B_Q), 1);
-        for (int i = 0; i < L::KST; ++i) {
-            mbar_init(bar(L::B_KF + i), 1);
-            mbar_init(bar(L::B_KE + i), 1);
+    if (warp == W_K) {
+        if (lane == 0) {
+            for (int t = 0; t < NQT; ++t) mbar_init(bar(L::B_Q + t), 1);
+            for (int i = 0; i < L::KST; ++i) {
+                mbar_init(bar(L::B_KF + i), 1);
+                mbar_init(bar(L::B_KE + i), 1);
+            }
+            for (int i = 0; i < L::VST; ++i) {
+                mbar_init(bar(L::B_VF + i), 1);
+                mbar_init(bar(L::B_VE + i), 1);
+            }
+            for (int t = 0; t < NQT; ++t) {
+                mbar_init(bar(L::B_SF + t), 1);
+                mbar_init(bar(L::B_PF + t), 4);
+                mbar_init(bar(L::B_OF + t), 1);
+            }
+            fence_barrier_init();
+            tma_prefetch_desc(&tm_q);
+            tma_prefetch_desc(&tm_k);
+            tma_prefetch_desc(&tm_v);
+            // Q does not depend on the schedule: start its loads now
+            for (int t = 0; t < (q1_rows ? 2 : 1); ++t) {
+                mbar_expect_tx(bar(L::B_Q + t), L::TILE);
+                for (int b = 0; b < L::NBOX; ++b)
+                    tma_load_3d(sQ + t * L::TILE + b * kBox, &tm_q, bar(L::B_Q + t), b * 64, head,
+                                static_cast<int>(row0 + t * BQ));
+            }
         }
-        for (int i = 0; i < L::VST; ++i) {
-            mbar_init(bar(L::B_VF + i), 1);
-            mbar_init(bar(L::B_VE + i), 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(bar(L::B_SF + b), 1);
-            mbar_init(bar(L::B_SE + b), kSoftmaxWarps);
-            mbar_init(bar(L::B_PF + b), kSoftmaxWarps);
-            mbar_init(bar(L::B_PE + b), 1);
-        }
-        mbar_init(bar(L::B_O), 1);
-        fence_barrier_init();
-        tma_prefetch_desc(&tm_q);
-        tma_prefetch_desc(&tm_k);
-        tma_prefetch_desc(&tm_v);
-        // Q does not depend on the schedule: start its load now
-        mbar_expect_tx(bar(L::B_Q), L::TILE);
-        for (int b = 0; b < L::NBOX; ++b)
-            tma_load_3d(sQ + b * kBox, &tm_q, bar(L::B_Q), b * 64, head, static_cast<int>(row0));
-    } else if (warp == 1) {
+    } else if (warp == W_MMA) {
         tmem_alloc(smem_u32(tmem_slot), 512);
         tmem_relinquish();
-    } else if (warp == 2 || warp == 3) {
-        // KV-tile schedule: sched[j] = tile kind (0 = skip)
-        int64_t qlo, qhi;
-        bool qany;
-        seg_qrange(sg, row0, row0 + BM, qlo, qhi, qany);
+    } else if (warp < kSchedWarps) {
+        // KV-tile schedule: sched[j] = kind for Q0 | kind for Q1 << 2 (0 = skip)
+        int64_t qlo0, qhi0, qlo1, qhi1;
+        bool qany0, qany1;
+        seg_qrange(sg, row0, row0 + BQ, qlo0, qhi0, qany0);
+        seg_qrange(sg, row0 + BQ, row0 + BM, qlo1, qhi1, qany1);
         int jmin = INT_MAX, jmax = 0;
-        for (int j = (warp - 2) * 32 + lane; j < n_kv_tiles; j += 64) {
-            const int k = seg_tile_kind(sg, qany, qlo, qhi, static_cast<int64_t>(j) * BN, BN);
+        for (int j = warp * 32 + lane; j < n_kv_tiles; j += kSchedWarps * 32) {
+            const int64_t c0 = static_cast<int64_t>(j) * BN;
+            const int k = seg_tile_kind(sg, qany0, qlo0, qhi0, c0, BN) | (seg_tile_kind(sg, qany1, qlo1, qhi1, c0, BN) << 2);
             sched[j] = static_cast<uint8_t>(k);
             if (k != 0) {
                 jmin = min(jmin, j);
@@ -240,8 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             jmax = max(jmax, __shfl_xor_sync(0xFFFFFFFFu, jmax, o));
         }
         if (lane == 0) {
-            reinterpret_cast<int*>(smem + L::OFF_JR)[2 * (warp - 2)] = jmin;
-            reinterpret_cast<int*>(smem + L::OFF_JR)[2 * (warp - 2) + 1] = jmax;
+            reinterpret_cast<int*>(smem + L::OFF_JR)[2 * warp] = jmin;
+            reinterpret_cast<int*>(smem + L::OFF_JR)[2 * warp + 1] = jmax;
         }
     }
     tc_fence_before();
@@ -249,14 +310,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // the used KV tiles lie in [j_lo, j_hi) (sched[j] == 0 marks skipped tiles inside it)
-    const int* jr = reinterpret_cast<const int*>(smem + L::OFF_JR);
-    const int j_lo = min(jr[0], jr[2]), j_hi = max(jr[1], jr[3]);
+    int j_lo = INT_MAX, j_hi = 0;
+    {
+        const int* jr = reinterpret_cast<const int*>(smem + L::OFF_JR);
+#pragma unroll
+        for (int w = 0; w < kSchedWarps; ++w) {
+            j_lo = min(j_lo, jr[2 * w]);
+            j_hi = max(j_hi, jr[2 * w + 1]);
+        }
+    }
     if (threadIdx.x == 0) CTA_STAMP(4);
 
-    if (warp == 0 || warp == 2) {
-        // ======== TMA producers: warp 0 streams K, warp 2 streams V (independent rings, so a
-        // K load never waits behind a V stage; one lane issues, the warp runs the loop) ========
-        const bool is_k = warp == 0;
+    if (warp == W_K || warp == W_V) {
+        // ======== TMA producers: K and V in independent rings (a K load never waits behind a
+        // V stage); one lane issues, the warp runs the loop ========
+        const bool is_k = warp == W_K;
         const int nst = is_k ? L::KST : L::VST;
         const uint32_t s0 = is_k ? sK : sV;
         const int bfull = is_k ? L::B_KF : L::B_VF, bempty = is_k ? L::B_KE : L::B_VE;
@@ -275,254 +343,257 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             ++it;
         }
-    } else if (warp == 1) {
+    } else if (warp == W_MMA) {
         // ================= MMA issuer (warp-uniform loop, one lane issues) =================
-        constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, false, false);
-        constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, HD, false, true);
-        const uint64_t dq = umma_desc_sw128(sQ, 16, 1024);
+        constexpr uint32_t idesc_qk = idesc_bf16_f32(BQ, BN, false, false);
+        constexpr uint32_t idesc_pv = idesc_bf16_f32(BQ, HD, false, true);
+        const uint64_t dq0 = umma_desc_sw128(sQ, 16, 1024);
         const uint64_t dk0 = umma_desc_sw128(sK, 16, 1024);
         const uint64_t dv0 = umma_desc_sw128(sV, kBox, 1024);
-        // S(b) = Q K^T: M=128, N=128, K=HD in steps of 16 (32 B inside a 128-B swizzle row)
-        auto issue_qk = [&](int ks, int b) {
+        // S_t = Q_t K^T: M=128, N=128, K=HD in steps of 16 (32 B inside a 128-B swizzle row)
+        auto issue_qk = [&](int t, int ks) {
             const uint64_t dk = dk0 + static_cast<uint64_t>((ks * L::TILE) >> 4);
+            const uint64_t dq = dq0 + static_cast<uint64_t>((t * L::TILE) >> 4);
 #pragma unroll
             for (int kk = 0; kk < HD / 16; ++kk) {
                 const uint64_t off = static_cast<uint64_t>(((kk / 4) * kBox + (kk % 4) * 32) >> 4);
-                mma_ss(tmem + COL_S + 128 * b, dq + off, dk + off, idesc_qk, kk > 0 ? 1u : 0u);
+                mma_ss(tmem + col_s(t), dq + off, dk + off, idesc_qk, kk > 0 ? 1u : 0u);
             }
         };
-        // O += P(b) V: M=128, N=HD, K=128 keys in steps of 16 (V rows, 2048 B)
-        auto issue_pv = [&](int vs, int b, bool acc) {
+        // O_t += P_t V: M=128, N=HD, K=128 keys in steps of 16 (V rows, 2048 B); P_t is bf16
+        // in the S_t columns (8 TMEM columns per 16 keys)
+        auto issue_pv = [&](int t, int vs, bool acc) {
             const uint64_t dv = dv0 + static_cast<uint64_t>((vs * L::TILE) >> 4);
 #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk)
-                mma_ts(tmem + COL_O, tmem + COL_P + 64 * b + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4),
+                mma_ts(tmem + col_o(t), tmem + col_s(t) + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4),
                        idesc_pv, (acc || kk > 0) ? 1u : 0u);
         };
-        int n_used = 0;
-        for (int j = j_lo; j < j_hi; ++j) n_used += sched[j] != 0;
-        mbar_wait(bar(L::B_Q), 0);
-        tc_fence_after();
-        for (int it = 0; it < 2 && it < n_used; ++it) {  // prologue: S(0), S(1)
-            mbar_wait(bar(L::B_KF + it), 0);
-            tc_fence_after();
-            if (elect_one()) {
-                issue_qk(it, it);
-                mma_commit(bar(L::B_SF + it));
-                mma_commit(bar(L::B_KE + it));
-            }
-            __syncwarp();
-        }
-        for (int it = 0; it < n_used; ++it) {
-            const int b = it & 1;
-            const uint32_t ph = (it >> 1) & 1;
-            if (it + 2 < n_used) {  // scores two tiles ahead, once softmax has read S(it)
-                const int ks = (it + 2) % L::KST;
-                mbar_wait(bar(L::B_SE + b), ph);
-                mbar_wait(bar(L::B_KF + ks), ((it + 2) / L::KST) & 1);
-                tc_fence_after();
-                if (elect_one()) {
-                    KTRACE(8, it);
-                    issue_qk(ks, b);
-                    mma_commit(bar(L::B_SF + b));
-                    mma_commit(bar(L::B_KE + ks));
-                    KTRACE(9, it);
+        // Iteration `it` (union tile j_it): for t = 0, 1: O_t += P_t(j_{it-1}) V_{it-1} (if
+        // query tile t used j_{it-1}), then S_t = Q_t K_{it}^T (if it uses j_it).  K stage it
+        // is released after its S's, V stage it-1 after its PVs (commit = all prior MMAs).
+        int pv0 = 0, pv1 = 0;      // PVs issued per query tile (P_full phases consumed)
+        bool q0 = false, q1 = false;
+        int prev_kinds = 0, it = 0;
+        int j = j_lo;
+        while (j < j_hi && sched[j] == 0) ++j;
+        for (;;) {
+            const bool have = j < j_hi;
+            const int kinds = have ? sched[j] : 0;
+            const int last_pv_t = (prev_kinds >> 2) ? 1 : 0;
+            bool k_waited = false, v_waited = false;
+#pragma unroll
+            for (int t = 0; t < NQT; ++t) {
+                if ((prev_kinds >> (2 * t)) & 3) {
+                    int& pv = t == 0 ? pv0 : pv1;
+                    mbar_wait(bar(L::B_PF + t), pv & 1);
+                    if (!v_waited) {
+                        mbar_wait(bar(L::B_VF + (it - 1) % L::VST), ((it - 1) / L::VST) & 1);
+                        v_waited = true;
+                    }
+                    tc_fence_after();
+                    if (elect_one()) {
+                        KTRACE(8 + 2 * t, it);
+                        issue_pv(t, (it - 1) % L::VST, pv > 0);
+                        if (t == last_pv_t) mma_commit(bar(L::B_VE + (it - 1) % L::VST));
+                    }
+                    __syncwarp();
+                    ++pv;
                 }
-                __syncwarp();
+                if ((kinds >> (2 * t)) & 3) {
+                    bool& qr = t == 0 ? q0 : q1;
+                    if (!qr) {
+                        mbar_wait(bar(L::B_Q + t), 0);
+                        qr = true;
+                    }
+                    if (!k_waited) {
+                        mbar_wait(bar(L::B_KF + it % L::KST), (it / L::KST) & 1);
+                        k_waited = true;
+                    }
+                    tc_fence_after();
+                    if (elect_one()) {
+                        KTRACE(9 + 2 * t, it);
+                        issue_qk(t, it % L::KST);
+                        mma_commit(bar(L::B_SF + t));
+                    }
+                    __syncwarp();
+                }
             }
-            const int vs = it % L::VST;
-            mbar_wait(bar(L::B_VF + vs), (it / L::VST) & 1);
-            mbar_wait(bar(L::B_PF + b), ph);
-            tc_fence_after();
-            if (elect_one()) {
-                KTRACE(10, it);
-                issue_pv(vs, b, it > 0);
-                mma_commit(bar(L::B_PE + b));
-                mma_commit(bar(L::B_VE + vs));
-                if (it == n_used - 1) mma_commit(bar(L::B_O));
-                KTRACE(11, it);
-            }
+            if (!have) break;
+            if (elect_one()) mma_commit(bar(L::B_KE + it % L::KST));
             __syncwarp();
+            prev_kinds = kinds;
+            ++it;
+            ++j;
+            while (j < j_hi && sched[j] == 0) ++j;
         }
-    } else if (warp >= 4) {
-        // ================= softmax + epilogue =================
-        const int quad = warp & 3;       // TMEM lane quadrant: query rows 32*quad ..
-        const int cg = (warp - 4) >> 2;  // key columns 32*cg .. of each S tile; O columns 32*cg ..
+        if (elect_one()) {
+            mma_commit(bar(L::B_OF + 0));
+            mma_commit(bar(L::B_OF + 1));
+        }
+        __syncwarp();
+    } else if (warp < 4 * NQT) {
+        // ================= softmax + epilogue: thread = one query row of tile t =================
+        const int t = warp >> 2;
+        const int quad = warp & 3;  // TMEM lane quadrant
         const int r = quad * 32 + lane;
-        const int64_t row = row0 + r;
+        const int64_t row = row0 + t * BQ + r;
         const bool row_ok = row < sg.nq;
-        const int64_t my_qpos = row_ok ? seg_qpos(sg, row) : INT64_MAX;
+        const int64_t my_qpos = row_ok ? seg_qpos(sg, row) : (INT64_MAX >> 2);
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        const uint32_t tS = tmem + lane_off + COL_S + 32 * cg;
-        const uint32_t tP = tmem + lane_off + COL_P + 16 * cg;
-        const uint32_t tO = tmem + lane_off + COL_O + 32 * cg;
-        const bool owns_o = cg * 32 < HD;  // HD = 64: column groups 2, 3 own no O columns
+        const uint32_t tS = tmem + lane_off + col_s(t);
+        const uint32_t tO = tmem + lane_off + col_o(t);
         const float sl2 = p.scale_log2;
         float m = -INFINITY;
-        float2 lacc = make_float2(0.f, 0.f);
-        // mask (diagonal / ragged tiles) and this warp's 32-column row max of one S tile
-        auto mask_max = [&](uint32_t (&sv)[32], int j, int kind) {
-            if (kind == TILE_PARTIAL) {
-                const int64_t c0 = static_cast<int64_t>(j) * BN + 32 * cg;
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (!seg_visible(sg, c0 + i, my_qpos)) sv[i] = __float_as_uint(-INFINITY);
-            }
-            float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-                mx0 = fmaxf(mx0, __uint_as_float(sv[i]));
-                mx1 = fmaxf(mx1, __uint_as_float(sv[i + 1]));
-                mx2 = fmaxf(mx2, __uint_as_float(sv[i + 2]));
-                mx3 = fmaxf(mx3, __uint_as_float(sv[i + 3]));
-            }
-            return fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-        };
-        // row max over the four column groups of this lane quadrant (parity-double-buffered)
-        auto exchange_max = [&](float lmx, int parity) {
-            float* rq = red + ((parity * 4 + quad) * 32 + lane) * 4;
-            rq[cg] = lmx;
-            named_bar_sync(1 + quad, 128);
-            const float4 m4 = *reinterpret_cast<const float4*>(rq);
-            return fmaxf(fmaxf(m4.x, m4.y), fmaxf(m4.z, m4.w));
-        };
-        int it = 0;
+        float2 lacc0 = make_float2(0.f, 0.f), lacc1 = make_float2(0.f, 0.f);
+        int n = 0;
         for (int j = j_lo; j < j_hi; ++j) {
-            const int kind = sched[j];
+            const int kind = (sched[j] >> (2 * t)) & 3;
             if (kind == 0) continue;
-            const int b = it & 1;
-            const uint32_t ph = (it >> 1) & 1;
-            uint32_t s[32];
-            mbar_wait(bar(L::B_SF + b), ph);
-            if (lane == 0 && (warp == 4 || warp == 19)) KTRACE(warp == 4 ? 0 : 4, it);
+            uint32_t s[BN];
+            mbar_wait(bar(L::B_SF + t), n & 1);
+            if (lane == 0 && quad == 0) KTRACE(4 * t + 0, n);
             tc_fence_after();
-            tmem_ld32(tS + 128 * b, s);
-            tc_wait_ld_regs(s);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar(L::B_SE + b));  // S(b) may now be overwritten
-            if (threadIdx.x == 128 && it == 0) CTA_STAMP(5);
-            const float mx = exchange_max(mask_max(s, j, kind), it & 1);
-            if (lane == 0 && warp == 4) KTRACE(1, it);
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) tmem_ld32p(tS + 32 * c, s + 32 * c);
+            tc_wait_ld();
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) reg_tie32(s + 32 * c);
+            if (threadIdx.x == 0 && n == 0) CTA_STAMP(5);
+            if (kind == TILE_PARTIAL) mask_tile(s, sg, j, my_qpos);
+            float mx;
+            {
+                float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
+#pragma unroll
+                for (int i = 0; i < BN; i += 8) {
+                    a0 = fmaxf(a0, fmaxf(__uint_as_float(s[i + 0]), __uint_as_float(s[i + 1])));
+                    a1 = fmaxf(a1, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
+                    a2 = fmaxf(a2, fmaxf(__uint_as_float(s[i + 4]), __uint_as_float(s[i + 5])));
+                    a3 = fmaxf(a3, fmaxf(__uint_as_float(s[i + 6]), __uint_as_float(s[i + 7])));
+                }
+                mx = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+            }
             const float m_new = fmaxf(m, mx * sl2);
             const bool need = m_new > m + 8.0f;
-            if (__any_sync(0xFFFFFFFFu, need)) {
-                const float alpha = need ? ex2(m - m_new) : 1.0f;
-                if (need) {
-                    lacc.x *= alpha;
-                    lacc.y *= alpha;
-                    m = m_new;
-                }
-                if (it > 0 && owns_o) {  // O holds PV up to it-1: wait for it, rescale 32 columns
-                    mbar_wait(bar(L::B_PE + (b ^ 1)), ((it - 1) >> 1) & 1);
-                    tc_fence_after();
-                    uint32_t o[32];
-                    tmem_ld32(tO, o);
-                    tc_wait_ld_regs(o);
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                    tmem_st32(tO, o);
-                }
+            float alpha = 1.0f;
+            if (need) {
+                alpha = ex2(m - m_new);
+                lacc0.x *= alpha;
+                lacc0.y *= alpha;
+                lacc1.x *= alpha;
+                lacc1.y *= alpha;
+                m = m_new;
             }
+            if (lane == 0 && quad == 0) KTRACE(4 * t + 1, n);
             const float m_use = (m == -INFINITY) ? 0.f : m;
             const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m_use, -m_use);
-            uint32_t pk[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc, nm);
-                float2 pp;
-                if ((CDSP_EMU_MASK >> (i % 8)) & 1) {  // pairs on the FMA pipe (default 3/8: pairs 1, 4, 6 of 8)
-                    pp = ex2_fma2(x);
-                } else {
-                    pp.x = ex2(x.x);
-                    pp.y = ex2(x.y);
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float2 x =
+                        ffma2(make_float2(__uint_as_float(s[32 * c + 2 * i]), __uint_as_float(s[32 * c + 2 * i + 1])), sc, nm);
+                    float2 pp;
+                    if ((CDSP_EMU_MASK >> (i % 8)) & 1) {  // pairs on the FMA pipe (default 3/8)
+                        pp = ex2_fma2(x);
+                    } else {
+                        pp.x = ex2(x.x);
+                        pp.y = ex2(x.y);
+                    }
+                    if (i & 1) lacc1 = fadd2(lacc1, pp);
+                    else lacc0 = fadd2(lacc0, pp);
+                    pk[i] = pack_bf16(pp.x, pp.y);
                 }
-                lacc = fadd2(lacc, pp);
-                pk[i] = pack_bf16(pp.x, pp.y);
+                tmem_st16(tS + 16 * c, pk);  // P chunk c over S columns already in registers
             }
-            if (lane == 0 && warp == 4) KTRACE(2, it);
-            if (it >= 2) {  // P(b) must have been consumed by PV(it-2)
-                mbar_wait(bar(L::B_PE + b), ((it - 2) >> 1) & 1);
-                tc_fence_after();
+            if (lane == 0 && quad == 0) KTRACE(4 * t + 2, n);
+            // O_t holds PV_t up to the previous tile (committed before this S_t): rescale it
+            if (n > 0 && __any_sync(0xFFFFFFFFu, need)) {
+#pragma unroll 1
+                for (int c = 0; c < HD / 32; ++c) {
+                    uint32_t o[32];
+                    tmem_ld32p(tO + 32 * c, o);
+                    tc_wait_ld();
+                    reg_tie32(o);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                    tmem_st32(tO + 32 * c, o);
+                }
             }
-            tmem_st16(tP + 64 * b, pk);
             tc_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar(L::B_PF + b));
-            if (lane == 0 && (warp == 4 || warp == 19)) KTRACE(warp == 4 ? 3 : 5, it);
-            ++it;
+            if (lane == 0) mbar_arrive(bar(L::B_PF + t));
+            if (lane == 0 && quad == 0) KTRACE(4 * t + 3, n);
+            ++n;
         }
 
         // ---------------- epilogue: normalise, then write / LSE-merge (R3) ----------------
-        const int n_used = it;
-        if (threadIdx.x == 128) CTA_STAMP(6);
-        if (n_used > 0) {
-            mbar_wait(bar(L::B_O), 0);
-            tc_fence_after();
-        }
-        // row sum over the four column groups (all four hold the same running max); the
-        // exchange buffer of parity n_used is free: every warp of the quadrant passed the
-        // last max exchange (parity n_used - 1) before writing here
-        float* rs = red + (((n_used & 1) * 4 + quad) * 32 + lane) * 4;
-        rs[cg] = lacc.x + lacc.y;
-        named_bar_sync(1 + quad, 128);
-        const float4 l4 = *reinterpret_cast<const float4*>(rs);
-        const float l = (l4.x + l4.y) + (l4.z + l4.w);
+        if (threadIdx.x == 0) CTA_STAMP(6);
+        mbar_wait(bar(L::B_OF + t), 0);
+        tc_fence_after();
+        const float l = (lacc0.x + lacc0.y) + (lacc1.x + lacc1.y);
         const float inv_l = l > 0.f ? 1.0f / l : 0.f;
         const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
         const int64_t nq = sg.nq;
-        const size_t orow = (static_cast<size_t>(row_ok ? row : 0) * p.Hq + head) * HD + 32 * cg;
         float wa = 0.f, wb = 1.f, lse_out = lse_b;
-        if (p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST) {
+        const bool merge = p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST;
+        const bool to_acc = p.mode == CDSP_ATTN_FIRST || p.mode == CDSP_ATTN_MID;
+        if (merge) {
             const float lse_a = row_ok ? p.lse_acc[static_cast<size_t>(head) * nq + row] : -INFINITY;
             merge_weights(lse_a, lse_b, wa, wb, lse_out);
         }
         const float sbw = wb * inv_l;
-        uint32_t o[32];
-        if (n_used > 0 && owns_o) {
-            tmem_ld32(tO, o);
-            tc_wait_ld();
-        } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = 0u;
-        }
-        if (row_ok && owns_o) {
-            float v[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]) * sbw;
-            if (p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST) {
-                const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const float4 a = a4[i];
-                    v[4 * i + 0] = fmaf(wa, a.x, v[4 * i + 0]);
-                    v[4 * i + 1] = fmaf(wa, a.y, v[4 * i + 1]);
-                    v[4 * i + 2] = fmaf(wa, a.z, v[4 * i + 2]);
-                    v[4 * i + 3] = fmaf(wa, a.w, v[4 * i + 3]);
-                }
-            }
-            if (p.mode == CDSP_ATTN_FIRST || p.mode == CDSP_ATTN_MID) {
-                float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        const size_t orow = (static_cast<size_t>(row_ok ? row : 0) * p.Hq + head) * HD;
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            if (n > 0) {
+                tmem_ld32p(tO + 32 * c, o);
+                tc_wait_ld();
+                reg_tie32(o);
             } else {
-                uint4* d4 = reinterpret_cast<uint4*>(p.out + orow);
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    d4[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                                       pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+                for (int i = 0; i < 32; ++i) o[i] = 0u;
             }
-            if (cg == 0) {
-                const size_t li = static_cast<size_t>(head) * nq + row;
-                if (p.mode == CDSP_ATTN_FIRST || p.mode == CDSP_ATTN_MID) {
-                    p.lse_acc[li] = lse_out;
-                } else if (p.lse) {
-                    p.lse[li] = lse_out;
+            if (row_ok) {
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]) * sbw;
+                if (merge) {
+                    const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float4 a = a4[i];
+                        v[4 * i + 0] = fmaf(wa, a.x, v[4 * i + 0]);
+                        v[4 * i + 1] = fmaf(wa, a.y, v[4 * i + 1]);
+                        v[4 * i + 2] = fmaf(wa, a.z, v[4 * i + 2]);
+                        v[4 * i + 3] = fmaf(wa, a.w, v[4 * i + 3]);
+                    }
+                }
+                if (to_acc) {
+                    float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow + 32 * c);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                } else {
+                    uint4* d4 = reinterpret_cast<uint4*>(p.out + orow + 32 * c);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        d4[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                                           pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
                 }
             }
         }
-        if (threadIdx.x == 128) CTA_STAMP(7);
+        if (row_ok) {
+            const size_t li = static_cast<size_t>(head) * nq + row;
+            if (to_acc) {
+                p.lse_acc[li] = lse_out;
+            } else if (p.lse) {
+                p.lse[li] = lse_out;
+            }
+        }
+        if (threadIdx.x == 0) CTA_STAMP(7);
     }
 
 #ifdef CDSP_KTRACE
@@ -539,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- teardown
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == W_MMA) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
