@@ -10,30 +10,36 @@
 // B200 design (not the paper's A100 FlashAttention-2), from measurements on the box:
 //  * tcgen05.mma M=128 reaches the full 8192 FLOP/clk/SM only for N >= 128 (N=64: ~48 clk
 //    per K=16 step instead of 32; tools/mma_rate.cu), so S = Q K^T uses 128-key tiles.
+//    The issuing thread is paced by the tensor pipe (a group of 8 MMAs is accepted about
+//    when the previous group drains), so the MMA order below is the execution order.
 //  * MUFU.EX2 issues 16 lanes/clk/SM (tools/exp_rate.cu): the 16384 exponentials of a
-//    128x128 tile take 1024 clk, exactly the two MMAs of that tile.  3/8 of them therefore
-//    run as a cubic on the FMA pipe, and the softmax must spend almost no issue slots on
-//    anything else.  One thread owns one query row (all 128 columns of S in registers):
-//    the row max needs no cross-warp exchange and per-tile bookkeeping (waits, arrives,
-//    TMEM addressing) is paid by 4 warps per tile instead of 16.
-//  * one CTA = two 128-row query tiles (Q0, Q1) of one head, 11 warps:
-//      warps 0-3   softmax + epilogue of Q0 (warp w owns TMEM lanes 32*(w%4)..)
-//      warps 4-7   softmax + epilogue of Q1
-//      warp 8      TMA producer: Q0, Q1 once, then K tiles (2 stages)
+//    128x128 tile take 1024 clk, exactly the two MMAs of that tile, and TMEM reads run at
+//    ~64 B/clk per SM sub-partition (64 KB of S: ~256 clk).  The softmax of one tile is
+//    therefore longer than its MMAs; it must not sit on the tensor pipe's critical path.
+//  * one CTA = one 128-row query tile of one head, 11 warps:
+//      warps 0-3   softmax group 0: KV tiles 0, 2, 4, ... of the schedule
+//      warps 4-7   softmax group 1: KV tiles 1, 3, 5, ...
+//                  (warp w owns TMEM lanes 32*(w%4).., one thread = one query row holding
+//                  all 128 scores of the tile in registers)
+//      warp 8      TMA producer: Q once, then K tiles (3 stages)
 //      warp 9      TMA producer: V tiles (2 stages)
 //      warp 10     TMEM allocator + tcgen05.mma issuer (warp-uniform loop, one lane issues)
-//    The tensor pipe alternates [O0 += P0 V_{j-1}, S0 = Q0 K_j^T] and [O1 += P1 V_{j-1},
-//    S1 = Q1 K_j^T]: while it works for one query tile the other tile's softmax runs, so
-//    each softmax group has a full half-period (two MMAs) for its 128x128 tile.
-//  * TMEM (512 cols): O0 [0,128), O1 [128,256), S0 [256,384), S1 [384,512).  P (bf16) is
-//    written over its own S columns and is the A operand of PV straight from TMEM; the
-//    next S into those columns is issued after that PV on the same in-order tensor pipe.
-//    S_t(j) is committed after PV_t(j-1), so when the softmax sees S_t(j), O_t is stable.
-//  * lazy rescaling: the running max only moves when it grows by > 8 (log2 units); O is
-//    rescaled in TMEM after P is stored (registers of S are dead by then).
-//  * masks from segment descriptors: empty tiles are skipped per query tile, full tiles run
-//    mask-free, diagonal / ragged tiles build per-row 32-bit column masks from the three
-//    visible intervals (history, segment 0, segment 1).
+//  * TMEM (512 cols): O [0,128), S/P triple buffer [128,256) [256,384) [384,512).  P (bf16)
+//    is written over its own S columns and is the A operand of PV straight from TMEM.  The
+//    MMA order is S(0) S(1) S(2) | PV(0) S(3) | PV(1) S(4) | ...: S(n+3) reuses the buffer
+//    of P(n) right after PV(n) (same in-order pipe), so scores are always two tiles ahead
+//    and the two softmax groups overlap each other's exponentials.
+//  * the only serial link between consecutive tiles is the running row max m (online
+//    softmax): a group takes the row max of its own tile first, then m(n-1) from the other
+//    group through shared memory, publishes m(n) and only then runs the exponentials.
+//    Each group keeps its own row sum l (rescaled whenever m moves); the two are added in
+//    the epilogue.  Lazy rescaling: m only moves when it grows by > 8 (log2 units); O is
+//    then rescaled in TMEM after PV(n-1) completed and before m(n) is published.
+//  * 1/4 of the exponentials run as a cubic on the FMA pipe (rel. error 7.5e-5, far below
+//    bf16's 2^-9), packed fp32x2 FFMA2/FADD2.
+//  * masks from segment descriptors: empty tiles are skipped, full tiles run mask-free,
+//    diagonal / ragged tiles build per-row 32-bit column masks from the three visible
+//    intervals (history, segment 0, segment 1).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -46,8 +52,23 @@
 #include "internal.h"
 #include "ptx.cuh"
 
+// MMA issuer's barrier waits: spin (lowest latency) or sleep on the phase (frees issue slots
+// for the softmax warps sharing its SMSP)
+#ifndef CDSP_MMA_SPIN
+#define CDSP_MMA_SPIN 0
+#endif
+#if CDSP_MMA_SPIN
+#define MMA_WAIT mbar_wait_spin
+#else
+#define MMA_WAIT mbar_wait
+#endif
+
+#ifndef CDSP_VST  // V shared-memory stages (K has one per S buffer)
+#define CDSP_VST 2
+#endif
+
 #ifndef CDSP_EMU_MASK
-#define CDSP_EMU_MASK 0x52
+#define CDSP_EMU_MASK 0x22
 #endif
 
 namespace cdsp {
@@ -56,10 +77,9 @@ using namespace ptx;
 namespace {
 
 constexpr int kThreads = 352;           // 11 warps
-constexpr int BQ = 128;                 // rows per query tile (TMEM lanes)
-constexpr int NQT = 2;                  // query tiles per CTA
-constexpr int BM = BQ * NQT;            // query rows per CTA
+constexpr int BM = 128;                 // query rows per CTA (TMEM lanes)
 constexpr int BN = 128;                 // KV rows per tile
+constexpr int NSB = 3;                  // S/P buffers in TMEM
 constexpr int kBox = 128 * 128;         // TMA box: 128 rows x 64 bf16 (128-byte swizzle rows)
 constexpr int kSchedMax = 8192;         // KV tiles per launch (1M keys)
 constexpr int W_K = 8, W_V = 9, W_MMA = 10;
@@ -69,22 +89,28 @@ template <int HD>
 struct Layout {
     static constexpr int NBOX = HD / 64;
     static constexpr int TILE = kBox * NBOX;  // one 128-row tile of Q, K or V
-    static constexpr int KST = 2, VST = 2;
+    static constexpr int KST = 3, VST = CDSP_VST;  // KST == NSB: K stage n%3 is free once S(n) is
     static constexpr int OFF_Q = 0;
-    static constexpr int OFF_K = OFF_Q + NQT * TILE;
+    static constexpr int OFF_K = OFF_Q + TILE;
     static constexpr int OFF_V = OFF_K + KST * TILE;
-    static constexpr int OFF_BAR = OFF_V + VST * TILE;
-    // q_full[2], k_full[KST], k_empty[KST], v_full[VST], v_empty[VST], s_full[2], p_full[2], o_full[2]
-    static constexpr int B_Q = 0, B_KF = B_Q + NQT, B_KE = B_KF + KST, B_VF = B_KE + KST, B_VE = B_VF + VST,
-                         B_SF = B_VE + VST, B_PF = B_SF + NQT, B_OF = B_PF + NQT, NBAR = B_OF + NQT;
+    static constexpr int OFF_M = OFF_V + VST * TILE;       // running row max m(n): [2 parity][128] float
+    static constexpr int OFF_L = OFF_M + 2 * BM * 4;       // epilogue: per-group (m_used, l) [2][128] float2
+    static constexpr int OFF_BAR = OFF_L + 2 * BM * 8;
+    // q_full, k_full[KST], v_full[VST], v_empty[VST], s_full[NSB], p_full[NSB], m_ready[2],
+    // o_full.  Every tcgen05.commit costs the tensor pipe ~30 clk (tools/mma_pattern.cu), so
+    // each MMA group commits once: s_full[b] (S(n) done) also frees K stage n % 3, and
+    // v_empty[s] (PV(n) done) also tells a rescaling softmax group that O is stable.
+    static constexpr int B_Q = 0, B_KF = 1, B_VF = B_KF + KST, B_VE = B_VF + VST, B_SF = B_VE + VST,
+                         B_PF = B_SF + NSB, B_MR = B_PF + NSB, B_OF = B_MR + 2, NBAR = B_OF + 1;
+    static_assert(KST == NSB, "K stages are released through s_full");
     static constexpr int OFF_TMEM_SLOT = OFF_BAR + NBAR * 8;
     static constexpr int OFF_JR = OFF_TMEM_SLOT + 16;   // used-tile range per setup warp: (min, max+1)
     static constexpr int OFF_SCHED = OFF_JR + 8 * kSchedWarps;
     static constexpr int SMEM = OFF_SCHED + kSchedMax + 1024;  // + alignment slack
 };
 
-__host__ __device__ constexpr uint32_t col_o(int t) { return 128u * t; }
-__host__ __device__ constexpr uint32_t col_s(int t) { return 256u + 128u * t; }
+constexpr uint32_t COL_O = 0;
+__host__ __device__ constexpr uint32_t col_s(int b) { return 128u + 128u * b; }
 
 struct TcParams {
     cdsp_segments seg;
@@ -172,6 +198,12 @@ __device__ __forceinline__ void reg_tie32(uint32_t* r) {
                    "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
                    "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
 }
+__device__ __forceinline__ void reg_tie16(uint32_t* r) {
+    asm volatile(""
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]));
+}
 __device__ __forceinline__ void tmem_ld32p(uint32_t taddr, uint32_t* r) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -246,50 +278,44 @@ __global__ void __maxnreg__(168)
     const int kvh = head / p.g;
     const int64_t row0 = static_cast<int64_t>(rb) * BM;
     const int n_kv_tiles = static_cast<int>((sg.nkv + BN - 1) / BN);
-    const bool q1_rows = row0 + BQ < sg.nq;
 
     // ---- setup
     if (warp == W_K) {
         if (lane == 0) {
-            for (int t = 0; t < NQT; ++t) mbar_init(bar(L::B_Q + t), 1);
-            for (int i = 0; i < L::KST; ++i) {
-                mbar_init(bar(L::B_KF + i), 1);
-                mbar_init(bar(L::B_KE + i), 1);
-            }
+            mbar_init(bar(L::B_Q), 1);
+            for (int i = 0; i < L::KST; ++i) mbar_init(bar(L::B_KF + i), 1);
             for (int i = 0; i < L::VST; ++i) {
                 mbar_init(bar(L::B_VF + i), 1);
                 mbar_init(bar(L::B_VE + i), 1);
             }
-            for (int t = 0; t < NQT; ++t) {
-                mbar_init(bar(L::B_SF + t), 1);
-                mbar_init(bar(L::B_PF + t), 4);
-                mbar_init(bar(L::B_OF + t), 1);
+            for (int b = 0; b < NSB; ++b) {
+                mbar_init(bar(L::B_SF + b), 1);
+                mbar_init(bar(L::B_PF + b), 4);
             }
+            for (int i = 0; i < 2; ++i) {
+                mbar_init(bar(L::B_MR + i), BM);
+            }
+            mbar_init(bar(L::B_OF), 1);
             fence_barrier_init();
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
-            // Q does not depend on the schedule: start its loads now
-            for (int t = 0; t < (q1_rows ? 2 : 1); ++t) {
-                mbar_expect_tx(bar(L::B_Q + t), L::TILE);
-                for (int b = 0; b < L::NBOX; ++b)
-                    tma_load_3d(sQ + t * L::TILE + b * kBox, &tm_q, bar(L::B_Q + t), b * 64, head,
-                                static_cast<int>(row0 + t * BQ));
-            }
+            // Q does not depend on the schedule: start its load now
+            mbar_expect_tx(bar(L::B_Q), L::TILE);
+            for (int b = 0; b < L::NBOX; ++b)
+                tma_load_3d(sQ + b * kBox, &tm_q, bar(L::B_Q), b * 64, head, static_cast<int>(row0));
         }
     } else if (warp == W_MMA) {
         tmem_alloc(smem_u32(tmem_slot), 512);
         tmem_relinquish();
     } else if (warp < kSchedWarps) {
-        // KV-tile schedule: sched[j] = kind for Q0 | kind for Q1 << 2 (0 = skip)
-        int64_t qlo0, qhi0, qlo1, qhi1;
-        bool qany0, qany1;
-        seg_qrange(sg, row0, row0 + BQ, qlo0, qhi0, qany0);
-        seg_qrange(sg, row0 + BQ, row0 + BM, qlo1, qhi1, qany1);
+        // KV-tile schedule: sched[j] = tile kind (0 = skip)
+        int64_t qlo, qhi;
+        bool qany;
+        seg_qrange(sg, row0, row0 + BM, qlo, qhi, qany);
         int jmin = INT_MAX, jmax = 0;
         for (int j = warp * 32 + lane; j < n_kv_tiles; j += kSchedWarps * 32) {
-            const int64_t c0 = static_cast<int64_t>(j) * BN;
-            const int k = seg_tile_kind(sg, qany0, qlo0, qhi0, c0, BN) | (seg_tile_kind(sg, qany1, qlo1, qhi1, c0, BN) << 2);
+            const int k = seg_tile_kind(sg, qany, qlo, qhi, static_cast<int64_t>(j) * BN, BN);
             sched[j] = static_cast<uint8_t>(k);
             if (k != 0) {
                 jmin = min(jmin, j);
@@ -327,14 +353,15 @@ __global__ void __maxnreg__(168)
         const bool is_k = warp == W_K;
         const int nst = is_k ? L::KST : L::VST;
         const uint32_t s0 = is_k ? sK : sV;
-        const int bfull = is_k ? L::B_KF : L::B_VF, bempty = is_k ? L::B_KE : L::B_VE;
+        const int bfull = is_k ? L::B_KF : L::B_VF, bempty = is_k ? L::B_SF : L::B_VE;
         const void* map = is_k ? static_cast<const void*>(&tm_k) : static_cast<const void*>(&tm_v);
         const uint64_t pol_kv = policy_evict_last();
         int it = 0;
         for (int j = j_lo; j < j_hi; ++j) {
             if (sched[j] == 0) continue;
             const int st = it % nst;
-            mbar_wait(bar(bempty + st), ((it / nst) & 1) ^ 1);
+            // stage st last held tile it - nst: free once S(it - nst) (K) / PV(it - nst) (V) is done
+            if (it >= nst) mbar_wait(bar(bempty + st), ((it - nst) / nst) & 1);
             if (elect_one()) {
                 mbar_expect_tx(bar(bfull + st), L::TILE);
                 for (int b = 0; b < L::NBOX; ++b)
@@ -345,146 +372,188 @@ __global__ void __maxnreg__(168)
         }
     } else if (warp == W_MMA) {
         // ================= MMA issuer (warp-uniform loop, one lane issues) =================
-        constexpr uint32_t idesc_qk = idesc_bf16_f32(BQ, BN, false, false);
-        constexpr uint32_t idesc_pv = idesc_bf16_f32(BQ, HD, false, true);
-        const uint64_t dq0 = umma_desc_sw128(sQ, 16, 1024);
+        constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, false, false);
+        constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, HD, false, true);
+        const uint64_t dq = umma_desc_sw128(sQ, 16, 1024);
         const uint64_t dk0 = umma_desc_sw128(sK, 16, 1024);
         const uint64_t dv0 = umma_desc_sw128(sV, kBox, 1024);
-        // S_t = Q_t K^T: M=128, N=128, K=HD in steps of 16 (32 B inside a 128-B swizzle row)
-        auto issue_qk = [&](int t, int ks) {
+        // S(b) = Q K^T: M=128, N=128, K=HD in steps of 16 (32 B inside a 128-B swizzle row)
+        auto issue_qk = [&](int ks, int b) {
             const uint64_t dk = dk0 + static_cast<uint64_t>((ks * L::TILE) >> 4);
-            const uint64_t dq = dq0 + static_cast<uint64_t>((t * L::TILE) >> 4);
 #pragma unroll
             for (int kk = 0; kk < HD / 16; ++kk) {
                 const uint64_t off = static_cast<uint64_t>(((kk / 4) * kBox + (kk % 4) * 32) >> 4);
-                mma_ss(tmem + col_s(t), dq + off, dk + off, idesc_qk, kk > 0 ? 1u : 0u);
+                mma_ss(tmem + col_s(b), dq + off, dk + off, idesc_qk, kk > 0 ? 1u : 0u);
             }
         };
-        // O_t += P_t V: M=128, N=HD, K=128 keys in steps of 16 (V rows, 2048 B); P_t is bf16
-        // in the S_t columns (8 TMEM columns per 16 keys)
-        auto issue_pv = [&](int t, int vs, bool acc) {
+        // O += P(b) V: M=128, N=HD, K=128 keys in steps of 16 (V rows, 2048 B); P(b) is bf16
+        // in the S(b) columns (8 TMEM columns per 16 keys)
+        auto issue_pv = [&](int vs, int b, bool acc) {
             const uint64_t dv = dv0 + static_cast<uint64_t>((vs * L::TILE) >> 4);
 #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk)
-                mma_ts(tmem + col_o(t), tmem + col_s(t) + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4),
+                mma_ts(tmem + COL_O, tmem + col_s(b) + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4),
                        idesc_pv, (acc || kk > 0) ? 1u : 0u);
         };
-        // Iteration `it` (union tile j_it): for t = 0, 1: O_t += P_t(j_{it-1}) V_{it-1} (if
-        // query tile t used j_{it-1}), then S_t = Q_t K_{it}^T (if it uses j_it).  K stage it
-        // is released after its S's, V stage it-1 after its PVs (commit = all prior MMAs).
-        int pv0 = 0, pv1 = 0;      // PVs issued per query tile (P_full phases consumed)
-        bool q0 = false, q1 = false;
-        int prev_kinds = 0, it = 0;
-        int j = j_lo;
-        while (j < j_hi && sched[j] == 0) ++j;
-        for (;;) {
-            const bool have = j < j_hi;
-            const int kinds = have ? sched[j] : 0;
-            const int last_pv_t = (prev_kinds >> 2) ? 1 : 0;
-            bool k_waited = false, v_waited = false;
-#pragma unroll
-            for (int t = 0; t < NQT; ++t) {
-                if ((prev_kinds >> (2 * t)) & 3) {
-                    int& pv = t == 0 ? pv0 : pv1;
-                    mbar_wait(bar(L::B_PF + t), pv & 1);
-                    if (!v_waited) {
-                        mbar_wait(bar(L::B_VF + (it - 1) % L::VST), ((it - 1) / L::VST) & 1);
-                        v_waited = true;
-                    }
-                    tc_fence_after();
-                    if (elect_one()) {
-                        KTRACE(8 + 2 * t, it);
-                        issue_pv(t, (it - 1) % L::VST, pv > 0);
-                        if (t == last_pv_t) mma_commit(bar(L::B_VE + (it - 1) % L::VST));
-                    }
-                    __syncwarp();
-                    ++pv;
-                }
-                if ((kinds >> (2 * t)) & 3) {
-                    bool& qr = t == 0 ? q0 : q1;
-                    if (!qr) {
-                        mbar_wait(bar(L::B_Q + t), 0);
-                        qr = true;
-                    }
-                    if (!k_waited) {
-                        mbar_wait(bar(L::B_KF + it % L::KST), (it / L::KST) & 1);
-                        k_waited = true;
-                    }
-                    tc_fence_after();
-                    if (elect_one()) {
-                        KTRACE(9 + 2 * t, it);
-                        issue_qk(t, it % L::KST);
-                        mma_commit(bar(L::B_SF + t));
-                    }
-                    __syncwarp();
-                }
+        int n_used = 0;
+        for (int j = j_lo; j < j_hi; ++j) n_used += sched[j] != 0;
+        auto issue_s = [&](int n) {  // S(n) into buffer n % NSB; K stage n % KST
+            const int ks = n % L::KST;
+            MMA_WAIT(bar(L::B_KF + ks), (n / L::KST) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                KTRACE(9, n);
+                issue_qk(ks, n % NSB);
+                mma_commit(bar(L::B_SF + n % NSB));  // S(n) ready; K stage ks free
             }
-            if (!have) break;
-            if (elect_one()) mma_commit(bar(L::B_KE + it % L::KST));
             __syncwarp();
-            prev_kinds = kinds;
-            ++it;
-            ++j;
-            while (j < j_hi && sched[j] == 0) ++j;
+        };
+        if (n_used > 0) {
+            MMA_WAIT(bar(L::B_Q), 0);
+            for (int n = 0; n < NSB && n < n_used; ++n) issue_s(n);
         }
-        if (elect_one()) {
-            mma_commit(bar(L::B_OF + 0));
-            mma_commit(bar(L::B_OF + 1));
+        for (int n = 0; n < n_used; ++n) {
+            const int b = n % NSB, vs = n % L::VST;
+            MMA_WAIT(bar(L::B_VF + vs), (n / L::VST) & 1);
+            MMA_WAIT(bar(L::B_PF + b), (n / NSB) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                KTRACE(8, n);
+                issue_pv(vs, b, n > 0);
+                mma_commit(bar(L::B_VE + vs));  // V stage free; O includes PV(n)
+                if (n == n_used - 1) mma_commit(bar(L::B_OF));
+            }
+            __syncwarp();
+            if (n + NSB < n_used) issue_s(n + NSB);  // into the buffer P(n) just left
         }
-        __syncwarp();
-    } else if (warp < 4 * NQT) {
-        // ================= softmax + epilogue: thread = one query row of tile t =================
-        const int t = warp >> 2;
+        if (n_used == 0) {
+            if (elect_one()) mma_commit(bar(L::B_OF));
+            __syncwarp();
+        }
+    } else if (warp < 8) {
+        // ========= softmax group g (tiles n = g, g+2, ...): thread = one query row =========
+        const int g = warp >> 2;
         const int quad = warp & 3;  // TMEM lane quadrant
         const int r = quad * 32 + lane;
-        const int64_t row = row0 + t * BQ + r;
+        const int64_t row = row0 + r;
         const bool row_ok = row < sg.nq;
         const int64_t my_qpos = row_ok ? seg_qpos(sg, row) : (INT64_MAX >> 2);
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        const uint32_t tS = tmem + lane_off + col_s(t);
-        const uint32_t tO = tmem + lane_off + col_o(t);
+        const uint32_t tO = tmem + lane_off + COL_O;
+        float* msh = reinterpret_cast<float*>(smem + L::OFF_M);  // [2][BM]
         const float sl2 = p.scale_log2;
-        float m = -INFINITY;
+        float m = -INFINITY;       // m(n) of the last tile this thread has seen
+        float m_used = -INFINITY;  // max that this group's l is relative to
         float2 lacc0 = make_float2(0.f, 0.f), lacc1 = make_float2(0.f, 0.f);
         int n = 0;
         for (int j = j_lo; j < j_hi; ++j) {
-            const int kind = (sched[j] >> (2 * t)) & 3;
+            const int kind = sched[j];
             if (kind == 0) continue;
+            if ((n & 1) != g) {
+                ++n;
+                continue;
+            }
+            const int b = n % NSB;
+            const uint32_t tS = tmem + lane_off + col_s(b);
             uint32_t s[BN];
-            mbar_wait(bar(L::B_SF + t), n & 1);
-            if (lane == 0 && quad == 0) KTRACE(4 * t + 0, n);
+            mbar_wait(bar(L::B_SF + b), (n / NSB) & 1);
+            if (lane == 0 && quad == 0) KTRACE(4 * g + 0, n);
             tc_fence_after();
-#pragma unroll
-            for (int c = 0; c < BN / 32; ++c) tmem_ld32p(tS + 32 * c, s + 32 * c);
+#if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 0
+            // debug: MMA pipeline alone (no TMEM traffic from the softmax; results garbage)
+            if (n > 0) mbar_wait(bar(L::B_MR + ((n - 1) & 1)), ((n - 1) >> 1) & 1);
+            mbar_arrive(bar(L::B_MR + (n & 1)));
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(L::B_PF + b));
+            ++n;
+            continue;
+#endif
+            // columns 0-63, then 64-127 in flight while the first half's max is taken (the
+            // mask, when needed, goes over the whole tile first)
+            tmem_ld32p(tS, s);
+            tmem_ld32p(tS + 32, s + 32);
             tc_wait_ld();
-#pragma unroll
-            for (int c = 0; c < BN / 32; ++c) reg_tie32(s + 32 * c);
+            reg_tie32(s);
+            reg_tie32(s + 32);
+            tmem_ld32p(tS + 64, s + 64);
+            tmem_ld32p(tS + 96, s + 96);
             if (threadIdx.x == 0 && n == 0) CTA_STAMP(5);
-            if (kind == TILE_PARTIAL) mask_tile(s, sg, j, my_qpos);
-            float mx;
-            {
-                float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
+            float a[8];
 #pragma unroll
-                for (int i = 0; i < BN; i += 8) {
-                    a0 = fmaxf(a0, fmaxf(__uint_as_float(s[i + 0]), __uint_as_float(s[i + 1])));
-                    a1 = fmaxf(a1, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
-                    a2 = fmaxf(a2, fmaxf(__uint_as_float(s[i + 4]), __uint_as_float(s[i + 5])));
-                    a3 = fmaxf(a3, fmaxf(__uint_as_float(s[i + 6]), __uint_as_float(s[i + 7])));
+            for (int k = 0; k < 8; ++k) a[k] = -INFINITY;
+            if (kind == TILE_PARTIAL) {
+                tc_wait_ld();
+                reg_tie32(s + 64);
+                reg_tie32(s + 96);
+                mask_tile(s, sg, j, my_qpos);
+#pragma unroll
+                for (int i = 0; i < BN; i += 16)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        a[k] = fmaxf(a[k], fmaxf(__uint_as_float(s[i + 2 * k]), __uint_as_float(s[i + 2 * k + 1])));
+            } else {
+#pragma unroll
+                for (int i = 0; i < BN / 2; i += 16)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        a[k] = fmaxf(a[k], fmaxf(__uint_as_float(s[i + 2 * k]), __uint_as_float(s[i + 2 * k + 1])));
+                tc_wait_ld();
+                reg_tie32(s + 64);
+                reg_tie32(s + 96);
+#pragma unroll
+                for (int i = BN / 2; i < BN; i += 16)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        a[k] = fmaxf(a[k], fmaxf(__uint_as_float(s[i + 2 * k]), __uint_as_float(s[i + 2 * k + 1])));
+            }
+            const float mx =
+                fmaxf(fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])), fmaxf(fmaxf(a[4], a[5]), fmaxf(a[6], a[7]))) * sl2;
+            // ---- the serial link: m(n) = lazy max(m(n-1), rowmax(S(n))) ----
+            if (n > 0) {
+                mbar_wait(bar(L::B_MR + ((n - 1) & 1)), ((n - 1) >> 1) & 1);
+                m = msh[((n - 1) & 1) * BM + r];
+            }
+            const bool need = mx > m + 8.0f;
+            const float m_prev = m;
+            if (need) m = mx;
+            if (lane == 0 && quad == 0) KTRACE(4 * g + 1, n);
+            // O holds PV up to n-1 relative to m(n-1): rescale it once PV(n-1) completed, before
+            // m(n) is published (so no later PV can be issued meanwhile)
+            if (n > 0 && __any_sync(0xFFFFFFFFu, need)) {
+                mbar_wait(bar(L::B_VE + (n - 1) % L::VST), ((n - 1) / L::VST) & 1);  // PV(n-1) done
+                tc_fence_after();
+                const float alpha = need ? ex2(m_prev - m) : 1.0f;
+#pragma unroll 1
+                for (int c = 0; c < HD / 16; ++c) {
+                    uint32_t o[16];
+                    tmem_ld16(tO + 16 * c, o);
+                    tc_wait_ld();
+                    reg_tie16(o);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                    tmem_st16(tO + 16 * c, o);
                 }
-                mx = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
             }
-            const float m_new = fmaxf(m, mx * sl2);
-            const bool need = m_new > m + 8.0f;
-            float alpha = 1.0f;
-            if (need) {
-                alpha = ex2(m - m_new);
-                lacc0.x *= alpha;
-                lacc0.y *= alpha;
-                lacc1.x *= alpha;
-                lacc1.y *= alpha;
-                m = m_new;
+            msh[(n & 1) * BM + r] = m;
+            mbar_arrive(bar(L::B_MR + (n & 1)));
+#if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 1
+            // debug: S read + row max only, no exponentials / P stores
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(L::B_PF + b));
+            ++n;
+            continue;
+#endif
+            // this group's row sum follows m
+            if (m != m_used) {
+                const float beta = ex2(m_used - m);  // m_used = -inf: l is 0 anyway
+                lacc0.x *= beta;
+                lacc0.y *= beta;
+                lacc1.x *= beta;
+                lacc1.y *= beta;
+                m_used = m;
             }
-            if (lane == 0 && quad == 0) KTRACE(4 * t + 1, n);
             const float m_use = (m == -INFINITY) ? 0.f : m;
             const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m_use, -m_use);
 #pragma unroll
@@ -495,7 +564,7 @@ __global__ void __maxnreg__(168)
                     const float2 x =
                         ffma2(make_float2(__uint_as_float(s[32 * c + 2 * i]), __uint_as_float(s[32 * c + 2 * i + 1])), sc, nm);
                     float2 pp;
-                    if ((CDSP_EMU_MASK >> (i % 8)) & 1) {  // pairs on the FMA pipe (default 3/8)
+                    if ((CDSP_EMU_MASK >> (i % 8)) & 1) {  // pairs on the FMA pipe (default 1/4)
                         pp = ex2_fma2(x);
                     } else {
                         pp.x = ex2(x.x);
@@ -507,33 +576,34 @@ __global__ void __maxnreg__(168)
                 }
                 tmem_st16(tS + 16 * c, pk);  // P chunk c over S columns already in registers
             }
-            if (lane == 0 && quad == 0) KTRACE(4 * t + 2, n);
-            // O_t holds PV_t up to the previous tile (committed before this S_t): rescale it
-            if (n > 0 && __any_sync(0xFFFFFFFFu, need)) {
-#pragma unroll 1
-                for (int c = 0; c < HD / 32; ++c) {
-                    uint32_t o[32];
-                    tmem_ld32p(tO + 32 * c, o);
-                    tc_wait_ld();
-                    reg_tie32(o);
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                    tmem_st32(tO + 32 * c, o);
-                }
-            }
+            if (lane == 0 && quad == 0) KTRACE(4 * g + 2, n);
             tc_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar(L::B_PF + t));
-            if (lane == 0 && quad == 0) KTRACE(4 * t + 3, n);
+            if (lane == 0) mbar_arrive(bar(L::B_PF + b));
+            if (lane == 0 && quad == 0) KTRACE(4 * g + 3, n);
             ++n;
         }
+        const int n_used = n;
 
         // ---------------- epilogue: normalise, then write / LSE-merge (R3) ----------------
         if (threadIdx.x == 0) CTA_STAMP(6);
-        mbar_wait(bar(L::B_OF + t), 0);
+        // final m = m(n_used-1); combine the two groups' row sums relative to it
+        float2* lsh = reinterpret_cast<float2*>(smem + L::OFF_L);  // [2][BM] (m_used, l)
+        lsh[g * BM + r] = make_float2(m_used, (lacc0.x + lacc0.y) + (lacc1.x + lacc1.y));
+        if (n_used > 0) {
+            mbar_wait(bar(L::B_MR + ((n_used - 1) & 1)), ((n_used - 1) >> 1) & 1);
+            m = msh[((n_used - 1) & 1) * BM + r];
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // both groups' (m_used, l) visible
+        float l = 0.f;
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg) {
+            const float2 ml = lsh[gg * BM + r];
+            if (ml.y > 0.f) l += ml.y * ex2(ml.x - m);
+        }
+        mbar_wait(bar(L::B_OF), 0);
         tc_fence_after();
-        const float l = (lacc0.x + lacc0.y) + (lacc1.x + lacc1.y);
         const float inv_l = l > 0.f ? 1.0f / l : 0.f;
         const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
         const int64_t nq = sg.nq;
@@ -546,10 +616,11 @@ __global__ void __maxnreg__(168)
         }
         const float sbw = wb * inv_l;
         const size_t orow = (static_cast<size_t>(row_ok ? row : 0) * p.Hq + head) * HD;
+        // group g writes O columns [g*HD/2, (g+1)*HD/2)
 #pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
+        for (int c = g * (HD / 64); c < (g + 1) * (HD / 64); ++c) {
             uint32_t o[32];
-            if (n > 0) {
+            if (n_used > 0) {
                 tmem_ld32p(tO + 32 * c, o);
                 tc_wait_ld();
                 reg_tie32(o);
@@ -565,11 +636,11 @@ __global__ void __maxnreg__(168)
                     const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const float4 a = a4[i];
-                        v[4 * i + 0] = fmaf(wa, a.x, v[4 * i + 0]);
-                        v[4 * i + 1] = fmaf(wa, a.y, v[4 * i + 1]);
-                        v[4 * i + 2] = fmaf(wa, a.z, v[4 * i + 2]);
-                        v[4 * i + 3] = fmaf(wa, a.w, v[4 * i + 3]);
+                        const float4 av = a4[i];
+                        v[4 * i + 0] = fmaf(wa, av.x, v[4 * i + 0]);
+                        v[4 * i + 1] = fmaf(wa, av.y, v[4 * i + 1]);
+                        v[4 * i + 2] = fmaf(wa, av.z, v[4 * i + 2]);
+                        v[4 * i + 3] = fmaf(wa, av.w, v[4 * i + 3]);
                     }
                 }
                 if (to_acc) {
@@ -585,7 +656,7 @@ __global__ void __maxnreg__(168)
                 }
             }
         }
-        if (row_ok) {
+        if (row_ok && g == 0) {
             const size_t li = static_cast<size_t>(head) * nq + row;
             if (to_acc) {
                 p.lse_acc[li] = lse_out;

@@ -58,11 +58,35 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parit
 }
 // Wait for the phase with parity `parity` to complete.  A watchdog traps after ~4 s so a
 // protocol bug fails the launch instead of hanging the GPU.
+#ifndef CDSP_WAIT_SLEEP
+#define CDSP_WAIT_SLEEP 1
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
+#if !CDSP_WAIT_SLEEP
+    {
+        const uint64_t t0 = globaltimer();
+        uint32_t n = 0;
+        while (!mbar_try_wait(bar, parity)) {
+            if ((++n & 1023u) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+        }
+        return;
+    }
+#endif
     const uint64_t t0 = globaltimer();
+    uint32_t n = 0;
     while (!mbar_try_wait_sleep(bar, parity)) {
-        if (globaltimer() - t0 > 4000000000ull) __trap();
+        if ((++n & 255u) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+    }
+}
+// Same, without the suspend hint: lowest wake-up latency, for a latency-critical waiter
+// (the MMA issuer) whose spinning costs one warp's issue slots.
+__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
+    if (mbar_try_wait(bar, parity)) return;
+    const uint64_t t0 = globaltimer();
+    uint32_t n = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if ((++n & 1023u) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
     }
 }
 
