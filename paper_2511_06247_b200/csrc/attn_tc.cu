@@ -35,8 +35,13 @@
 //    Each group keeps its own row sum l (rescaled whenever m moves); the two are added in
 //    the epilogue.  Lazy rescaling: m only moves when it grows by > 8 (log2 units); O is
 //    then rescaled in TMEM after PV(n-1) completed and before m(n) is published.
-//  * 1/4 of the exponentials run as a cubic on the FMA pipe (rel. error 7.5e-5, far below
-//    bf16's 2^-9), packed fp32x2 FFMA2/FADD2.
+//  * 1/8 of the exponentials run as a cubic on the FMA pipe (rel. error 7.5e-5, far below
+//    bf16's 2^-9), packed fp32x2 FFMA2/FADD2.  Under sustained load the B200 sits at its
+//    ~1000 W cap (SM clock ~1.5 GHz, tools/clock_probe.py), so energy per tile matters as much
+//    as clocks per tile: 1/8 measured best sustained (1/4: -3.5%, 3/8: -3%, none: -1%).
+//  * one score tile is 128 fp32 registers; holding it whole spilled loop state whose reloads
+//    queue behind MUFU traffic, so a thread keeps 64 scores: columns 64-127 are read for the
+//    row max, 0-63 for max + exponentials, and 64-127 again for theirs.
 //  * masks from segment descriptors: empty tiles are skipped, full tiles run mask-free,
 //    diagonal / ragged tiles build per-row 32-bit column masks from the three visible
 //    intervals (history, segment 0, segment 1).
@@ -68,7 +73,7 @@
 #endif
 
 #ifndef CDSP_EMU_MASK
-#define CDSP_EMU_MASK 0x22
+#define CDSP_EMU_MASK 0x02
 #endif
 
 namespace cdsp {
@@ -95,17 +100,18 @@ struct Layout {
     static constexpr int OFF_V = OFF_K + KST * TILE;
     static constexpr int OFF_M = OFF_V + VST * TILE;       // running row max m(n): [2 parity][128] float
     static constexpr int OFF_L = OFF_M + 2 * BM * 4;       // epilogue: per-group (m_used, l) [2][128] float2
-    static constexpr int OFF_BAR = OFF_L + 2 * BM * 8;
-    // q_full, k_full[KST], v_full[VST], v_empty[VST], s_full[NSB], p_full[NSB], m_ready[2],
-    // o_full.  Every tcgen05.commit costs the tensor pipe ~30 clk (tools/mma_pattern.cu), so
+    static constexpr int OFF_QP = OFF_L + 2 * BM * 8;      // query position per row: [128] int64
+    static constexpr int OFF_BAR = OFF_QP + BM * 8;
+    // q_full, k_full[KST], v_full[VST], v_empty[VST], s_full[NSB], p_full[NSB], o_full.
+    // (m(n) goes from one softmax group to the other through named barriers 2, 3.)  Every tcgen05.commit costs the tensor pipe ~30 clk (tools/mma_pattern.cu), so
     // each MMA group commits once: s_full[b] (S(n) done) also frees K stage n % 3, and
     // v_empty[s] (PV(n) done) also tells a rescaling softmax group that O is stable.
     static constexpr int B_Q = 0, B_KF = 1, B_VF = B_KF + KST, B_VE = B_VF + VST, B_SF = B_VE + VST,
-                         B_PF = B_SF + NSB, B_MR = B_PF + NSB, B_OF = B_MR + 2, NBAR = B_OF + 1;
+                         B_PF = B_SF + NSB, B_OF = B_PF + NSB, NBAR = B_OF + 1;
     static_assert(KST == NSB, "K stages are released through s_full");
     static constexpr int OFF_TMEM_SLOT = OFF_BAR + NBAR * 8;
     static constexpr int OFF_JR = OFF_TMEM_SLOT + 16;   // used-tile range per setup warp: (min, max+1)
-    static constexpr int OFF_SCHED = OFF_JR + 8 * kSchedWarps;
+    static constexpr int OFF_SCHED = OFF_JR + 12 * kSchedWarps;
     static constexpr int SMEM = OFF_SCHED + kSchedMax + 1024;  // + alignment slack
 };
 
@@ -188,6 +194,13 @@ __device__ __forceinline__ float2 ex2_fma2(float2 x) {
                        __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
 }
 
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // Registers loaded by tcgen05.ld are only valid after tcgen05.wait::ld; tying them to an
 // (empty) volatile asm after the wait keeps their uses below it.
 __device__ __forceinline__ void reg_tie32(uint32_t* r) {
@@ -203,6 +216,11 @@ __device__ __forceinline__ void reg_tie16(uint32_t* r) {
                  : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
                    "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
                    "+r"(r[15]));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
 }
 __device__ __forceinline__ void tmem_ld32p(uint32_t taddr, uint32_t* r) {
     asm volatile(
@@ -226,10 +244,13 @@ __device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
     return hm & ~((1u << l) - 1u);
 }
 
-// Mask a partial tile: the KV rows of tile j visible to a query at position qpos are the
-// union of [0, b0) (history), [a1, b1) (segment 0 rows with pos <= qpos) and [a2, b2)
-// (segment 1 rows with pos <= qpos), tile-relative — seg_visible() written as intervals.
-__device__ __forceinline__ void mask_tile(uint32_t* s, const cdsp_segments& sg, int j, int64_t qpos) {
+// Mask columns [col0, col0 + 32*NW) of a partial tile (s[0] = column col0): the KV rows of
+// tile j visible to a query at position qpos are the union of [0, b0) (history), [a1, b1)
+// (segment 0 rows with pos <= qpos) and [a2, b2) (segment 1 rows with pos <= qpos),
+// tile-relative — seg_visible() written as intervals.
+template <int NW>
+__device__ __forceinline__ void mask_cols(uint32_t* s, const cdsp_segments& sg, int j, int64_t qpos, int col0) {
+    asm volatile("" : "+l"(qpos));  // keep this arithmetic on the (rare) partial-tile path
     const int64_t c0 = static_cast<int64_t>(j) * BN;
     const int nk = clamp_bn(sg.nkv - c0);
     const int h = clamp_bn(sg.kv_hist - c0);
@@ -241,11 +262,47 @@ __device__ __forceinline__ void mask_tile(uint32_t* s, const cdsp_segments& sg, 
     const int a1 = h, b1 = min(min(e0, lim0), nk);
     const int a2 = e0, b2 = min(nk, lim1);
 #pragma unroll
-    for (int w = 0; w < BN / 32; ++w) {
-        const uint32_t mk = range_bits(0, b0, 32 * w) | range_bits(a1, b1, 32 * w) | range_bits(a2, b2, 32 * w);
+    for (int w = 0; w < NW; ++w) {
+        const int base = col0 + 32 * w;
+        const uint32_t mk = range_bits(0, b0, base) | range_bits(a1, b1, base) | range_bits(a2, b2, base);
 #pragma unroll
         for (int i = 0; i < 32; ++i)
             if (!((mk >> i) & 1u)) s[32 * w + i] = __float_as_uint(-INFINITY);
+    }
+}
+
+__device__ __forceinline__ float max64(const uint32_t* s) {
+    float a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fmaxf(__uint_as_float(s[2 * k]), __uint_as_float(s[2 * k + 1]));
+#pragma unroll
+    for (int i = 16; i < 64; i += 16)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = fmaxf(a[k], fmaxf(__uint_as_float(s[i + 2 * k]), __uint_as_float(s[i + 2 * k + 1])));
+    return fmaxf(fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])), fmaxf(fmaxf(a[4], a[5]), fmaxf(a[6], a[7])));
+}
+
+// p = 2^(s*sl2 - m) for 32 scores -> 16 bf16 pairs stored to TMEM columns tP .. tP+15 (two
+// tcgen05.st x8); row sum accumulated in lacc.  Pairs selected by CDSP_EMU_MASK run on the FMA pipe.
+__device__ __forceinline__ void exp32_store(const uint32_t* s, float2 sc, float2 nm, float2& lacc, uint32_t tP) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int ii = 0; ii < 8; ++ii) {
+            const int i = 8 * h + ii;
+            const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc, nm);
+            float2 pp;
+            if ((CDSP_EMU_MASK >> (i % 8)) & 1) {
+                pp = ex2_fma2(x);
+            } else {
+                pp.x = ex2(x.x);
+                pp.y = ex2(x.y);
+            }
+            lacc = fadd2(lacc, pp);
+            pk[ii] = pack_bf16(pp.x, pp.y);
+        }
+        tmem_st8(tP + 8 * h, pk);
     }
 }
 
@@ -292,9 +349,6 @@ __global__ void __maxnreg__(168)
                 mbar_init(bar(L::B_SF + b), 1);
                 mbar_init(bar(L::B_PF + b), 4);
             }
-            for (int i = 0; i < 2; ++i) {
-                mbar_init(bar(L::B_MR + i), BM);
-            }
             mbar_init(bar(L::B_OF), 1);
             fence_barrier_init();
             tma_prefetch_desc(&tm_q);
@@ -313,36 +367,40 @@ __global__ void __maxnreg__(168)
         int64_t qlo, qhi;
         bool qany;
         seg_qrange(sg, row0, row0 + BM, qlo, qhi, qany);
-        int jmin = INT_MAX, jmax = 0;
+        int jmin = INT_MAX, jmax = 0, cnt = 0;
         for (int j = warp * 32 + lane; j < n_kv_tiles; j += kSchedWarps * 32) {
             const int k = seg_tile_kind(sg, qany, qlo, qhi, static_cast<int64_t>(j) * BN, BN);
             sched[j] = static_cast<uint8_t>(k);
             if (k != 0) {
                 jmin = min(jmin, j);
                 jmax = max(jmax, j + 1);
+                ++cnt;
             }
         }
         for (int o = 16; o > 0; o >>= 1) {
             jmin = min(jmin, __shfl_xor_sync(0xFFFFFFFFu, jmin, o));
             jmax = max(jmax, __shfl_xor_sync(0xFFFFFFFFu, jmax, o));
+            cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
         }
         if (lane == 0) {
-            reinterpret_cast<int*>(smem + L::OFF_JR)[2 * warp] = jmin;
-            reinterpret_cast<int*>(smem + L::OFF_JR)[2 * warp + 1] = jmax;
+            reinterpret_cast<int*>(smem + L::OFF_JR)[3 * warp] = jmin;
+            reinterpret_cast<int*>(smem + L::OFF_JR)[3 * warp + 1] = jmax;
+            reinterpret_cast<int*>(smem + L::OFF_JR)[3 * warp + 2] = cnt;
         }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    // the used KV tiles lie in [j_lo, j_hi) (sched[j] == 0 marks skipped tiles inside it)
-    int j_lo = INT_MAX, j_hi = 0;
+    // the n_used used KV tiles lie in [j_lo, j_hi) (sched[j] == 0 marks skipped tiles inside)
+    int j_lo = INT_MAX, j_hi = 0, n_used = 0;
     {
         const int* jr = reinterpret_cast<const int*>(smem + L::OFF_JR);
 #pragma unroll
         for (int w = 0; w < kSchedWarps; ++w) {
-            j_lo = min(j_lo, jr[2 * w]);
-            j_hi = max(j_hi, jr[2 * w + 1]);
+            j_lo = min(j_lo, jr[3 * w]);
+            j_hi = max(j_hi, jr[3 * w + 1]);
+            n_used += jr[3 * w + 2];
         }
     }
     if (threadIdx.x == 0) CTA_STAMP(4);
@@ -395,8 +453,6 @@ __global__ void __maxnreg__(168)
                 mma_ts(tmem + COL_O, tmem + col_s(b) + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4),
                        idesc_pv, (acc || kk > 0) ? 1u : 0u);
         };
-        int n_used = 0;
-        for (int j = j_lo; j < j_hi; ++j) n_used += sched[j] != 0;
         auto issue_s = [&](int n) {  // S(n) into buffer n % NSB; K stage n % KST
             const int ks = n % L::KST;
             MMA_WAIT(bar(L::B_KF + ks), (n / L::KST) & 1);
@@ -437,81 +493,66 @@ __global__ void __maxnreg__(168)
         const int r = quad * 32 + lane;
         const int64_t row = row0 + r;
         const bool row_ok = row < sg.nq;
-        const int64_t my_qpos = row_ok ? seg_qpos(sg, row) : (INT64_MAX >> 2);
+        // the row's query position is only needed on partial tiles: keep it out of registers
+        int64_t* qpos_sh = reinterpret_cast<int64_t*>(smem + L::OFF_QP);
+        if (g == 0) qpos_sh[r] = row_ok ? seg_qpos(sg, row) : (INT64_MAX >> 2);
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
         const uint32_t tO = tmem + lane_off + COL_O;
         float* msh = reinterpret_cast<float*>(smem + L::OFF_M);  // [2][BM]
         const float sl2 = p.scale_log2;
         float m = -INFINITY;       // m(n) of the last tile this thread has seen
         float m_used = -INFINITY;  // max that this group's l is relative to
-        float2 lacc0 = make_float2(0.f, 0.f), lacc1 = make_float2(0.f, 0.f);
-        int n = 0;
-        for (int j = j_lo; j < j_hi; ++j) {
+        float2 lacc = make_float2(0.f, 0.f);
+        // group g takes used tiles n = g, g+2, ...; jc = KV tile index of tile n
+        auto next_used = [&](int jj) {
+            ++jj;
+            while (jj < j_hi && sched[jj] == 0) ++jj;
+            return jj;
+        };
+        int jc = j_lo;
+        if (g == 1 && n_used > 1) jc = next_used(jc);
+        for (int n = g; n < n_used; n += 2, jc = next_used(next_used(jc))) {
+            const int j = jc;
             const int kind = sched[j];
-            if (kind == 0) continue;
-            if ((n & 1) != g) {
-                ++n;
-                continue;
-            }
             const int b = n % NSB;
             const uint32_t tS = tmem + lane_off + col_s(b);
-            uint32_t s[BN];
+            if (lane == 0 && quad == 0) KTRACE(12 + g, n);
             mbar_wait(bar(L::B_SF + b), (n / NSB) & 1);
             if (lane == 0 && quad == 0) KTRACE(4 * g + 0, n);
             tc_fence_after();
 #if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 0
             // debug: MMA pipeline alone (no TMEM traffic from the softmax; results garbage)
-            if (n > 0) mbar_wait(bar(L::B_MR + ((n - 1) & 1)), ((n - 1) >> 1) & 1);
-            mbar_arrive(bar(L::B_MR + (n & 1)));
+            if (n > 0) named_bar_sync(2 + ((n - 1) & 1), 2 * BM);
+            named_bar_arrive(2 + (n & 1), 2 * BM);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(L::B_PF + b));
-            ++n;
             continue;
 #endif
-            // columns 0-63, then 64-127 in flight while the first half's max is taken (the
-            // mask, when needed, goes over the whole tile first)
+            // 64 score registers: columns 64-127 first (max only), then 0-63 (max, kept for the
+            // exponentials); 64-127 are re-read from TMEM for their exponentials (P(n) only ever
+            // overwrites S columns 0-63)
+            uint32_t s[64];
+            tmem_ld32p(tS + 64, s);
+            tmem_ld32p(tS + 96, s + 32);
+            tc_wait_ld();
+            reg_tie32(s);
+            reg_tie32(s + 32);
+            if (threadIdx.x == 0 && n == 0) CTA_STAMP(5);
+            const bool partial = kind == TILE_PARTIAL;
+            if (partial) mask_cols<2>(s, sg, j, qpos_sh[r], 64);
+            const float mx_hi = max64(s);
             tmem_ld32p(tS, s);
             tmem_ld32p(tS + 32, s + 32);
             tc_wait_ld();
             reg_tie32(s);
             reg_tie32(s + 32);
-            tmem_ld32p(tS + 64, s + 64);
-            tmem_ld32p(tS + 96, s + 96);
-            if (threadIdx.x == 0 && n == 0) CTA_STAMP(5);
-            float a[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) a[k] = -INFINITY;
-            if (kind == TILE_PARTIAL) {
-                tc_wait_ld();
-                reg_tie32(s + 64);
-                reg_tie32(s + 96);
-                mask_tile(s, sg, j, my_qpos);
-#pragma unroll
-                for (int i = 0; i < BN; i += 16)
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        a[k] = fmaxf(a[k], fmaxf(__uint_as_float(s[i + 2 * k]), __uint_as_float(s[i + 2 * k + 1])));
-            } else {
-#pragma unroll
-                for (int i = 0; i < BN / 2; i += 16)
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        a[k] = fmaxf(a[k], fmaxf(__uint_as_float(s[i + 2 * k]), __uint_as_float(s[i + 2 * k + 1])));
-                tc_wait_ld();
-                reg_tie32(s + 64);
-                reg_tie32(s + 96);
-#pragma unroll
-                for (int i = BN / 2; i < BN; i += 16)
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        a[k] = fmaxf(a[k], fmaxf(__uint_as_float(s[i + 2 * k]), __uint_as_float(s[i + 2 * k + 1])));
-            }
-            const float mx =
-                fmaxf(fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])), fmaxf(fmaxf(a[4], a[5]), fmaxf(a[6], a[7]))) * sl2;
+            if (partial) mask_cols<2>(s, sg, j, qpos_sh[r], 0);
+            const float mx = fmaxf(mx_hi, max64(s)) * sl2;
             // ---- the serial link: m(n) = lazy max(m(n-1), rowmax(S(n))) ----
-            if (n > 0) {
-                mbar_wait(bar(L::B_MR + ((n - 1) & 1)), ((n - 1) >> 1) & 1);
+            if (n > 0) {  // m(n-1) from the other group (named barrier 2 + parity: 128 + 128 threads)
+                named_bar_sync(2 + ((n - 1) & 1), 2 * BM);
                 m = msh[((n - 1) & 1) * BM + r];
             }
             const bool need = mx > m + 8.0f;
@@ -536,63 +577,53 @@ __global__ void __maxnreg__(168)
                 }
             }
             msh[(n & 1) * BM + r] = m;
-            mbar_arrive(bar(L::B_MR + (n & 1)));
+            __threadfence_block();
+            named_bar_arrive(2 + (n & 1), 2 * BM);
 #if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 1
             // debug: S read + row max only, no exponentials / P stores
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(L::B_PF + b));
-            ++n;
             continue;
 #endif
             // this group's row sum follows m
             if (m != m_used) {
                 const float beta = ex2(m_used - m);  // m_used = -inf: l is 0 anyway
-                lacc0.x *= beta;
-                lacc0.y *= beta;
-                lacc1.x *= beta;
-                lacc1.y *= beta;
+                lacc.x *= beta;
+                lacc.y *= beta;
                 m_used = m;
             }
             const float m_use = (m == -INFINITY) ? 0.f : m;
             const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m_use, -m_use);
-#pragma unroll
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t pk[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float2 x =
-                        ffma2(make_float2(__uint_as_float(s[32 * c + 2 * i]), __uint_as_float(s[32 * c + 2 * i + 1])), sc, nm);
-                    float2 pp;
-                    if ((CDSP_EMU_MASK >> (i % 8)) & 1) {  // pairs on the FMA pipe (default 1/4)
-                        pp = ex2_fma2(x);
-                    } else {
-                        pp.x = ex2(x.x);
-                        pp.y = ex2(x.y);
-                    }
-                    if (i & 1) lacc1 = fadd2(lacc1, pp);
-                    else lacc0 = fadd2(lacc0, pp);
-                    pk[i] = pack_bf16(pp.x, pp.y);
-                }
-                tmem_st16(tS + 16 * c, pk);  // P chunk c over S columns already in registers
-            }
+            // keys 0-63 from registers -> P columns 0-31; keys 64-127 re-read in two pieces,
+            // each load in flight behind the previous piece's exponentials
+            exp32_store(s, sc, nm, lacc, tS);
+            tmem_ld32p(tS + 64, s);
+            exp32_store(s + 32, sc, nm, lacc, tS + 16);
+            tc_wait_ld();
+            reg_tie32(s);
+            tmem_ld32p(tS + 96, s + 32);
+            if (partial) mask_cols<1>(s, sg, j, qpos_sh[r], 64);
+            exp32_store(s, sc, nm, lacc, tS + 32);
+            tc_wait_ld();
+            reg_tie32(s + 32);
+            if (partial) mask_cols<1>(s + 32, sg, j, qpos_sh[r], 96);
+            exp32_store(s + 32, sc, nm, lacc, tS + 48);
             if (lane == 0 && quad == 0) KTRACE(4 * g + 2, n);
             tc_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(L::B_PF + b));
             if (lane == 0 && quad == 0) KTRACE(4 * g + 3, n);
-            ++n;
         }
-        const int n_used = n;
 
         // ---------------- epilogue: normalise, then write / LSE-merge (R3) ----------------
         if (threadIdx.x == 0) CTA_STAMP(6);
         // final m = m(n_used-1); combine the two groups' row sums relative to it
         float2* lsh = reinterpret_cast<float2*>(smem + L::OFF_L);  // [2][BM] (m_used, l)
-        lsh[g * BM + r] = make_float2(m_used, (lacc0.x + lacc0.y) + (lacc1.x + lacc1.y));
-        if (n_used > 0) {
-            mbar_wait(bar(L::B_MR + ((n_used - 1) & 1)), ((n_used - 1) >> 1) & 1);
+        lsh[g * BM + r] = make_float2(m_used, lacc.x + lacc.y);
+        if (n_used > 0 && ((n_used - 1) & 1) != g) {  // the other group made the last m: take it
+            named_bar_sync(2 + ((n_used - 1) & 1), 2 * BM);  // (pairs with its last arrive)
             m = msh[((n_used - 1) & 1) * BM + r];
         }
         asm volatile("bar.sync 1, 256;" ::: "memory");  // both groups' (m_used, l) visible

@@ -63,30 +63,34 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parit
 #endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
-#if !CDSP_WAIT_SLEEP
-    {
-        const uint64_t t0 = globaltimer();
-        uint32_t n = 0;
-        while (!mbar_try_wait(bar, parity)) {
-            if ((++n & 1023u) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
-        }
-        return;
-    }
-#endif
-    const uint64_t t0 = globaltimer();
+    // the watchdog clock is only read every 256 unsuccessful tries (a waiting warp shares its
+    // sub-partition's issue slots with working warps)
+    uint64_t t0 = 0;
     uint32_t n = 0;
+#if CDSP_WAIT_SLEEP
     while (!mbar_try_wait_sleep(bar, parity)) {
-        if ((++n & 255u) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+#else
+    while (!mbar_try_wait(bar, parity)) {
+#endif
+        if ((++n & 255u) == 0) {
+            const uint64_t t = globaltimer();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 4000000000ull) __trap();
+        }
     }
 }
 // Same, without the suspend hint: lowest wake-up latency, for a latency-critical waiter
 // (the MMA issuer) whose spinning costs one warp's issue slots.
 __device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
-    const uint64_t t0 = globaltimer();
+    uint64_t t0 = 0;
     uint32_t n = 0;
     while (!mbar_try_wait(bar, parity)) {
-        if ((++n & 1023u) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+        if ((++n & 1023u) == 0) {
+            const uint64_t t = globaltimer();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 4000000000ull) __trap();
+        }
     }
 }
 
