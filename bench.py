@@ -59,7 +59,7 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms during the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -73,7 +73,7 @@ class ClockSampler:
     def _run(self):
         try:
             p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                  "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                  "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE,
                                  stderr=subprocess.DEVNULL, text=True)
         except Exception:
             return
@@ -376,13 +376,24 @@ def main():
             traffic = json.load(open(prof)).get(f"L{L}_H{Hq}_s{s}")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_sustained"], "unit": UNIT,
-                "frac": achieved / peaks["bf16_sustained"], "traffic": traffic,
+    # Peak: the timed kernel launches add up to attn_ms (this rank).  A run whose kernel time
+    # is under 1 s stays at boost clocks, like the driver's burst GEMM (best of 10 single
+    # launches); a seconds-long run settles under the 1000 W cap, like its sustained GEMM
+    # (4 s loop).  Measured: 10 steps (72 ms) ran at 1965 MHz, 300 steps (2.4 s) at a median
+    # 1447 MHz with sw_power_cap (profiles/r01_bench_v8_long.json).
+    sustained = attn_ms >= 1000.0
+    peak = peaks["bf16_sustained"] if sustained else peaks["bf16_burst"]
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": UNIT,
+                "frac": achieved / peak, "traffic": traffic,
                 "kernel": "attn_tc_kernel<128> (tcgen05/TMEM/TMA)", "avg_launch_ms": attn_avg,
-                "launches_timed": attn_n,
-                "peak_note": f"bf16_tflops_sustained of MEASURED_PEAKS.json ({peaks['source']}); kernel runs "
-                             f"back-to-back in a seconds-long loop; burst peak {peaks['bf16_burst']}",
-                "frac_of_burst": achieved / peaks["bf16_burst"], "frac_of_spec_2250": achieved / 2250.0}
+                "launches_timed": attn_n, "kernel_ms_timed": attn_ms,
+                "peak_note": f"{'bf16_tflops_sustained' if sustained else 'bf16_tflops (burst)'} of "
+                             f"MEASURED_PEAKS.json ({peaks['source']}): the timed launches total "
+                             f"{attn_ms:.0f} ms ({'>=' if sustained else '<'} 1 s); burst "
+                             f"{peaks['bf16_burst']}, sustained {peaks['bf16_sustained']}",
+                "frac_of_burst": achieved / peaks["bf16_burst"],
+                "frac_of_sustained": achieved / peaks["bf16_sustained"],
+                "frac_of_spec_2250": achieved / 2250.0}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": cfg["scaling"],
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": cfg["config"],
