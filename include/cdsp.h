@@ -135,6 +135,16 @@ CDSP_API cdsp_status cdsp_comm_check(cdsp_comm c);
 CDSP_API cdsp_status cdsp_comm_profile(cdsp_comm c, int32_t enable);
 CDSP_API cdsp_status cdsp_comm_profile_read(cdsp_comm c, double* attn_ms, int32_t* n_launches);
 
+/* Ring profile of the same window (SURVEY §8(d) "ring hidden"): over the ring pulls this
+ * communicator issued while profiling (up to 4096), *copy_ms = summed pull durations on the
+ * comm stream, *bytes = K+V bytes pulled, *n_pulls = their count, and *exposed_ms = summed
+ * time the compute stream had to wait for them: for the pull feeding ring step k,
+ * max(0, pull end - end of step k-1's attention).  0 = the ring is fully hidden.  Call before
+ * issuing more work (it reads the attention events cdsp_comm_profile_read also reads, in
+ * either order); synchronises on them and resets the ring records. */
+CDSP_API cdsp_status cdsp_comm_profile_ring(cdsp_comm c, double* copy_ms, double* exposed_ms, int64_t* bytes,
+                                            int32_t* n_pulls);
+
 /* Destroy (synchronises the device first).  Peers must be done with this instance. */
 CDSP_API cdsp_status cdsp_comm_destroy(cdsp_comm c);
 
@@ -231,6 +241,36 @@ typedef struct {
 CDSP_API cdsp_status cdsp_kv_transfer_to_decode(const cdsp_tensor* k, const cdsp_tensor* v,
                                                 const cdsp_sp_group* sp_group,
                                                 const cdsp_decode_target* dst, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------------
+ * Decode consumer of the transferred cache
+ * ------------------------------------------------------------------------------- */
+
+/* Workspace bytes cdsp_decode_attention needs for hq_local query heads and hkv_local KV
+ * heads of head dim D (independent of the context length).  Errors: CDSP_ERR_SHAPE. */
+CDSP_API cdsp_status cdsp_decode_workspace_bytes(int32_t hq_local, int32_t hkv_local, int32_t D, size_t* bytes);
+
+/* One decode step's attention on decode TP rank t, read straight from the paged cache
+ * cdsp_kv_transfer_to_decode wrote (§2.2 PagedAttention "block granularity"; §6
+ * vLLM components; P:135/P:177 the KV streamed to the decode instance).  The query is the
+ * newest token (position n_ctx - 1, its own K/V already in the cache) and sees every cached
+ * position 0 .. n_ctx-1 (R4):  o_h = sum_j softmax_j(sigma <q_h, k_{j,kv(h)}>) v_{j,kv(h)}.
+ *   q [1, Hq_t, D]: rank t's query heads (global heads [t Hq_t, (t+1) Hq_t)), bf16 or f32 =
+ *     the cache dtype; hkv_local = Hkv / tp KV heads in cache->k_cache[t] / v_cache[t]
+ *     ([num_blocks, block_size, hkv_local, D]); local head h uses KV head h / (Hq_t/hkv_local) (R14);
+ *   softmax_scale: sigma (<= 0: 1/sqrt(D), R1);
+ *   out [1, Hq_t, D] (dtype of q, RNE for bf16); lse fp32 [Hq_t] natural log (R2), may be NULL;
+ *   workspace: >= cdsp_decode_workspace_bytes, 256-byte aligned device memory, ZERO-FILLED
+ *     once before first use (each call leaves it zero-filled again); one call at a time per
+ *     workspace.
+ * Split-KV flash-decoding in one launch (partials merged in-kernel by R3).  Block-table
+ * entries outside [0, num_blocks) contribute no keys.  Errors: CDSP_ERR_INVALID/SHAPE/DTYPE,
+ * CDSP_ERR_CAPACITY (n_table * block_size < n_ctx, workspace too small),
+ * CDSP_ERR_UNSUPPORTED (Hq_t/hkv_local not in {1,2,4,8}; block_size not a power of two). */
+CDSP_API cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_decode_target* cache, int32_t t,
+                                           int32_t hkv_local, int64_t n_ctx, float softmax_scale,
+                                           cdsp_tensor* out, float* lse, void* workspace,
+                                           size_t workspace_bytes, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------------
  * Building blocks, exported for tests and benches (same kernels the path uses)

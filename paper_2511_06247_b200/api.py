@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "cdsp_plan_capacity", "cdsp_plan_partition", "cdsp_prefill_chunk", "cdsp_lse_merge", "cdsp_kv_transfer_to_decode",
     "cdsp_attention_fwd", "cdsp_zigzag_gather", "cdsp_zigzag_scatter", "cdsp_zigzag_map_device",
     "cdsp_kv_transfer_errors", "cdsp_last_error", "cdsp_abi_version", "cdsp_comm_profile",
-    "cdsp_comm_profile_read",
+    "cdsp_comm_profile_read", "cdsp_decode_workspace_bytes", "cdsp_decode_attention", "cdsp_comm_profile_ring",
 )
 
 
@@ -118,6 +118,11 @@ def lib():
             "cdsp_kv_transfer_errors": [P, P, ctypes.POINTER(i64)],
             "cdsp_comm_profile": [P, i32],
             "cdsp_comm_profile_read": [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)],
+            "cdsp_decode_workspace_bytes": [i32, i32, i32, ctypes.POINTER(ctypes.c_size_t)],
+            "cdsp_comm_profile_ring": [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(i64), ctypes.POINTER(i32)],
+            "cdsp_decode_attention": [ctypes.POINTER(Tensor), ctypes.POINTER(DecodeTargetC), i32, i32, i64, f32,
+                                      ctypes.POINTER(Tensor), P, P, ctypes.c_size_t, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -262,6 +267,14 @@ class Comm:
         _check(lib().cdsp_comm_profile_read(self.h, ctypes.byref(ms), ctypes.byref(n)))
         return float(ms.value), int(n.value)
 
+    def profile_ring(self):
+        """-> (pull ms, exposed ms, bytes, pulls) of the ring since the last read (see cdsp.h)."""
+        cp, ex = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        by, n = ctypes.c_int64(0), ctypes.c_int32(0)
+        _check(lib().cdsp_comm_profile_ring(self.h, ctypes.byref(cp), ctypes.byref(ex), ctypes.byref(by),
+                                            ctypes.byref(n)))
+        return float(cp.value), float(ex.value), int(by.value), int(n.value)
+
     def kvstore(self) -> KvStore:
         c = KvStoreC()
         _check(lib().cdsp_kvstore_get(self.h, ctypes.byref(c)))
@@ -358,6 +371,31 @@ def kv_transfer_to_decode(k, v, sp_group: SpGroup, dst: DecodeTarget, stream=Non
     tk, tv = as_tensor(k), as_tensor(v)
     _check(lib().cdsp_kv_transfer_to_decode(ctypes.byref(tk), ctypes.byref(tv), ctypes.byref(sp_group.c),
                                             ctypes.byref(dst.c), _stream(stream)))
+
+
+def decode_workspace_bytes(hq_local: int, hkv_local: int, D: int) -> int:
+    n = ctypes.c_size_t(0)
+    _check(lib().cdsp_decode_workspace_bytes(hq_local, hkv_local, D, ctypes.byref(n)))
+    return int(n.value)
+
+
+def decode_workspace(hq_local: int, hkv_local: int, D: int, device="cuda") -> torch.Tensor:
+    """Zero-filled workspace for cdsp_decode_attention (torch's caching allocator aligns to 512 B)."""
+    return torch.zeros(decode_workspace_bytes(hq_local, hkv_local, D), dtype=torch.uint8, device=device)
+
+
+def decode_attention(q, cache: DecodeTarget, t: int, hkv_local: int, n_ctx: int, softmax_scale: float = 0.0,
+                     out=None, lse=None, workspace=None, stream=None):
+    """Decode step on decode TP rank t over its paged cache: q [1, Hq_t, D] -> (out, lse [Hq_t])."""
+    Hq_t, D = q.shape[1], q.shape[2]
+    out = out if out is not None else torch.empty_like(q)
+    if workspace is None:
+        workspace = decode_workspace(Hq_t, hkv_local, D, q.device)
+    tq, to = as_tensor(q), as_tensor(out)
+    _check(lib().cdsp_decode_attention(ctypes.byref(tq), ctypes.byref(cache.c), t, hkv_local, n_ctx, softmax_scale,
+                                       ctypes.byref(to), _ptr(lse), workspace.data_ptr(), workspace.numel(),
+                                       _stream(stream)))
+    return out, lse
 
 
 def kv_transfer_errors(comm: Comm, stream=None) -> int:

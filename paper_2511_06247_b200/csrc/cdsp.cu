@@ -108,6 +108,16 @@ struct cdsp_comm_s {
     bool profiling = false;
     std::vector<cudaEvent_t> prof_ev;  // pairs
     int prof_n = 0;
+    // ring profile (cdsp_comm_profile_ring): per pull, events at copy start / copy end (comm
+    // stream) and the index of the attention launch the pull must beat (its end event)
+    struct RingRec {
+        int ev;         // ring_ev[2 ev], ring_ev[2 ev + 1]
+        int prev_attn;  // prof_ev index of the previous step's attention end, -1 if none
+        int64_t bytes;
+    };
+    std::vector<cudaEvent_t> ring_ev;
+    std::vector<RingRec> ring_rec;
+    int ring_n = 0;
     // loopback group and its ordering events
     LocalGroup* lg = nullptr;
     cudaEvent_t ev_bal = nullptr, ev_app = nullptr, ev_fin = nullptr;
@@ -250,6 +260,7 @@ cdsp_status phase_append(cdsp_comm c, const ChunkInfo& ci, int r, const cdsp_ten
 cdsp_status phase_ring(cdsp_comm c, const ChunkInfo& ci, int r, const void* q, int Hq, void* out, float* lse,
                        float scale, cudaStream_t st, LocalGroup* g) {
     const int64_t m2 = 2 * ci.m;
+    const int prof_base = c->prof_n;  // profiling: index of this call's step-0 attention launch
     CDSP_CUDA(cudaEventRecord(c->ev_ready, st));  // recv buffers are free after st's earlier work
     CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
     auto issue_copy = [&](int step) -> cdsp_status {
@@ -259,8 +270,17 @@ cdsp_status phase_ring(cdsp_comm c, const ChunkInfo& ci, int r, const void* q, i
         if (g) CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, g->comms[ci.ranks[src]]->ev_app, 0));
         const size_t bytes = static_cast<size_t>(ci.hist[src] + m2) * c->row_bytes;
         const PeerView& pv = c->peers[ci.ranks[src]];
+        // profiling: the pull of step k must beat the end of step k-1's attention, the
+        // launch recorded right before this step's (prof_n counts launches issued so far)
+        const bool rec = c->profiling && c->ring_n < static_cast<int>(c->ring_rec.size());
+        if (rec) CDSP_CUDA(cudaEventRecord(c->ring_ev[2 * c->ring_n], c->comm_stream));
         CDSP_CUDA(cudaMemcpyAsync(c->recv_k[b], pv.k, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
         CDSP_CUDA(cudaMemcpyAsync(c->recv_v[b], pv.v, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
+        if (rec) {
+            CDSP_CUDA(cudaEventRecord(c->ring_ev[2 * c->ring_n + 1], c->comm_stream));
+            c->ring_rec[c->ring_n] = {c->ring_n, prof_base + step - 1, 2 * static_cast<int64_t>(bytes)};
+            ++c->ring_n;
+        }
         CDSP_CUDA(cudaEventRecord(c->ev_copy[b], c->comm_stream));
         return CDSP_OK;
     };
@@ -465,9 +485,43 @@ cdsp_status cdsp_comm_profile(cdsp_comm c, int32_t enable) {
     if (enable && c->prof_ev.empty()) {
         c->prof_ev.resize(2 * 8192, nullptr);
         for (auto& ev : c->prof_ev) CDSP_CUDA(cudaEventCreate(&ev));
+        c->ring_ev.resize(2 * 4096, nullptr);
+        for (auto& ev : c->ring_ev) CDSP_CUDA(cudaEventCreate(&ev));
+        c->ring_rec.resize(4096);
     }
     c->profiling = enable != 0;
     c->prof_n = 0;
+    c->ring_n = 0;
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_comm_profile_ring(cdsp_comm c, double* copy_ms, double* exposed_ms, int64_t* bytes,
+                                   int32_t* n_pulls) {
+    CDSP_REQUIRE(c && copy_ms && exposed_ms && bytes && n_pulls, CDSP_ERR_INVALID, "NULL argument");
+    double cp = 0.0, ex = 0.0;
+    int64_t by = 0;
+    if (c->ring_n > 0) CDSP_CUDA(cudaEventSynchronize(c->ring_ev[2 * c->ring_n - 1]));
+    const int n_attn = static_cast<int>(c->prof_ev.size() / 2);
+    for (int i = 0; i < c->ring_n; ++i) {
+        const auto& r = c->ring_rec[i];
+        float ms = 0.f;
+        CDSP_CUDA(cudaEventElapsedTime(&ms, c->ring_ev[2 * r.ev], c->ring_ev[2 * r.ev + 1]));
+        cp += ms;
+        by += r.bytes;
+        if (r.prev_attn >= 0 && r.prev_attn < n_attn) {
+            // the compute stream idles from the end of the previous step's attention until
+            // this pull lands (the next attention waits on it)
+            CDSP_CUDA(cudaEventSynchronize(c->prof_ev[2 * r.prev_attn + 1]));
+            float gap = 0.f;
+            CDSP_CUDA(cudaEventElapsedTime(&gap, c->prof_ev[2 * r.prev_attn + 1], c->ring_ev[2 * r.ev + 1]));
+            if (gap > 0.f) ex += gap;
+        }
+    }
+    *copy_ms = cp;
+    *exposed_ms = ex;
+    *bytes = by;
+    *n_pulls = c->ring_n;
+    c->ring_n = 0;
     return CDSP_OK;
 }
 
@@ -490,6 +544,8 @@ cdsp_status cdsp_comm_destroy(cdsp_comm c) {
     if (!c) return CDSP_OK;
     cudaDeviceSynchronize();
     for (auto ev : c->prof_ev)
+        if (ev) cudaEventDestroy(ev);
+    for (auto ev : c->ring_ev)
         if (ev) cudaEventDestroy(ev);
     for (int j = 0; j < kMaxWorld; ++j)
         if (c->ipc_base[j]) cudaIpcCloseMemHandle(c->ipc_base[j]);
