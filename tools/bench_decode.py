@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--tp", type=int, default=8)
+    ap.add_argument("--identity-table", action="store_true", help="block table = 0, 1, 2, ... (dev)")
     args = ap.parse_args()
     Hq, Hkv, D, B, tp = 32, 8, 128, 16, args.tp
     N = args.ctx
@@ -37,6 +38,8 @@ def main():
     n_logical = N // B
     nb = n_logical + n_logical // 4
     bt = block_table(n_logical, nb, seed=7).to(dev)
+    if args.identity_table:
+        bt = torch.arange(n_logical, dtype=torch.int32, device=dev)
     kc = [torch.empty((nb, B, Hkv // tp, D), dtype=torch.bfloat16, device=dev) for _ in range(tp)]
     vc = [torch.empty_like(x) for x in kc]
     dst = api.DecodeTarget(kc, vc, B, bt)
