@@ -286,12 +286,13 @@ def main():
         torch.cuda.synchronize()
     barrier()
     ms = e0.elapsed_time(e1)
+    ring_cp, ring_ex, ring_bytes, ring_n = comm.profile_ring()
     attn_ms, attn_n = comm.profile_read()
     comm.profile(False)
     comm.check()
     if dist is not None:
-        ms, attn_avg = dist_utils.max_over_ranks([ms, attn_ms / max(attn_n, 1)],
-                                                 device=None if shared is not None else dev)
+        ms, attn_avg, ring_ex, ring_cp = dist_utils.max_over_ranks(
+            [ms, attn_ms / max(attn_n, 1), ring_ex, ring_cp], device=None if shared is not None else dev)
     else:
         attn_avg = attn_ms / max(attn_n, 1)
     ms_step = ms / args.steps
@@ -399,6 +400,12 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": cfg["config"],
             "roofline": roofline, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(), "chunk_latency_ms": ms_step,
+            "ring": None if s == 1 else {
+                "pulls_per_step": ring_n / args.steps, "bytes_per_step": ring_bytes / args.steps,
+                "pull_ms_per_step": ring_cp / args.steps, "exposed_ms_per_step": ring_ex / args.steps,
+                "pull_gbs": ring_bytes / max(ring_cp, 1e-9) / 1e6,
+                "note": "owner-pull copy-engine reads of peer stores over NVLink (CUDA IPC); exposed = "
+                        "compute-stream wait for pulls, max over ranks (0 = ring fully hidden)"},
             "tflops_per_gpu": value / world}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(q, k, v, 1.0 / math.sqrt(D))

@@ -110,6 +110,14 @@ typedef struct cdsp_comm_s* cdsp_comm;
 CDSP_API cdsp_status cdsp_comm_create(cdsp_comm* out, int32_t rank, int32_t world, int32_t device,
                                       int64_t store_cap_tokens, int32_t Hkv, int32_t D, int32_t dtype);
 
+/* Same with n_layers per-layer KV stores (one per transformer layer; positions shared): the
+ * layer-wise prefill (cdsp_prefill_chunk_layer) overlaps each layer's cache balancing with
+ * the previous layer ("Cache-Balancing Latency Overlap", Fig. 6-b).  Allocates
+ * (2 n_layers + 4) * store_cap_tokens * Hkv * D * sizeof(dtype) (+ small) bytes. */
+CDSP_API cdsp_status cdsp_comm_create_layers(cdsp_comm* out, int32_t rank, int32_t world, int32_t device,
+                                             int64_t store_cap_tokens, int32_t n_layers, int32_t Hkv, int32_t D,
+                                             int32_t dtype);
+
 /* Export this instance's shared region as CDSP_IPC_HANDLE_BYTES bytes (host buffer). */
 CDSP_API cdsp_status cdsp_comm_ipc_handle(cdsp_comm c, void* handle_out);
 
@@ -157,9 +165,10 @@ typedef struct {
     int64_t n, cap;
 } cdsp_kvstore;
 
-CDSP_API cdsp_status cdsp_kvstore_get(cdsp_comm c, cdsp_kvstore* out);
+CDSP_API cdsp_status cdsp_kvstore_get(cdsp_comm c, cdsp_kvstore* out);               /* layer 0 */
+CDSP_API cdsp_status cdsp_kvstore_get_layer(cdsp_comm c, int32_t layer, cdsp_kvstore* out);
 
-/* Start a new request on this instance: its store becomes empty (host-side; stream-ordered
+/* Start a new request on this instance: its stores (all layers) become empty (host-side; stream-ordered
  * uses of the old content must be complete or on `cuda_stream`, which this call joins). */
 CDSP_API cdsp_status cdsp_kvstore_reset(cdsp_comm c, void* cuda_stream);
 
@@ -207,6 +216,20 @@ CDSP_API cdsp_status cdsp_prefill_chunk(const cdsp_tensor* q, const cdsp_tensor*
                                         cdsp_kvstore* prev_kv, const cdsp_sp_group* sp_group,
                                         float softmax_scale, cdsp_tensor* out, float* lse,
                                         void* cuda_stream);
+
+/* cdsp_prefill_chunk on layer `layer`'s store (0 <= layer < n_layers; prev_kv from
+ * cdsp_kvstore_get_layer).  A chunk is processed layer by layer: every rank of the group calls
+ * layers 0, 1, ... in order (the caller's per-layer work, e.g. the FC layers, goes between the
+ * calls on the same stream).  When the chunk re-balances history (its group grew), layer 0
+ * balances inline; right after layer l's ring is enqueued, a new rank issues layer l+1's
+ * balancing pulls on its communicator stream, so they run under the rest of layer l and the
+ * caller's FC work (Fig. 6-b); layer l+1 then only waits for them.  Old ranks
+ * overwrite a moved part only after its puller acknowledged the pull.  Result semantics per
+ * layer are exactly cdsp_prefill_chunk's. */
+CDSP_API cdsp_status cdsp_prefill_chunk_layer(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
+                                              cdsp_kvstore* prev_kv, const cdsp_sp_group* sp_group,
+                                              int32_t layer, float softmax_scale, cdsp_tensor* out, float* lse,
+                                              void* cuda_stream);
 
 /* n >= 1 partial attention results over disjoint key sets -> their combination (R3):
  *   M = max_i lse_i; lse = M + ln sum_i e^{lse_i - M}; O = sum_i e^{lse_i - M} O_i / sum_i e^{lse_i - M}.

@@ -32,6 +32,7 @@ EXPORTED_SYMBOLS = (
     "cdsp_attention_fwd", "cdsp_zigzag_gather", "cdsp_zigzag_scatter", "cdsp_zigzag_map_device",
     "cdsp_kv_transfer_errors", "cdsp_last_error", "cdsp_abi_version", "cdsp_comm_profile",
     "cdsp_comm_profile_read", "cdsp_decode_workspace_bytes", "cdsp_decode_attention", "cdsp_comm_profile_ring",
+    "cdsp_comm_create_layers", "cdsp_kvstore_get_layer", "cdsp_prefill_chunk_layer",
 )
 
 
@@ -94,6 +95,11 @@ def lib():
         P, i32, i64, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
         sig = {
             "cdsp_comm_create": [ctypes.POINTER(P), i32, i32, i32, i64, i32, i32, i32],
+            "cdsp_comm_create_layers": [ctypes.POINTER(P), i32, i32, i32, i64, i32, i32, i32, i32],
+            "cdsp_kvstore_get_layer": [P, i32, ctypes.POINTER(KvStoreC)],
+            "cdsp_prefill_chunk_layer": [ctypes.POINTER(Tensor)] * 3 + [ctypes.POINTER(KvStoreC),
+                                                                        ctypes.POINTER(SpGroupC), i32, f32,
+                                                                        ctypes.POINTER(Tensor), P, P],
             "cdsp_comm_ipc_handle": [P, P],
             "cdsp_comm_connect": [P, P],
             "cdsp_comm_connect_local": [ctypes.POINTER(P), i32],
@@ -229,15 +235,15 @@ class KvStore:
 
 class Comm:
     def __init__(self, rank: int, world: int, device: int, store_cap_tokens: int, Hkv: int, D: int,
-                 dtype: torch.dtype = torch.bfloat16):
+                 dtype: torch.dtype = torch.bfloat16, n_layers: int = 1):
         self.rank, self.world, self.device = rank, world, device
-        self.Hkv, self.D, self.dtype = Hkv, D, dtype
+        self.Hkv, self.D, self.dtype, self.n_layers = Hkv, D, dtype, n_layers
         h = ctypes.c_void_p()
-        _check(lib().cdsp_comm_create(ctypes.byref(h), rank, world, device, int(store_cap_tokens), Hkv, D,
-                                      _dtype_code(dtype)))
+        _check(lib().cdsp_comm_create_layers(ctypes.byref(h), rank, world, device, int(store_cap_tokens), n_layers,
+                                             Hkv, D, _dtype_code(dtype)))
         self.h = h
         self.cap = int(store_cap_tokens)
-        self._store = None
+        self._stores = {}
 
     def ipc_handle(self) -> bytes:
         buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
@@ -275,13 +281,14 @@ class Comm:
                                             ctypes.byref(n)))
         return float(cp.value), float(ex.value), int(by.value), int(n.value)
 
-    def kvstore(self) -> KvStore:
+    def kvstore(self, layer: int = 0) -> KvStore:
         c = KvStoreC()
-        _check(lib().cdsp_kvstore_get(self.h, ctypes.byref(c)))
-        if self._store is None:
-            self._store = _wrap_store(c, self)
-        self._store.c = c
-        return self._store
+        _check(lib().cdsp_kvstore_get_layer(self.h, layer, ctypes.byref(c)))
+        st = self._stores.get(layer)
+        if st is None:
+            st = self._stores[layer] = _wrap_store(c, self)
+        st.c = c
+        return st
 
     def reset(self, stream=None):
         _check(lib().cdsp_kvstore_reset(self.h, _stream(stream)))
@@ -330,14 +337,21 @@ class SpGroup:
 
 # ---- the four calls ----------------------------------------------------------------------------
 def prefill_chunk(q, k, v, prev_kv: KvStore, sp_group: SpGroup, softmax_scale: float = 0.0,
-                  out: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None, stream=None):
-    """cdsp_prefill_chunk: this rank's zigzag shard q/k/v [2m,H,D] -> out [2m,Hq,D] (+ lse [Hq,2m])."""
+                  out: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None, stream=None,
+                  layer: Optional[int] = None):
+    """cdsp_prefill_chunk (or cdsp_prefill_chunk_layer when `layer` is given): this rank's zigzag
+    shard q/k/v [2m,H,D] -> out [2m,Hq,D] (+ lse [Hq,2m])."""
     if out is None:
         out = torch.empty_like(q)
     tq, tk, tv, to = as_tensor(q), as_tensor(k), as_tensor(v), as_tensor(out)
-    _check(lib().cdsp_prefill_chunk(ctypes.byref(tq), ctypes.byref(tk), ctypes.byref(tv),
-                                    ctypes.byref(prev_kv.c), ctypes.byref(sp_group.c), float(softmax_scale),
-                                    ctypes.byref(to), _ptr(lse), _stream(stream)))
+    if layer is None:
+        _check(lib().cdsp_prefill_chunk(ctypes.byref(tq), ctypes.byref(tk), ctypes.byref(tv),
+                                        ctypes.byref(prev_kv.c), ctypes.byref(sp_group.c), float(softmax_scale),
+                                        ctypes.byref(to), _ptr(lse), _stream(stream)))
+    else:
+        _check(lib().cdsp_prefill_chunk_layer(ctypes.byref(tq), ctypes.byref(tk), ctypes.byref(tv),
+                                              ctypes.byref(prev_kv.c), ctypes.byref(sp_group.c), int(layer),
+                                              float(softmax_scale), ctypes.byref(to), _ptr(lse), _stream(stream)))
     return out
 
 

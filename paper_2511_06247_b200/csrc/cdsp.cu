@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -58,6 +59,7 @@ struct PeerView {
 // Loopback groups (cdsp_comm_connect_local): every instance lives in this process; a chunk's
 // cdsp_prefill_chunk calls are collected and issued together, ordered by CUDA events.
 struct PendingCall {
+    int layer;
     cdsp_tensor q, k, v, out;
     float* lse;
     cdsp_kvstore* prev_kv;
@@ -72,6 +74,7 @@ struct LocalGroup {
     int pending = 0;
     const cdsp_plan* plan = nullptr;
     int chunk = -1;
+    int layer = -1;
     int refs = 0;
 };
 }  // namespace
@@ -103,7 +106,14 @@ struct cdsp_comm_s {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_done = nullptr, ev_copy[2] = {nullptr, nullptr},
                 ev_comp[2] = {nullptr, nullptr};
-    int64_t n = 0;  // valid store rows
+    // layers (cdsp_comm_create_layers): one K/V store per layer, positions shared
+    int n_layers = 1;
+    size_t kv_bytes = 0;                 // bytes of one layer's K (or V) store
+    std::vector<int64_t> n_l;            // valid store rows per layer
+    std::vector<cudaEvent_t> ev_bal_l;   // per layer: this rank's balancing pulls done
+    std::vector<int> prebal;             // per layer: chunk whose balancing was pre-issued, -1 none
+    const cdsp_plan* prebal_plan = nullptr;
+    unsigned long long ack_expect[kMaxWorld] = {0};  // balancing acks expected from each puller
     // live kernel timing (cdsp_comm_profile)
     bool profiling = false;
     std::vector<cudaEvent_t> prof_ev;  // pairs
@@ -217,48 +227,112 @@ cdsp_segments segments_for(const ChunkInfo& ci, int r, int src) {
     return sgm;
 }
 
-// Cache balancing (R8): a ring rank new to the group pulls its part of an old rank's
-// store (copy engines, NVLink when the peer is another GPU).
-cdsp_status phase_balance(cdsp_comm c, const ChunkInfo& ci, int r, cudaStream_t st) {
+// Per-layer store views (the layers of one instance share geometry and the position array).
+inline char* layer_k(cdsp_comm c, const PeerView& pv, int layer) { return pv.k + layer * c->kv_bytes; }
+inline char* layer_v(cdsp_comm c, const PeerView& pv, int layer) { return pv.v + layer * c->kv_bytes; }
+inline bool balancing(const ChunkInfo& ci) { return ci.s_prev > 0 && ci.s > ci.s_prev; }
+
+// Cache balancing (R8) of one layer's store: a ring rank new to the group pulls its part
+// of an old rank's store (copy engines, NVLink when the peer is another GPU); positions move
+// with layer 0.  Multi-process: each pull is acknowledged to its source (a system-scope
+// counter in the source's flag page) so the source may overwrite that part afterwards;
+// loopback (g != NULL) orders the source by the puller's event instead.
+cdsp_status phase_balance_pull(cdsp_comm c, const ChunkInfo& ci, int r, int layer, cudaStream_t st, bool ack) {
+    BarrierArgs a;
+    std::memset(&a, 0, sizeof(a));
     for (int i = 0; i < ci.n_moves; ++i) {
         const cdsp_move& mv = ci.moves[i];
         if (mv.dst != r || mv.n_tok == 0) continue;
         const PeerView& src = c->peers[ci.ranks[mv.src]];
-        CDSP_CUDA(cudaMemcpyAsync(c->self.k, src.k + mv.src_off * c->row_bytes, mv.n_tok * c->row_bytes,
-                                  cudaMemcpyDeviceToDevice, st));
-        CDSP_CUDA(cudaMemcpyAsync(c->self.v, src.v + mv.src_off * c->row_bytes, mv.n_tok * c->row_bytes,
-                                  cudaMemcpyDeviceToDevice, st));
-        CDSP_CUDA(cudaMemcpyAsync(c->self.pos, src.pos + mv.src_off, mv.n_tok * sizeof(int32_t),
-                                  cudaMemcpyDeviceToDevice, st));
+        CDSP_CUDA(cudaMemcpyAsync(layer_k(c, c->self, layer), layer_k(c, src, layer) + mv.src_off * c->row_bytes,
+                                  mv.n_tok * c->row_bytes, cudaMemcpyDeviceToDevice, st));
+        CDSP_CUDA(cudaMemcpyAsync(layer_v(c, c->self, layer), layer_v(c, src, layer) + mv.src_off * c->row_bytes,
+                                  mv.n_tok * c->row_bytes, cudaMemcpyDeviceToDevice, st));
+        if (layer == 0)
+            CDSP_CUDA(cudaMemcpyAsync(c->self.pos, src.pos + mv.src_off, mv.n_tok * sizeof(int32_t),
+                                      cudaMemcpyDeviceToDevice, st));
+        if (ack) {  // signal only: the source's ack slot for this instance
+            a.remote[a.n] = src.flags + kMaxWorld + c->rank;
+            a.local[a.n] = c->self.flags + kMaxWorld + c->rank;
+            a.target[a.n] = 0;
+            ++a.n;
+        }
+    }
+    if (a.n > 0) {
+        a.err = c->err_dev;
+        CDSP_CHECK_STATUS(launch_peer_barrier(a, st));
+    }
+    return CDSP_OK;
+}
+
+// Multi-process source side: wait until every puller of this rank acknowledged its pull of
+// this layer (cumulative counters, so no reset is ever needed).
+cdsp_status phase_balance_wait(cdsp_comm c, const ChunkInfo& ci, int r, cudaStream_t st) {
+    BarrierArgs a;
+    std::memset(&a, 0, sizeof(a));
+    for (int i = 0; i < ci.n_moves; ++i) {
+        const cdsp_move& mv = ci.moves[i];
+        if (mv.src != r || mv.n_tok == 0) continue;
+        const int j = ci.ranks[mv.dst];
+        c->ack_expect[j] += 1;
+        a.remote[a.n] = nullptr;  // wait only
+        a.local[a.n] = c->self.flags + kMaxWorld + j;
+        a.target[a.n] = c->ack_expect[j];
+        ++a.n;
+    }
+    if (a.n > 0) {
+        a.err = c->err_dev;
+        CDSP_CHECK_STATUS(launch_peer_barrier(a, st));
     }
     return CDSP_OK;
 }
 
 // Append this rank's shard (k, v and global positions) after its balanced history.
-cdsp_status phase_append(cdsp_comm c, const ChunkInfo& ci, int r, const cdsp_tensor* k, const cdsp_tensor* v,
-                         cudaStream_t st) {
-    c->n = ci.hist[r];
+cdsp_status phase_append(cdsp_comm c, const ChunkInfo& ci, int r, int layer, const cdsp_tensor* k,
+                         const cdsp_tensor* v, cudaStream_t st) {
+    int64_t& n = c->n_l[layer];
+    n = ci.hist[r];
     AppendArgs a;
     a.k_src = k->ptr;
     a.v_src = v->ptr;
-    a.k_dst = c->self.k + c->n * c->row_bytes;
-    a.v_dst = c->self.v + c->n * c->row_bytes;
-    a.pos_dst = c->self.pos + c->n;
+    a.k_dst = layer_k(c, c->self, layer) + n * c->row_bytes;
+    a.v_dst = layer_v(c, c->self, layer) + n * c->row_bytes;
+    a.pos_dst = c->self.pos + n;
     a.n_rows = 2 * ci.m;
     a.row_bytes = static_cast<int64_t>(c->row_bytes);
     a.len0 = ci.m;
     a.pos0 = shard_pos0(ci, r);
     a.pos1 = shard_pos1(ci, r);
     CDSP_CHECK_STATUS(launch_store_append(a, st));
-    c->n += 2 * ci.m;
+    n += 2 * ci.m;
     return CDSP_OK;
+}
+
+// Layer-wise balancing overlap ("once the ring attention in current layer completes,
+// its inter-instance communicator can be reused to perform cache balancing for the next
+// layer"): right after layer l's ring is enqueued, a puller issues layer l+1's balancing
+// pulls on its comm stream, behind the ring pulls, so they run under the rest of layer l
+// (its last ring steps and whatever the caller runs next, e.g. the FC layers).
+cdsp_status prebalance_next(cdsp_comm c, const ChunkInfo& ci, int r, int layer, const cdsp_plan* plan, bool ack) {
+    const int nl = layer + 1;
+    if (!balancing(ci) || nl >= c->n_layers) return CDSP_OK;
+    static const bool off = getenv("CDSP_NO_PREBALANCE") != nullptr;  // measurement control only
+    if (off) return CDSP_OK;
+    CDSP_CHECK_STATUS(phase_balance_pull(c, ci, r, nl, c->comm_stream, ack));
+    CDSP_CUDA(cudaEventRecord(c->ev_bal_l[nl], c->comm_stream));
+    c->prebal[nl] = ci.c;
+    c->prebal_plan = plan;
+    return CDSP_OK;
+}
+inline bool prebalanced(cdsp_comm c, const ChunkInfo& ci, int layer, const cdsp_plan* plan) {
+    return c->prebal[layer] == ci.c && c->prebal_plan == plan;
 }
 
 // The ring (R10, R11): step k attends to src = (r - k) mod s's whole store; steps >= 1
 // read it through a copy-engine pull on the comm stream into receive buffer k & 1, overlapped
 // with step k-1.  g != NULL (loopback): each pull waits for src's append event.
-cdsp_status phase_ring(cdsp_comm c, const ChunkInfo& ci, int r, const void* q, int Hq, void* out, float* lse,
-                       float scale, cudaStream_t st, LocalGroup* g) {
+cdsp_status phase_ring(cdsp_comm c, const ChunkInfo& ci, int r, int layer, const void* q, int Hq, void* out,
+                       float* lse, float scale, cudaStream_t st, LocalGroup* g) {
     const int64_t m2 = 2 * ci.m;
     const int prof_base = c->prof_n;  // profiling: index of this call's step-0 attention launch
     CDSP_CUDA(cudaEventRecord(c->ev_ready, st));  // recv buffers are free after st's earlier work
@@ -274,8 +348,10 @@ cdsp_status phase_ring(cdsp_comm c, const ChunkInfo& ci, int r, const void* q, i
         // launch recorded right before this step's (prof_n counts launches issued so far)
         const bool rec = c->profiling && c->ring_n < static_cast<int>(c->ring_rec.size());
         if (rec) CDSP_CUDA(cudaEventRecord(c->ring_ev[2 * c->ring_n], c->comm_stream));
-        CDSP_CUDA(cudaMemcpyAsync(c->recv_k[b], pv.k, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
-        CDSP_CUDA(cudaMemcpyAsync(c->recv_v[b], pv.v, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
+        CDSP_CUDA(cudaMemcpyAsync(c->recv_k[b], layer_k(c, pv, layer), bytes, cudaMemcpyDeviceToDevice,
+                                  c->comm_stream));
+        CDSP_CUDA(cudaMemcpyAsync(c->recv_v[b], layer_v(c, pv, layer), bytes, cudaMemcpyDeviceToDevice,
+                                  c->comm_stream));
         if (rec) {
             CDSP_CUDA(cudaEventRecord(c->ring_ev[2 * c->ring_n + 1], c->comm_stream));
             c->ring_rec[c->ring_n] = {c->ring_n, prof_base + step - 1, 2 * static_cast<int64_t>(bytes)};
@@ -289,8 +365,8 @@ cdsp_status phase_ring(cdsp_comm c, const ChunkInfo& ci, int r, const void* q, i
         if (step + 1 >= 2 && step + 1 < ci.s) CDSP_CHECK_STATUS(issue_copy(step + 1));
         const int src = (r - step + ci.s) % ci.s;
         const int b = step & 1;
-        const char* kb = c->self.k;
-        const char* vb = c->self.v;
+        const char* kb = layer_k(c, c->self, layer);
+        const char* vb = layer_v(c, c->self, layer);
         if (step > 0) {
             CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_copy[b], 0));
             kb = c->recv_k[b];
@@ -306,37 +382,44 @@ cdsp_status phase_ring(cdsp_comm c, const ChunkInfo& ci, int r, const void* q, i
     return CDSP_OK;
 }
 
-// Loopback execution of one chunk by all its ranks, ordered by events:
-//   previous calls finished -> balancing pulls -> (old ranks wait for their pullers) append ->
-//   ring (each pull waits for the source's append) -> finish event.
-cdsp_status run_group_local(LocalGroup* g, const ChunkInfo& ci) {
+// Loopback execution of one chunk's layer by all its ranks, ordered by events:
+//   previous calls finished -> balancing pulls (unless pre-issued by the previous layer) ->
+//   (old ranks wait for their pullers) append -> ring (each pull waits for the source's
+//   append) -> finish event -> next layer's balancing pulls on the pullers' comm streams.
+cdsp_status run_group_local(LocalGroup* g, const ChunkInfo& ci, int layer) {
     auto comm_of = [&](int r) { return g->comms[ci.ranks[r]]; };
     for (int r = 0; r < ci.s; ++r)
         for (int j = 0; j < ci.s; ++j)
             if (comm_of(j)->fin_recorded) CDSP_CUDA(cudaStreamWaitEvent(g->calls[r].st, comm_of(j)->ev_fin, 0));
-    if (ci.s_prev > 0 && ci.s > ci.s_prev) {
+    if (balancing(ci)) {
         for (int r = 0; r < ci.s; ++r) {
-            CDSP_CHECK_STATUS(phase_balance(comm_of(r), ci, r, g->calls[r].st));
-            CDSP_CUDA(cudaEventRecord(comm_of(r)->ev_bal, g->calls[r].st));
+            cdsp_comm c = comm_of(r);
+            if (!prebalanced(c, ci, layer, g->plan)) {
+                CDSP_CHECK_STATUS(phase_balance_pull(c, ci, r, layer, g->calls[r].st, false));
+                CDSP_CUDA(cudaEventRecord(c->ev_bal_l[layer], g->calls[r].st));
+            } else {
+                CDSP_CUDA(cudaStreamWaitEvent(g->calls[r].st, c->ev_bal_l[layer], 0));
+            }
         }
         for (int i = 0; i < ci.n_moves; ++i)  // an old rank overwrites its moved parts only after the pull
-            CDSP_CUDA(cudaStreamWaitEvent(g->calls[ci.moves[i].src].st, comm_of(ci.moves[i].dst)->ev_bal, 0));
+            CDSP_CUDA(cudaStreamWaitEvent(g->calls[ci.moves[i].src].st, comm_of(ci.moves[i].dst)->ev_bal_l[layer], 0));
     }
     for (int r = 0; r < ci.s; ++r) {
         PendingCall& pc = g->calls[r];
-        CDSP_CHECK_STATUS(phase_append(comm_of(r), ci, r, &pc.k, &pc.v, pc.st));
+        CDSP_CHECK_STATUS(phase_append(comm_of(r), ci, r, layer, &pc.k, &pc.v, pc.st));
         CDSP_CUDA(cudaEventRecord(comm_of(r)->ev_app, pc.st));
-        pc.prev_kv->n = comm_of(r)->n;
+        pc.prev_kv->n = comm_of(r)->n_l[layer];
     }
     for (int r = 0; r < ci.s; ++r) {
         PendingCall& pc = g->calls[r];
-        CDSP_CHECK_STATUS(phase_ring(comm_of(r), ci, r, pc.q.ptr, static_cast<int>(pc.q.H), pc.out.ptr, pc.lse,
-                                     pc.scale, pc.st, g));
+        CDSP_CHECK_STATUS(phase_ring(comm_of(r), ci, r, layer, pc.q.ptr, static_cast<int>(pc.q.H), pc.out.ptr,
+                                     pc.lse, pc.scale, pc.st, g));
     }
     for (int r = 0; r < ci.s; ++r) {
         CDSP_CUDA(cudaEventRecord(comm_of(r)->ev_fin, g->calls[r].st));
         comm_of(r)->fin_recorded = true;
     }
+    for (int r = 0; r < ci.s; ++r) CDSP_CHECK_STATUS(prebalance_next(comm_of(r), ci, r, layer, g->plan, false));
     return CDSP_OK;
 }
 
@@ -350,11 +433,17 @@ int32_t cdsp_abi_version(void) { return CDSP_ABI_VERSION; }
 // ------------------------------------------------------------------------------- comm
 cdsp_status cdsp_comm_create(cdsp_comm* out, int32_t rank, int32_t world, int32_t device, int64_t store_cap_tokens,
                              int32_t Hkv, int32_t D, int32_t dtype) {
+    return cdsp_comm_create_layers(out, rank, world, device, store_cap_tokens, 1, Hkv, D, dtype);
+}
+
+cdsp_status cdsp_comm_create_layers(cdsp_comm* out, int32_t rank, int32_t world, int32_t device,
+                                    int64_t store_cap_tokens, int32_t n_layers, int32_t Hkv, int32_t D, int32_t dtype) {
     CDSP_REQUIRE(out != nullptr, CDSP_ERR_INVALID, "out is NULL");
     *out = nullptr;
     CDSP_REQUIRE(world >= 1 && world <= kMaxWorld, CDSP_ERR_INVALID, "world %d not in [1,%d]", world, kMaxWorld);
     CDSP_REQUIRE(rank >= 0 && rank < world, CDSP_ERR_INVALID, "rank %d not in [0,%d)", rank, world);
     CDSP_REQUIRE(store_cap_tokens >= 1 && Hkv >= 1, CDSP_ERR_SHAPE, "bad store geometry");
+    CDSP_REQUIRE(n_layers >= 1 && n_layers <= 1024, CDSP_ERR_INVALID, "n_layers %d not in [1,1024]", n_layers);
     CDSP_REQUIRE(D == 64 || D == 128, CDSP_ERR_SHAPE, "head dim %d not in {64,128}", D);
     CDSP_REQUIRE(dtype_ok(dtype), CDSP_ERR_DTYPE, "bad dtype %d", dtype);
     CDSP_CUDA(cudaSetDevice(device));
@@ -369,10 +458,16 @@ cdsp_status cdsp_comm_create(cdsp_comm* out, int32_t rank, int32_t world, int32_
     c->esize = dtype_size(dtype);
     c->row_bytes = static_cast<size_t>(Hkv) * D * c->esize;
     const size_t kv_bytes = align_up(static_cast<size_t>(store_cap_tokens) * c->row_bytes, 256);
-    c->off_v = kv_bytes;
-    c->off_pos = 2 * kv_bytes;
+    c->n_layers = n_layers;
+    c->kv_bytes = kv_bytes;
+    c->n_l.assign(n_layers, 0);
+    c->prebal.assign(n_layers, -1);
+    c->ev_bal_l.assign(n_layers, nullptr);
+    c->off_v = static_cast<size_t>(n_layers) * kv_bytes;
+    c->off_pos = 2 * static_cast<size_t>(n_layers) * kv_bytes;
     c->off_flags = c->off_pos + align_up(static_cast<size_t>(store_cap_tokens) * 4, 256);
-    c->region_bytes = c->off_flags + align_up(kMaxWorld * sizeof(unsigned long long), 256);
+    // flags: [0, 8) peer-barrier counters, [8, 16) balancing-ack counters (per peer)
+    c->region_bytes = c->off_flags + align_up(2 * kMaxWorld * sizeof(unsigned long long), 256);
     auto fail = [&](cudaError_t e, const char* what) {
         set_error("%s failed: %s", what, cudaGetErrorString(e));
         cdsp_comm_destroy(c);
@@ -409,6 +504,10 @@ cdsp_status cdsp_comm_create(cdsp_comm* out, int32_t rank, int32_t world, int32_
                            &c->ev_comp[1], &c->ev_bal,    &c->ev_app,     &c->ev_fin};
     for (auto* ev : evs) {
         e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return fail(e, "cudaEventCreate");
+    }
+    for (auto& ev : c->ev_bal_l) {
+        e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
         if (e != cudaSuccess) return fail(e, "cudaEventCreate");
     }
     e = cudaDeviceSynchronize();
@@ -454,7 +553,8 @@ cdsp_status cdsp_comm_connect_local(cdsp_comm* comms, int32_t world) {
         CDSP_REQUIRE(comms[i] != nullptr, CDSP_ERR_INVALID, "comms[%d] is NULL", i);
         CDSP_REQUIRE(comms[i]->rank == i && comms[i]->world == world, CDSP_ERR_INVALID,
                      "comms[%d] has rank %d / world %d", i, comms[i]->rank, comms[i]->world);
-        CDSP_REQUIRE(comms[i]->cap == comms[0]->cap && comms[i]->Hkv == comms[0]->Hkv &&
+        CDSP_REQUIRE(comms[i]->cap == comms[0]->cap && comms[i]->n_layers == comms[0]->n_layers &&
+                         comms[i]->Hkv == comms[0]->Hkv &&
                          comms[i]->D == comms[0]->D && comms[i]->dtype == comms[0]->dtype &&
                          comms[i]->device == comms[0]->device,
                      CDSP_ERR_INVALID, "loopback communicators must share geometry and device");
@@ -547,6 +647,8 @@ cdsp_status cdsp_comm_destroy(cdsp_comm c) {
         if (ev) cudaEventDestroy(ev);
     for (auto ev : c->ring_ev)
         if (ev) cudaEventDestroy(ev);
+    for (auto ev : c->ev_bal_l)
+        if (ev) cudaEventDestroy(ev);
     for (int j = 0; j < kMaxWorld; ++j)
         if (c->ipc_base[j]) cudaIpcCloseMemHandle(c->ipc_base[j]);
     if (c->o_acc) cudaFree(c->o_acc);
@@ -565,12 +667,15 @@ cdsp_status cdsp_comm_destroy(cdsp_comm c) {
     return CDSP_OK;
 }
 
-cdsp_status cdsp_kvstore_get(cdsp_comm c, cdsp_kvstore* out) {
+cdsp_status cdsp_kvstore_get(cdsp_comm c, cdsp_kvstore* out) { return cdsp_kvstore_get_layer(c, 0, out); }
+
+cdsp_status cdsp_kvstore_get_layer(cdsp_comm c, int32_t layer, cdsp_kvstore* out) {
     CDSP_REQUIRE(c && out, CDSP_ERR_INVALID, "NULL argument");
-    out->k = cdsp_tensor{c->self.k, c->dtype, c->cap, c->Hkv, c->D};
-    out->v = cdsp_tensor{c->self.v, c->dtype, c->cap, c->Hkv, c->D};
+    CDSP_REQUIRE(layer >= 0 && layer < c->n_layers, CDSP_ERR_INVALID, "layer %d not in [0,%d)", layer, c->n_layers);
+    out->k = cdsp_tensor{layer_k(c, c->self, layer), c->dtype, c->cap, c->Hkv, c->D};
+    out->v = cdsp_tensor{layer_v(c, c->self, layer), c->dtype, c->cap, c->Hkv, c->D};
     out->pos = c->self.pos;
-    out->n = c->n;
+    out->n = c->n_l[layer];
     out->cap = c->cap;
     return CDSP_OK;
 }
@@ -578,7 +683,9 @@ cdsp_status cdsp_kvstore_get(cdsp_comm c, cdsp_kvstore* out) {
 cdsp_status cdsp_kvstore_reset(cdsp_comm c, void* cuda_stream) {
     CDSP_REQUIRE(c != nullptr, CDSP_ERR_INVALID, "NULL comm");
     (void)cuda_stream;  // content is overwritten in stream order by the next chunk
-    c->n = 0;
+    for (auto& n : c->n_l) n = 0;
+    for (auto& pb : c->prebal) pb = -1;
+    c->prebal_plan = nullptr;
     return CDSP_OK;
 }
 
@@ -623,6 +730,12 @@ cdsp_status cdsp_plan_partition(const cdsp_plan* plan, int32_t c, int32_t* tok_r
 cdsp_status cdsp_prefill_chunk(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
                                cdsp_kvstore* prev_kv, const cdsp_sp_group* sp_group, float softmax_scale,
                                cdsp_tensor* out, float* lse, void* cuda_stream) {
+    return cdsp_prefill_chunk_layer(q, k, v, prev_kv, sp_group, 0, softmax_scale, out, lse, cuda_stream);
+}
+
+cdsp_status cdsp_prefill_chunk_layer(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
+                                     cdsp_kvstore* prev_kv, const cdsp_sp_group* sp_group, int32_t layer,
+                                     float softmax_scale, cdsp_tensor* out, float* lse, void* cuda_stream) {
     CDSP_REQUIRE(sp_group && sp_group->comm && sp_group->plan && prev_kv, CDSP_ERR_INVALID,
                  "NULL sp_group/comm/plan/prev_kv");
     CDSP_CHECK_STATUS(check_tensor(q, "q"));
@@ -646,11 +759,14 @@ cdsp_status cdsp_prefill_chunk(const cdsp_tensor* q, const cdsp_tensor* k, const
                  "head dim mismatch");
     CDSP_REQUIRE(k->H == c->Hkv && v->H == c->Hkv, CDSP_ERR_SHAPE, "k/v heads must equal store Hkv=%d", c->Hkv);
     CDSP_REQUIRE(q->H % c->Hkv == 0 && out->H == q->H, CDSP_ERR_SHAPE, "Hq %% Hkv != 0 or out heads != Hq");
-    CDSP_REQUIRE(prev_kv->k.ptr == c->self.k && prev_kv->v.ptr == c->self.v, CDSP_ERR_INVALID,
-                 "prev_kv is not this communicator's store (use cdsp_kvstore_get)");
-    CDSP_REQUIRE(c->n == ci.store_before[r], CDSP_ERR_PLAN,
-                 "store holds %lld rows but the plan expects %lld before chunk %d (missing cdsp_kvstore_reset?)",
-                 static_cast<long long>(c->n), static_cast<long long>(ci.store_before[r]), ci.c);
+    CDSP_REQUIRE(layer >= 0 && layer < c->n_layers, CDSP_ERR_INVALID, "layer %d not in [0,%d)", layer, c->n_layers);
+    CDSP_REQUIRE(prev_kv->k.ptr == layer_k(c, c->self, layer) && prev_kv->v.ptr == layer_v(c, c->self, layer),
+                 CDSP_ERR_INVALID, "prev_kv is not this communicator's layer-%d store (use cdsp_kvstore_get_layer)",
+                 layer);
+    CDSP_REQUIRE(c->n_l[layer] == ci.store_before[r], CDSP_ERR_PLAN,
+                 "layer %d store holds %lld rows but the plan expects %lld before chunk %d (missing "
+                 "cdsp_kvstore_reset?)",
+                 layer, static_cast<long long>(c->n_l[layer]), static_cast<long long>(ci.store_before[r]), ci.c);
     for (int i = 0; i < ci.s; ++i)
         CDSP_REQUIRE(ci.hist[i] + m2 <= c->cap, CDSP_ERR_CAPACITY,
                      "ring rank %d needs %lld store rows, capacity %lld", i,
@@ -667,38 +783,46 @@ cdsp_status cdsp_prefill_chunk(const cdsp_tensor* q, const cdsp_tensor* k, const
         // call that completes the group issues every rank's phases in dependency order, with
         // CUDA events instead of device-side peer barriers
         LocalGroup* g = c->lg;
-        CDSP_REQUIRE(g->pending == 0 || (g->plan == sp_group->plan && g->chunk == sp_group->chunk), CDSP_ERR_INVALID,
-                     "loopback group has a pending call for another chunk");
+        CDSP_REQUIRE(g->pending == 0 ||
+                         (g->plan == sp_group->plan && g->chunk == sp_group->chunk && g->layer == layer),
+                     CDSP_ERR_INVALID, "loopback group has a pending call for another chunk / layer");
         CDSP_REQUIRE(!g->calls[r].set, CDSP_ERR_INVALID, "ring rank %d already called chunk %d", r, ci.c);
         g->plan = sp_group->plan;
         g->chunk = sp_group->chunk;
-        g->calls[r] = PendingCall{*q, *k, *v, *out, lse, prev_kv, scale, st, true};
+        g->layer = layer;
+        g->calls[r] = PendingCall{layer, *q, *k, *v, *out, lse, prev_kv, scale, st, true};
         if (++g->pending < ci.s) return CDSP_OK;
         g->pending = 0;
-        cdsp_status rc = run_group_local(g, ci);
+        cdsp_status rc = run_group_local(g, ci, layer);
         for (int i = 0; i < ci.s; ++i) g->calls[i].set = false;
         return rc;
     }
 
-    // B1
-    if (ci.s > 1) CDSP_CHECK_STATUS(barrier(c, ci, st));
-    // cache balancing (R8)
-    if (ci.s_prev > 0 && ci.s > ci.s_prev) {
-        CDSP_CHECK_STATUS(phase_balance(c, ci, r, st));
-        CDSP_CHECK_STATUS(barrier(c, ci, st));  // B2
+    // B1 (once per chunk: every peer finished the previous chunk, all layers)
+    if (ci.s > 1 && layer == 0) CDSP_CHECK_STATUS(barrier(c, ci, st));
+    // cache balancing (R8) of this layer, unless the previous layer pre-issued it
+    if (balancing(ci)) {
+        if (prebalanced(c, ci, layer, sp_group->plan))
+            CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_bal_l[layer], 0));
+        else
+            CDSP_CHECK_STATUS(phase_balance_pull(c, ci, r, layer, st, true));
+        CDSP_CHECK_STATUS(phase_balance_wait(c, ci, r, st));  // sources: pullers are done with it
     }
-    c->n = ci.hist[r];
-    if (ci.s == 1 && c->n == 0) {
+    int64_t& n = c->n_l[layer];
+    n = ci.hist[r];
+    if (ci.s == 1 && n == 0) {
         // single instance, no history: the attention reads this call's k/v directly while the
         // copy engines append them to the store on the comm stream (no SMs taken from it)
         CDSP_CUDA(cudaEventRecord(c->ev_ready, st));
         CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-        CDSP_CUDA(cudaMemcpyAsync(c->self.k, k->ptr, m2 * c->row_bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
-        CDSP_CUDA(cudaMemcpyAsync(c->self.v, v->ptr, m2 * c->row_bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
+        CDSP_CUDA(cudaMemcpyAsync(layer_k(c, c->self, layer), k->ptr, m2 * c->row_bytes, cudaMemcpyDeviceToDevice,
+                                  c->comm_stream));
+        CDSP_CUDA(cudaMemcpyAsync(layer_v(c, c->self, layer), v->ptr, m2 * c->row_bytes, cudaMemcpyDeviceToDevice,
+                                  c->comm_stream));
         CDSP_CHECK_STATUS(launch_fill_positions(c->self.pos, m2, ci.m, shard_pos0(ci, r), shard_pos1(ci, r),
                                                 c->comm_stream));
-        c->n = m2;
-        prev_kv->n = c->n;
+        n = m2;
+        prev_kv->n = n;
         CDSP_CHECK_STATUS(run_attention_timed(c, q->ptr, k->ptr, v->ptr, c->dtype, Hq, c->Hkv, c->D,
                                               segments_for(ci, r, 0), scale, CDSP_ATTN_ONLY, nullptr, nullptr,
                                               out->ptr, lse, st));
@@ -706,14 +830,16 @@ cdsp_status cdsp_prefill_chunk(const cdsp_tensor* q, const cdsp_tensor* k, const
         CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
         return CDSP_OK;
     }
-    CDSP_CHECK_STATUS(phase_append(c, ci, r, k, v, st));
-    prev_kv->n = c->n;
+    CDSP_CHECK_STATUS(phase_append(c, ci, r, layer, k, v, st));
+    prev_kv->n = n;
     if (ci.s == 1) {
-        return run_attention_timed(c, q->ptr, c->self.k, c->self.v, c->dtype, Hq, c->Hkv, c->D,
-                                   segments_for(ci, r, 0), scale, CDSP_ATTN_ONLY, nullptr, nullptr, out->ptr, lse, st);
+        return run_attention_timed(c, q->ptr, layer_k(c, c->self, layer), layer_v(c, c->self, layer), c->dtype, Hq,
+                                   c->Hkv, c->D, segments_for(ci, r, 0), scale, CDSP_ATTN_ONLY, nullptr, nullptr,
+                                   out->ptr, lse, st);
     }
     CDSP_CHECK_STATUS(barrier(c, ci, st));  // B3
-    return phase_ring(c, ci, r, q->ptr, Hq, out->ptr, lse, scale, st, nullptr);
+    CDSP_CHECK_STATUS(phase_ring(c, ci, r, layer, q->ptr, Hq, out->ptr, lse, scale, st, nullptr));
+    return prebalance_next(c, ci, r, layer, sp_group->plan, true);
 }
 
 // ------------------------------------------------------------------------------- merge

@@ -74,7 +74,8 @@ struct PagedArgs {
 };
 cdsp_status launch_paged_scatter(const PagedArgs& a, cudaStream_t st);
 
-// Peer barrier: signal every listed peer, wait for each peer's matching signal.
+// Peer barrier: signal every listed peer, wait for each peer's matching signal.  remote[j] NULL:
+// wait only; target[j] 0: signal only.
 struct BarrierArgs {
     int n;
     unsigned long long* remote[8];  // peer j's flag slot for this instance (peer memory)

@@ -176,7 +176,7 @@ __global__ void peer_barrier_kernel(const BarrierArgs a) {
     const int j = threadIdx.x;
     if (j >= a.n) return;
     __threadfence_system();  // this stream's prior writes before the signal
-    atomicAdd_system(a.remote[j], 1ull);
+    if (a.remote[j]) atomicAdd_system(a.remote[j], 1ull);  // NULL: wait only
     const uint64_t t0 = gtimer();
     while (true) {
         unsigned long long v;

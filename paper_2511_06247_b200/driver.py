@@ -124,3 +124,57 @@ def run_plan_distributed(q_shards, k_shards, v_shards, plan: api.Plan, comm: api
                           softmax_scale, o, l, stream=stream)
         outs.append(o)
     return outs
+
+
+def run_plan_loopback_layers(qkv_layers, plan: api.Plan, comms: List[api.Comm], softmax_scale: float = 0.0,
+                             streams: Optional[Sequence[torch.cuda.Stream]] = None, between=None):
+    """Layer-wise CDSP prefill on loopback instances (cdsp_prefill_chunk_layer).
+
+    qkv_layers[l] = (q, k, v) full-prompt tensors of layer l.  For every chunk, layers are
+    called in order on every ring rank; ``between(layer, chunk, rank, stream)`` (optional) runs
+    the caller's per-layer work (e.g. an FC stand-in) on each rank's stream after its layer call
+    — the window the next layer's cache balancing overlaps (Fig. 6-b).
+    Returns per layer (out [N,Hq,D], lse [Hq,N])."""
+    q0 = qkv_layers[0][0]
+    device = q0.device
+    N, Hq, D = q0.shape
+    n_layers = len(qkv_layers)
+    world = len(comms)
+    if streams is None:
+        streams = [torch.cuda.Stream(device=device) for _ in range(world)]
+    cur = torch.cuda.current_stream(device)
+    for s in streams:
+        s.wait_stream(cur)
+    for cm in comms:
+        cm.reset(cur)
+    shards = [prepare_shards(q, k, v, plan) for q, k, v in qkv_layers]
+    for s in streams:
+        s.wait_stream(cur)
+    outs = [alloc_out_shards(plan, Hq, D, q0.dtype, device) for _ in range(n_layers)]
+    res = [(torch.empty_like(q0), torch.empty((Hq, N), dtype=torch.float32, device=device)) for _ in range(n_layers)]
+    for c, (L, ranks) in enumerate(plan.chunks):
+        for l in range(n_layers):
+            for r, inst in enumerate(ranks):
+                qs, ks, vs = shards[l][c][r]
+                o_r, l_r = outs[l][c][r]
+                api.prefill_chunk(qs, ks, vs, comms[inst].kvstore(l), api.SpGroup(comms[inst], plan, c),
+                                  softmax_scale, o_r, l_r, stream=streams[inst], layer=l)
+            if between is not None:
+                for r, inst in enumerate(ranks):
+                    with torch.cuda.stream(streams[inst]):
+                        between(l, c, r, streams[inst])
+    C = 0
+    for c, (L, ranks) in enumerate(plan.chunks):
+        for r, inst in enumerate(ranks):
+            idx = _rank_lse_index(plan, c, r, device)
+            for l in range(n_layers):
+                o_r, l_r = outs[l][c][r]
+                with torch.cuda.stream(streams[inst]):
+                    api.zigzag_scatter(o_r, len(ranks), r, res[l][0][C:C + L], stream=streams[inst])
+                    res[l][1].index_copy_(1, idx, l_r)
+        C += L
+    for s in streams:
+        cur.wait_stream(s)
+    for cm in comms:
+        cm.check()
+    return res

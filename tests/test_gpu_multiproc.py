@@ -25,7 +25,9 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, plan_list=PLAN, n_layers=None, seed=31):
+    """n_layers None: single-store API (cdsp_prefill_chunk); else the layered API, layers called
+    in order per chunk with a matmul between them (the FC stand-in the balancing overlaps)."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), CUDA_DEVICE_MAX_CONNECTIONS="32")
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -33,26 +35,36 @@ def _worker(rank, world, port, q):
         torch.cuda.set_device(0)
         from cdsp_inputs import qkv
         from paper_2511_06247_b200 import api, dist_utils
-        dist_utils.check_plan_consistent(PLAN)
-        plan = api.Plan(PLAN)
-        comm = api.Comm(rank, world, 0, api.plan_capacity(plan), HKV, D, torch.bfloat16)
+        dist_utils.check_plan_consistent(plan_list)
+        plan = api.Plan(plan_list)
+        layers = [None] if n_layers is None else list(range(n_layers))
+        comm = api.Comm(rank, world, 0, api.plan_capacity(plan), HKV, D, torch.bfloat16, n_layers=len(layers))
         comm.connect_process_group()
-        qf, kf, vf = (t.cuda() for t in qkv(N, HQ, HKV, D, torch.bfloat16, seed=31))
+        data = [tuple(t.cuda() for t in qkv(N, HQ, HKV, D, torch.bfloat16, seed=seed + (l or 0))) for l in layers]
+        fc = torch.randn(2048, 2048, device="cuda", dtype=torch.bfloat16)
         outs = []
-        for c, (L, ranks) in enumerate(PLAN):
+        for c, (L, ranks) in enumerate(plan_list):
+            if rank not in ranks:
+                continue
             C = plan.chunk_start(c)
             s = len(ranks)
             r = ranks.index(rank)
-            qs = api.zigzag_gather(qf[C:C + L].contiguous(), s, r)
-            ks = api.zigzag_gather(kf[C:C + L].contiguous(), s, r)
-            vs = api.zigzag_gather(vf[C:C + L].contiguous(), s, r)
-            o = torch.empty_like(qs)
-            lse = torch.empty((HQ, qs.shape[0]), dtype=torch.float32, device="cuda")
-            api.prefill_chunk(qs, ks, vs, comm.kvstore(), api.SpGroup(comm, plan, c), 0.0, o, lse)
+            _, _, rank_pos, _ = api.plan_partition(plan, c)
+            for li, l in enumerate(layers):
+                qf, kf, vf = data[li]
+                qs = api.zigzag_gather(qf[C:C + L].contiguous(), s, r)
+                ks = api.zigzag_gather(kf[C:C + L].contiguous(), s, r)
+                vs = api.zigzag_gather(vf[C:C + L].contiguous(), s, r)
+                o = torch.empty_like(qs)
+                lse = torch.empty((HQ, qs.shape[0]), dtype=torch.float32, device="cuda")
+                api.prefill_chunk(qs, ks, vs, comm.kvstore(l or 0), api.SpGroup(comm, plan, c), 0.0, o, lse,
+                                  layer=l)
+                for _ in range(4):
+                    fc = fc @ fc * 1e-3  # FC-layer stand-in on the same stream
+                outs.append((li, rank_pos[r], o, lse))
             torch.cuda.synchronize()
             comm.check()
-            _, _, rank_pos, _ = api.plan_partition(plan, c)
-            outs.append((rank_pos[r], o.float().cpu().numpy(), lse.cpu().numpy()))
+        outs = [(li, pos, o.float().cpu().numpy(), lse.cpu().numpy()) for li, pos, o, lse in outs]
         dist.barrier()
         comm.close()
         q.put((rank, outs, None))
@@ -62,14 +74,14 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_processes_ipc_ring_matches_oracle():
+def _run_two(plan_list, n_layers, seed):
     import oracle
     from cdsp_inputs import qkv
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, plan_list, n_layers, seed)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -80,15 +92,30 @@ def test_two_processes_ipc_ring_matches_oracle():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    qf, kf, vf = qkv(N, HQ, HKV, D, torch.bfloat16, seed=31)
+    data = [qkv(N, HQ, HKV, D, torch.bfloat16, seed=seed + li) for li in range(n_layers or 1)]
+    checked = 0
     for r in range(world):
-        for pos, o, lse in res[r]:
+        for li, pos, o, lse in res[r]:
+            qf, kf, vf = data[li]
             sel = pos[:: max(1, len(pos) // 96)]
             o_ref, l_ref = oracle.causal_rows(qf.float().numpy(), kf.float().numpy(), vf.float().numpy(),
                                               1.0 / math.sqrt(D), rows=sel)
             idx = np.searchsorted(pos, sel) if np.all(np.diff(pos) > 0) else np.array([list(pos).index(x) for x in sel])
-            assert np.abs(o[idx] - o_ref).max() <= 2e-2
-            assert np.abs(lse[:, idx] - l_ref).max() <= 1e-3
+            assert np.abs(o[idx] - o_ref).max() <= 2e-2, (r, li)
+            assert np.abs(lse[:, idx] - l_ref).max() <= 1e-3, (r, li)
+            checked += 1
+    assert checked == sum(len(ranks) for _, ranks in plan_list) * (n_layers or 1)
+
+
+def test_two_processes_ipc_ring_matches_oracle():
+    _run_two(PLAN, None, 31)
+
+
+def test_two_processes_layered_balancing_acks():
+    """Layered API across processes with a growing group (s 1 -> 2): layer 0 balances inline,
+    layers 1, 2 are pre-balanced on the comm stream during the previous layer, and the old
+    rank overwrites the moved half only after the new rank's cross-process acknowledgement."""
+    _run_two([(1024, [0]), (1024, [0, 1]), (2048, [0, 1])], 3, 41)
 
 
 def test_bench_torchrun_two_ranks_one_gpu():
