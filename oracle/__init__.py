@@ -48,10 +48,12 @@ def lib():
         _lib.oracle_causal_rows.argtypes = [P, P, P, i64, i32, i32, i32, dbl, P, i64, P, P]
         _lib.oracle_zigzag_map.argtypes = [i64, i32, P, P]
         _lib.oracle_plan_stores.argtypes = [i32, P, P, P, i32, P, P, i64, P, P]
+        _lib.oracle_plan_stores_il.argtypes = [i32, P, P, P, P, i32, P, P, i64, P, P]
+        _lib.oracle_striped_map.argtypes = [i64, i32, P, P]
         _lib.oracle_paged_write.argtypes = [P, P, i64, i32, i32, i32, i32, i32, P, i64, i64, P]
         _lib.oracle_lse_merge.argtypes = [i32, P, P, i64, i32, i32, P, P]
-        for f in ("oracle_attention", "oracle_causal_rows", "oracle_zigzag_map",
-                  "oracle_plan_stores", "oracle_paged_write", "oracle_lse_merge",
+        for f in ("oracle_attention", "oracle_causal_rows", "oracle_zigzag_map", "oracle_striped_map",
+                  "oracle_plan_stores", "oracle_plan_stores_il", "oracle_paged_write", "oracle_lse_merge",
                   "oracle_num_threads"):
             getattr(_lib, f).restype = ctypes.c_int
     return _lib
@@ -127,10 +129,18 @@ def zigzag_map(L: int, s: int):
     return tr, ts
 
 
-def rank_positions(L: int, s: int, C: int = 0):
+def striped_map(L: int, s: int):
+    """(tok_rank int32 [L], tok_slot int32 [L]) of the striped (round-robin) partition."""
+    tr = np.empty(L, np.int32)
+    ts = np.empty(L, np.int32)
+    _check(lib().oracle_striped_map(L, s, _p(tr), _p(ts)), "oracle_striped_map")
+    return tr, ts
+
+
+def rank_positions(L: int, s: int, C: int = 0, interleave: str = "zigzag"):
     """[s, 2m] int64 global positions of each ring rank's shard rows, derived from the
-    oracle's zigzag map (row tok_slot[t] of rank tok_rank[t] holds position C + t)."""
-    tr, ts = zigzag_map(L, s)
+    oracle's zigzag (or striped) map (row tok_slot[t] of rank tok_rank[t] holds position C + t)."""
+    tr, ts = (striped_map if interleave == "striped" else zigzag_map)(L, s)
     m = L // (2 * s)
     pos = np.full((s, 2 * m), -1, np.int64)
     pos[tr, ts] = C + np.arange(L, dtype=np.int64)
@@ -140,12 +150,13 @@ def rank_positions(L: int, s: int, C: int = 0):
 def plan_stores(plan, upto: int):
     """Store state right before chunk `upto` computes (after its balancing).
 
-    plan: list of (len, [ring-order instance ids]).
+    plan: list of (len, [ring-order instance ids]) or (len, ids, "striped" | "zigzag").
     Returns (store_n [s], store_pos list of int64 arrays, moves list of (src,dst,off,n))."""
     n_chunks = len(plan)
     lens = np.array([c[0] for c in plan], np.int64)
     sps = np.array([len(c[1]) for c in plan], np.int32)
     ranks = np.array([r for c in plan for r in c[1]], np.int32)
+    il = np.array([1 if (len(c) > 2 and c[2] == "striped") else 0 for c in plan], np.int32)
     total = int(lens.sum())
     s = int(sps[upto])
     store_n = np.zeros(s, np.int64)
@@ -153,8 +164,8 @@ def plan_stores(plan, upto: int):
     store_pos = np.zeros((s, stride), np.int64)
     moves = np.zeros((8, 4), np.int64)
     nm = np.zeros(1, np.int32)
-    _check(lib().oracle_plan_stores(n_chunks, _p(lens), _p(sps), _p(ranks), upto, _p(store_n),
-                                    _p(store_pos), stride, _p(moves), _p(nm)), "oracle_plan_stores")
+    _check(lib().oracle_plan_stores_il(n_chunks, _p(lens), _p(sps), _p(ranks), _p(il), upto, _p(store_n),
+                                       _p(store_pos), stride, _p(moves), _p(nm)), "oracle_plan_stores")
     return (store_n, [store_pos[i, :store_n[i]].copy() for i in range(s)],
             [tuple(int(x) for x in moves[i]) for i in range(int(nm[0]))])
 

@@ -13,6 +13,7 @@
  *   oracle_attention        exact masked softmax attention (definition)
  *   oracle_causal_rows      the same over the whole unsharded prompt, for selected rows
  *   oracle_zigzag_map       zigzag 2N-shard partition, chunk-local (R5)
+ *   oracle_striped_map      striped (round-robin) partition
  *   oracle_plan_stores      CDSP cache balancing + store contents per chunk (R8, R9)
  *   oracle_paged_write      decode paged-KV writer (R15)
  *   oracle_lse_merge        n-way log-sum-exp merge of partial attention (R3)
@@ -172,6 +173,23 @@ int oracle_zigzag_map(int64_t L, int s, int32_t* tok_rank, int32_t* tok_slot) {
 }
 
 /*
+ * Striped partition, chunk-local.  P:75 (§2.3): "Striped Attention [5] partitions the
+ * sequence into evenly-spaced stripes and assigns them to each instance in a round-robin
+ * manner, so that each instance can conduct computation to every KV cache shard"; P:161:
+ * "we can still adopt striped/zigzag attention to achieve intra-chunk attention load
+ * balance".  Stripes of one token: token t belongs to instance t mod s and is row t / s
+ * of its shard (reading R20; the chunk length rule R6, L % 2s == 0, is kept for both).
+ */
+int oracle_striped_map(int64_t L, int s, int32_t* tok_rank, int32_t* tok_slot) {
+    if (s <= 0 || L < 0 || (L % (2 * (int64_t)s)) != 0) return ORACLE_ERR_ARG;
+    for (int64_t t = 0; t < L; ++t) {
+        if (tok_rank) tok_rank[t] = (int32_t)(t % s);   /* round-robin owner */
+        if (tok_slot) tok_slot[t] = (int32_t)(t / s);   /* stripe index      */
+    }
+    return ORACLE_OK;
+}
+
+/*
  * CDSP store simulation: the plan A = [(token count, instance group)] (D1) is run
  * through P:155 (§4.1, Fig. 5): "each chunk's tokens are evenly interleaved across the
  * assigned prefill instance group.  All instance groups compute sequentially following
@@ -198,9 +216,22 @@ int oracle_zigzag_map(int64_t L, int s, int32_t* tok_rank, int32_t* tok_slot) {
  * of chunk `upto`'s balancing; *n_moves their count.  Returns ORACLE_ERR_PLAN for an
  * illegal plan.
  */
+int oracle_plan_stores_il(int n_chunks, const int64_t* len, const int32_t* sp, const int32_t* ranks,
+                          const int32_t* interleave, int upto, int64_t* store_n, int64_t* store_pos,
+                          int64_t pos_stride, int64_t* moves, int32_t* n_moves);
+
 int oracle_plan_stores(int n_chunks, const int64_t* len, const int32_t* sp, const int32_t* ranks,
                        int upto, int64_t* store_n, int64_t* store_pos, int64_t pos_stride,
                        int64_t* moves, int32_t* n_moves) {
+    return oracle_plan_stores_il(n_chunks, len, sp, ranks, NULL, upto, store_n, store_pos, pos_stride, moves,
+                                 n_moves);
+}
+
+/* As oracle_plan_stores; interleave[c] (NULL: all zigzag) = 0 zigzag, 1 striped picks how
+ * chunk c's tokens are interleaved ("striped/zigzag"), i.e. the shard appended. */
+int oracle_plan_stores_il(int n_chunks, const int64_t* len, const int32_t* sp, const int32_t* ranks,
+                          const int32_t* interleave, int upto, int64_t* store_n, int64_t* store_pos,
+                          int64_t pos_stride, int64_t* moves, int32_t* n_moves) {
     if (n_chunks <= 0 || !len || !sp || !ranks || upto < 0 || upto >= n_chunks || !store_n)
         return ORACLE_ERR_ARG;
     /* validate the plan (R9) */
@@ -278,17 +309,23 @@ int oracle_plan_stores(int n_chunks, const int64_t* len, const int32_t* sp, cons
         /* 2. compute chunk c, then append each rank's zigzag shard to its store */
         const int64_t L = len[c];
         const int64_t m = L / (2 * (int64_t)s);
+        const int striped = interleave && interleave[c] == 1;
+        if (interleave && interleave[c] != 0 && interleave[c] != 1) { rc = ORACLE_ERR_PLAN; break; }
         for (int i = 0; i < s; ++i) {
             const int inst = grp[i];
             int64_t n = stn[inst];
-            for (int64_t x = 0; x < m; ++x) st[inst][n++] = C + (int64_t)i * m + x;               /* S_i */
-            for (int64_t x = 0; x < m; ++x) st[inst][n++] = C + (int64_t)(2 * s - 1 - i) * m + x; /* S_{2s-1-i} */
+            if (striped) {
+                for (int64_t x = 0; x < L / s; ++x) st[inst][n++] = C + x * s + i;                 /* stripe x */
+            } else {
+                for (int64_t x = 0; x < m; ++x) st[inst][n++] = C + (int64_t)i * m + x;            /* S_i */
+                for (int64_t x = 0; x < m; ++x) st[inst][n++] = C + (int64_t)(2 * s - 1 - i) * m + x; /* S_{2s-1-i} */
+            }
             stn[inst] = n;
         }
         C += L;
         off += s;
     }
-    {
+    if (rc == ORACLE_OK) {
         const int s = sp[upto];
         const int32_t* grp = ranks + off;
         for (int i = 0; i < s; ++i) {

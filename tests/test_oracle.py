@@ -235,6 +235,82 @@ def test_zigzag_rejects_ragged():
         oracle.zigzag_map(10, 4)
 
 
+# ---- striped partition ---------------------------------
+
+def test_striped_matches_paper_definition_golden():
+    """golden/striped_p75.txt: round-robin owners of one-token stripes."""
+    n_rows = 0
+    with open(os.path.join(GOLDEN, "striped_p75.txt")) as f:
+        for line in f:
+            if not line.strip() or line.startswith("#"):
+                continue
+            head, owners = line.split("|")
+            N, L = (int(x) for x in head.split())
+            owners = [int(x) for x in owners.split()]
+            tr, ts = oracle.striped_map(L, N)
+            assert tr.tolist() == owners
+            # within an instance, its tokens keep their order (slot = stripe index)
+            for inst in range(N):
+                np.testing.assert_array_equal(ts[tr == inst], np.arange(L // N))
+            n_rows += 1
+    assert n_rows == 4
+
+
+@pytest.mark.parametrize("s", [1, 2, 4, 8])
+@pytest.mark.parametrize("n", [2, 6, 16])
+def test_striped_permutation_and_work_closed_form(s, n):
+    """Permutation; causal work of rank r = s n(n-1)/2 + n(r+1) for n = L/s tokens per rank
+    (sum over its tokens i s + r of i s + r + 1): every rank within n(s-1) pairs of every
+    other — near balance, not zigzag's exact balance."""
+    L = s * n
+    if L % (2 * s):
+        pytest.skip("R6: L % 2s == 0")
+    tr, ts = oracle.striped_map(L, s)
+    assert len(set(zip(tr.tolist(), ts.tolist()))) == L
+    work = np.zeros(s, np.int64)
+    np.add.at(work, tr, np.arange(L) + 1)
+    for r in range(s):
+        assert work[r] == s * n * (n - 1) // 2 + n * (r + 1)
+    assert work.max() - work.min() == n * (s - 1)
+
+
+@pytest.mark.parametrize("s", [2, 4, 8])
+def test_striped_per_step_shifted_causal(s):
+    """Ring step with source src: q row i (position i s + r) sees kv row j (j s + src) iff
+    j <= i (src <= r) or j < i (src > r) — a shifted causal mask; brute force."""
+    n = 6
+    pos = oracle.rank_positions(s * n, s, interleave="striped")
+    for r in range(s):
+        for src in range(s):
+            vis = pos[src][None, :] <= pos[r][:, None]
+            i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+            expect = (j <= i) if src <= r else (j < i)
+            np.testing.assert_array_equal(vis, expect)
+            assert vis.sum() == (n * (n + 1) // 2 if src <= r else n * (n - 1) // 2)
+
+
+def test_striped_rejects_ragged():
+    with pytest.raises(oracle.OracleError):
+        oracle.striped_map(12, 4)
+
+
+def test_striped_plan_stores():
+    """Striped chunks append their stripes; balancing (R8) and conservation are unchanged."""
+    plan = [(64, [0, 1], "striped"), (64, [0, 1, 2, 3]), (128, list(range(8)), "striped"),
+            (32, list(range(8)), "striped")]
+    C = 0
+    for c in range(len(plan)):
+        n, pos, _ = oracle.plan_stores(plan, c)
+        np.testing.assert_array_equal(np.sort(np.concatenate(pos)), np.arange(C))
+        if C > 0:
+            assert n.max() - n.min() <= 1
+        C += plan[c][0]
+    # chunk 0 (striped over [0, 1]): rank r's store before chunk 1's balancing = r, r+2, ...
+    n, pos, _ = oracle.plan_stores([(64, [0, 1], "striped"), (32, [0, 1])], 1)
+    for r in range(2):
+        np.testing.assert_array_equal(pos[r], np.arange(r, 64, 2))
+
+
 # ---- cache balancing (P:155) --------------------------------------------------------------
 
 def test_balancing_matches_fig5():
