@@ -12,7 +12,8 @@ One step = one pass of the whole hot path over the chunk:
   a4-a6 cdsp_prefill_chunk: store append, ring KV exchange (s>1), block attention with the
         LSE merge fused into its epilogue
   a2 zigzag scatter of the output shard (cdsp_zigzag_scatter)
-  a7 KV transfer into decode paged caches (cdsp_kv_transfer_to_decode)
+  a7 KV transfer into decode paged caches (cdsp_kv_transfer_to_decode), on a side stream
+     concurrent with a4-a6 (the chunk's KV is final before its attention starts)
 (a3 balancing does not occur in a single-chunk plan.)
 
 value = algorithmic attention FLOPs of the chunk, 4*d*Hq*L(L+1)/2, over the
@@ -248,6 +249,12 @@ def main():
     # steps, output scatter, paged scatter
     launches_per_step = 3 if s == 1 else 3 + 2 + 1 + s + 1 + 1
 
+    # a7 runs on its own stream: the chunk's KV is final once its shard exists, so the transfer
+    # to the decode caches streams out while the attention computes ("dedicated ... streams";
+    # HBM-bound scatter beside a tensor-bound kernel); the step ends when both are done
+    xfer = torch.cuda.Stream(dev)
+    ev_kv = torch.cuda.Event()
+
     def step(qq=None, kk=None, vv=None, oo=None):
         qq, kk, vv, oo = (qq if qq is not None else q), (kk if kk is not None else k), \
             (vv if vv is not None else v), (oo if oo is not None else out_full)
@@ -256,15 +263,21 @@ def main():
         if s == 1:
             # one rank: the zigzag partition (S_0 then S_1) is the identity, so the shard IS the
             # chunk and a2 moves no data; the output is written in place
+            ev_kv.record(stream)
+            xfer.wait_event(ev_kv)
+            api.kv_transfer_to_decode(kk, vv, group, dst, xfer)
             api.prefill_chunk(qq, kk, vv, comm.kvstore(), group, 0.0, oo, lse_s, stream)
-            api.kv_transfer_to_decode(kk, vv, group, dst, stream)
+            stream.wait_stream(xfer)
             return
         api.zigzag_gather(qq, s, rank, qs, stream)
         api.zigzag_gather(kk, s, rank, ks, stream)
         api.zigzag_gather(vv, s, rank, vs, stream)
+        ev_kv.record(stream)
+        xfer.wait_event(ev_kv)
+        api.kv_transfer_to_decode(ks, vs, group, dst, xfer)
         api.prefill_chunk(qs, ks, vs, comm.kvstore(), group, 0.0, out_s, lse_s, stream)
         api.zigzag_scatter(out_s, s, rank, oo, stream)
-        api.kv_transfer_to_decode(ks, vs, group, dst, stream)
+        stream.wait_stream(xfer)  # ks/vs are rewritten by the next step's gathers
 
     def barrier():
         if dist is not None:

@@ -45,7 +45,7 @@ extern "C" {
 #define CDSP_API
 #endif
 
-#define CDSP_ABI_VERSION 1
+#define CDSP_ABI_VERSION 2
 #define CDSP_IPC_HANDLE_BYTES 64   /* one cudaIpcMemHandle_t */
 #define CDSP_MAX_SP 8
 
@@ -63,6 +63,12 @@ typedef enum {
 
 typedef enum { CDSP_F32 = 0, CDSP_BF16 = 1 } cdsp_dtype;
 
+/* How a chunk's tokens are interleaved over its group ("striped/zigzag"; R5, R20):
+ * ZIGZAG: 2s shards S_j = [j m, (j+1) m), ring rank i holds S_i then S_{2s-1-i};
+ * STRIPED ("evenly-spaced stripes ... round-robin"): token t -> ring rank t mod s,
+ * shard row t / s. */
+typedef enum { CDSP_ZIGZAG = 0, CDSP_STRIPED = 1 } cdsp_interleave;
+
 /* A contiguous device tensor [T, H, D]; element type `dtype`. */
 typedef struct {
     void* ptr;
@@ -78,6 +84,7 @@ typedef struct {
 typedef struct {
     int64_t len;
     int32_t sp;
+    int32_t interleave;     /* cdsp_interleave (0 = zigzag) */
     const int32_t* ranks;   /* host memory */
 } cdsp_chunk;
 
@@ -192,7 +199,8 @@ CDSP_API cdsp_status cdsp_plan_capacity(const cdsp_plan* plan, int64_t* rows);
  * earlier chunks) writes (NULL outputs are skipped):
  *   tok_rank[L], tok_slot[L]: chunk-local token t is row tok_slot[t] of ring rank
  *       tok_rank[t]'s shard; zigzag: shard S_j = [j m, (j+1) m) belongs to ring rank
- *       j (j < s) or 2s-1-j, and rank i's shard is S_i followed by S_{2s-1-i};
+ *       j (j < s) or 2s-1-j, and rank i's shard is S_i followed by S_{2s-1-i}; striped
+ *       chunks (R20): tok_rank[t] = t mod s, tok_slot[t] = t / s;
  *   rank_pos[s * 2m]: global position (C + local) of each shard row, rank-major;
  *   moves[<= CDSP_MAX_SP], *n_moves: the balancing transfers executed before chunk c (R8).
  * Errors: CDSP_ERR_INVALID, CDSP_ERR_PLAN. */
@@ -201,8 +209,8 @@ CDSP_API cdsp_status cdsp_plan_partition(const cdsp_plan* plan, int32_t c, int32
                                          int32_t* n_moves);
 
 /* Collective over plan->chunks[chunk].ranks.  The calling instance is ring rank r.
- *   q [2m, Hq, D], k/v [2m, Hkv, D]: this rank's zigzag shard of the chunk (S_r then
- *     S_{2s-1-r}), post-projection ("each instance first calculates its local tokens'
+ *   q [2m, Hq, D], k/v [2m, Hkv, D]: this rank's shard of the chunk (zigzag: S_r then
+ *     S_{2s-1-r}; striped: tokens r, r + s, r + 2s, ...), post-projection ("each instance first calculates its local tokens'
  *     query, key, value"), dtype bf16 or f32 (all equal, = store dtype).
  *   prev_kv: this instance's store view (cdsp_kvstore_get).  Before the chunk, history is
  *     re-balanced from the previous group (R8); afterwards k/v are appended and
@@ -299,14 +307,16 @@ CDSP_API cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_deco
  * Building blocks, exported for tests and benches (same kernels the path uses)
  * ------------------------------------------------------------------------------- */
 
-/* Segment description of one block-attention launch (one ring step).  Query row i has
- * global position q_pos0 + i for i < q_len0, else q_pos1 + (i - q_len0).  KV rows
- * [0, kv_hist) are history (always visible); row kv_hist + j has position
- * kv_pos0 + j for j < kv_len0, else kv_pos1 + (j - kv_len0).  Key visible iff its
- * position <= the query's (R4).  Rows >= nq / >= nkv do not exist. */
+/* Segment description of one block-attention launch (one ring step).  With st = pos_stride
+ * (0 or 1: contiguous; s for a striped chunk), query row i has global position
+ * q_pos0 + i st for i < q_len0, else q_pos1 + (i - q_len0) st.  KV rows [0, kv_hist) are
+ * history (always visible); row kv_hist + j has position kv_pos0 + j st for
+ * j < kv_len0, else kv_pos1 + (j - kv_len0) st.  Key visible iff its position <= the
+ * query's (R4).  Rows >= nq / >= nkv do not exist. */
 typedef struct {
     int64_t nq, q_len0, q_pos0, q_pos1;
     int64_t nkv, kv_hist, kv_len0, kv_pos0, kv_pos1;
+    int64_t pos_stride;
 } cdsp_segments;
 
 /* Merge mode of cdsp_attention_fwd. */
@@ -331,6 +341,13 @@ CDSP_API cdsp_status cdsp_zigzag_gather(const cdsp_tensor* full, int32_t s, int3
                                         void* cuda_stream);
 CDSP_API cdsp_status cdsp_zigzag_scatter(const cdsp_tensor* shard, int32_t s, int32_t r, cdsp_tensor* full,
                                          void* cuda_stream);
+
+/* Striped gather / scatter (R20): full [L, H, D] <-> ring rank r's shard [L/s, H, D]
+ * (shard row i = full row i s + r).  L % 2s == 0.  Bit-exact. */
+CDSP_API cdsp_status cdsp_striped_gather(const cdsp_tensor* full, int32_t s, int32_t r, cdsp_tensor* shard,
+                                         void* cuda_stream);
+CDSP_API cdsp_status cdsp_striped_scatter(const cdsp_tensor* shard, int32_t s, int32_t r, cdsp_tensor* full,
+                                          void* cuda_stream);
 
 /* Device zigzag maps: tok_rank / tok_slot int32 [L] device. */
 CDSP_API cdsp_status cdsp_zigzag_map_device(int64_t L, int32_t s, int32_t* tok_rank, int32_t* tok_slot,

@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = (
     "cdsp_kv_transfer_errors", "cdsp_last_error", "cdsp_abi_version", "cdsp_comm_profile",
     "cdsp_comm_profile_read", "cdsp_decode_workspace_bytes", "cdsp_decode_attention", "cdsp_comm_profile_ring",
     "cdsp_comm_create_layers", "cdsp_kvstore_get_layer", "cdsp_prefill_chunk_layer",
+    "cdsp_striped_gather", "cdsp_striped_scatter",
 )
 
 
@@ -49,7 +50,8 @@ class Tensor(ctypes.Structure):
 
 
 class Chunk(ctypes.Structure):
-    _fields_ = [("len", ctypes.c_int64), ("sp", ctypes.c_int32), ("ranks", ctypes.POINTER(ctypes.c_int32))]
+    _fields_ = [("len", ctypes.c_int64), ("sp", ctypes.c_int32), ("interleave", ctypes.c_int32),
+                ("ranks", ctypes.POINTER(ctypes.c_int32))]
 
 
 class PlanC(ctypes.Structure):
@@ -78,7 +80,7 @@ class DecodeTargetC(ctypes.Structure):
 
 class Segments(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("nq", "q_len0", "q_pos0", "q_pos1", "nkv", "kv_hist",
-                                              "kv_len0", "kv_pos0", "kv_pos1")]
+                                              "kv_len0", "kv_pos0", "kv_pos1", "pos_stride")]
 
 
 _lib = None
@@ -120,6 +122,8 @@ def lib():
                                                                   ctypes.POINTER(Tensor), P, P],
             "cdsp_zigzag_gather": [ctypes.POINTER(Tensor), i32, i32, ctypes.POINTER(Tensor), P],
             "cdsp_zigzag_scatter": [ctypes.POINTER(Tensor), i32, i32, ctypes.POINTER(Tensor), P],
+            "cdsp_striped_gather": [ctypes.POINTER(Tensor), i32, i32, ctypes.POINTER(Tensor), P],
+            "cdsp_striped_scatter": [ctypes.POINTER(Tensor), i32, i32, ctypes.POINTER(Tensor), P],
             "cdsp_zigzag_map_device": [i64, i32, P, P, P],
             "cdsp_kv_transfer_errors": [P, P, ctypes.POINTER(i64)],
             "cdsp_comm_profile": [P, i32],
@@ -176,15 +180,21 @@ def _ptr(x: Optional[torch.Tensor]):
 
 
 # ---- plan ----------------------------------------------------------------------------------
+INTERLEAVE = {"zigzag": 0, "striped": 1}
+
+
 class Plan:
-    """CDSP plan A = [(token count, ring-order instance group)]."""
+    """CDSP plan A = [(token count, ring-order instance group[, "zigzag" | "striped"])] (P:233;
+    interleave per chunk, "striped/zigzag", default zigzag)."""
 
     def __init__(self, chunks: Sequence[tuple]):
-        self.chunks = [(int(L), [int(r) for r in ranks]) for L, ranks in chunks]
+        self.chunks = [(int(c[0]), [int(r) for r in c[1]]) for c in chunks]
+        self.interleave = [c[2] if len(c) > 2 else "zigzag" for c in chunks]
         self._rank_arrays = [(ctypes.c_int32 * len(r))(*r) for _, r in self.chunks]
         arr = (Chunk * len(self.chunks))()
         for i, (L, r) in enumerate(self.chunks):
-            arr[i] = Chunk(L, len(r), ctypes.cast(self._rank_arrays[i], ctypes.POINTER(ctypes.c_int32)))
+            arr[i] = Chunk(L, len(r), INTERLEAVE[self.interleave[i]],
+                           ctypes.cast(self._rank_arrays[i], ctypes.POINTER(ctypes.c_int32)))
         self._arr = arr
         self.c = PlanC(len(self.chunks), ctypes.cast(arr, ctypes.POINTER(Chunk)))
 
@@ -419,13 +429,13 @@ def kv_transfer_errors(comm: Comm, stream=None) -> int:
 
 
 # ---- building blocks ------------------------------------------------------------------------------
-def segments(nq, q_len0, q_pos0, q_pos1, nkv, kv_hist, kv_len0, kv_pos0, kv_pos1) -> Segments:
-    return Segments(nq, q_len0, q_pos0, q_pos1, nkv, kv_hist, kv_len0, kv_pos0, kv_pos1)
+def segments(nq, q_len0, q_pos0, q_pos1, nkv, kv_hist, kv_len0, kv_pos0, kv_pos1, pos_stride=1) -> Segments:
+    return Segments(nq, q_len0, q_pos0, q_pos1, nkv, kv_hist, kv_len0, kv_pos0, kv_pos1, pos_stride)
 
 
 def causal_segments(nq: int, nkv: int, q_pos0: int = 0, kv_hist: int = 0) -> Segments:
     """Contiguous queries at q_pos0.. over kv_hist history rows + contiguous keys at 0.."""
-    return Segments(nq, nq, q_pos0, 0, nkv, kv_hist, nkv - kv_hist, 0, 0)
+    return Segments(nq, nq, q_pos0, 0, nkv, kv_hist, nkv - kv_hist, 0, 0, 1)
 
 
 def attention_fwd(q, k, v, seg: Segments, softmax_scale: float = 0.0, mode: int = ATTN_ONLY,
@@ -444,6 +454,31 @@ def zigzag_gather(full, s: int, r: int, shard=None, stream=None):
     tf, ts = as_tensor(full), as_tensor(shard)
     _check(lib().cdsp_zigzag_gather(ctypes.byref(tf), s, r, ctypes.byref(ts), _stream(stream)))
     return shard
+
+
+def striped_gather(full, s: int, r: int, shard=None, stream=None):
+    if shard is None:
+        shard = torch.empty((full.shape[0] // s,) + tuple(full.shape[1:]), dtype=full.dtype, device=full.device)
+    tf, ts = as_tensor(full), as_tensor(shard)
+    _check(lib().cdsp_striped_gather(ctypes.byref(tf), s, r, ctypes.byref(ts), _stream(stream)))
+    return shard
+
+
+def striped_scatter(shard, s: int, r: int, full, stream=None):
+    ts, tf = as_tensor(shard), as_tensor(full)
+    _check(lib().cdsp_striped_scatter(ctypes.byref(ts), s, r, ctypes.byref(tf), _stream(stream)))
+    return full
+
+
+def shard_gather(full, s: int, r: int, interleave: str = "zigzag", shard=None, stream=None):
+    """This ring rank's shard of a chunk under the chunk's interleave."""
+    f = striped_gather if interleave == "striped" else zigzag_gather
+    return f(full, s, r, shard, stream)
+
+
+def shard_scatter(shard, s: int, r: int, full, interleave: str = "zigzag", stream=None):
+    f = striped_scatter if interleave == "striped" else zigzag_scatter
+    return f(shard, s, r, full, stream)
 
 
 def zigzag_scatter(shard, s: int, r: int, full, stream=None):

@@ -15,8 +15,9 @@ namespace cdsp {
 
 enum TileKind : int { TILE_EMPTY = 0, TILE_FULL = 1, TILE_PARTIAL = 2 };
 
+// Positions step by pos_stride (1 zigzag / contiguous, s striped; cdsp.h).
 __host__ __device__ __forceinline__ int64_t seg_qpos(const cdsp_segments& s, int64_t i) {
-    return i < s.q_len0 ? s.q_pos0 + i : s.q_pos1 + (i - s.q_len0);
+    return i < s.q_len0 ? s.q_pos0 + i * s.pos_stride : s.q_pos1 + (i - s.q_len0) * s.pos_stride;
 }
 
 // Min / max global position of valid query rows [r0, r1) (clipped to nq).  any=false: no rows.
@@ -27,15 +28,16 @@ __host__ __device__ __forceinline__ void seg_qrange(const cdsp_segments& s, int6
     hi = INT64_MIN;
     any = false;
     const int64_t a0 = r0, a1 = r1 < s.q_len0 ? r1 : s.q_len0;  // segment 0 part
+    const int64_t st = s.pos_stride;
     if (a0 < a1) {
         any = true;
-        lo = s.q_pos0 + a0;
-        hi = s.q_pos0 + a1 - 1;
+        lo = s.q_pos0 + a0 * st;
+        hi = s.q_pos0 + (a1 - 1) * st;
     }
     const int64_t b0 = r0 > s.q_len0 ? r0 : s.q_len0, b1 = r1;  // segment 1 part
     if (b0 < b1) {
         any = true;
-        const int64_t l1 = s.q_pos1 + (b0 - s.q_len0), h1 = s.q_pos1 + (b1 - 1 - s.q_len0);
+        const int64_t l1 = s.q_pos1 + (b0 - s.q_len0) * st, h1 = s.q_pos1 + (b1 - 1 - s.q_len0) * st;
         lo = l1 < lo ? l1 : lo;
         hi = h1 > hi ? h1 : hi;
     }
@@ -52,14 +54,14 @@ __host__ __device__ __forceinline__ int seg_tile_kind(const cdsp_segments& s, bo
     {  // segment 0 rows [max(c0,hist), min(c1,e0))
         const int64_t a = c0 > s.kv_hist ? c0 : s.kv_hist, b = c1 < e0 ? c1 : e0;
         if (a < b) {
-            kmin = s.kv_pos0 + (a - s.kv_hist);
-            kmax = s.kv_pos0 + (b - 1 - s.kv_hist);
+            kmin = s.kv_pos0 + (a - s.kv_hist) * s.pos_stride;
+            kmax = s.kv_pos0 + (b - 1 - s.kv_hist) * s.pos_stride;
         }
     }
     {  // segment 1 rows [max(c0,e0), c1)
         const int64_t a = c0 > e0 ? c0 : e0, b = c1;
         if (a < b) {
-            const int64_t x0 = s.kv_pos1 + (a - e0), x1 = s.kv_pos1 + (b - 1 - e0);
+            const int64_t x0 = s.kv_pos1 + (a - e0) * s.pos_stride, x1 = s.kv_pos1 + (b - 1 - e0) * s.pos_stride;
             kmin = x0 < kmin ? x0 : kmin;
             kmax = x1 > kmax ? x1 : kmax;
         }
@@ -75,7 +77,7 @@ __device__ __forceinline__ bool seg_visible(const cdsp_segments& s, int64_t c, i
     if (c >= s.nkv) return false;
     if (c < s.kv_hist) return true;
     const int64_t j = c - s.kv_hist;
-    const int64_t kp = j < s.kv_len0 ? s.kv_pos0 + j : s.kv_pos1 + (j - s.kv_len0);
+    const int64_t kp = j < s.kv_len0 ? s.kv_pos0 + j * s.pos_stride : s.kv_pos1 + (j - s.kv_len0) * s.pos_stride;
     return kp <= qpos;
 }
 

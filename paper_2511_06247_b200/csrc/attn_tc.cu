@@ -256,8 +256,14 @@ __device__ __forceinline__ void mask_cols(uint32_t* s, const cdsp_segments& sg, 
     const int h = clamp_bn(sg.kv_hist - c0);
     const int64_t e0abs = sg.kv_hist + sg.kv_len0;
     const int e0 = clamp_bn(e0abs - c0);
-    const int lim0 = clamp_bn(qpos - sg.kv_pos0 + sg.kv_hist + 1 - c0);
-    const int lim1 = clamp_bn(qpos - sg.kv_pos1 + e0abs + 1 - c0);
+    // rows of segment 0 / 1 with position <= qpos: floor((qpos - pos0) / st) + 1 (0 if negative)
+    int64_t n0 = qpos - sg.kv_pos0 + 1, n1 = qpos - sg.kv_pos1 + 1;
+    if (sg.pos_stride != 1) {
+        n0 = n0 > 0 ? (n0 - 1) / sg.pos_stride + 1 : 0;
+        n1 = n1 > 0 ? (n1 - 1) / sg.pos_stride + 1 : 0;
+    }
+    const int lim0 = clamp_bn(n0 + sg.kv_hist - c0);
+    const int lim1 = clamp_bn(n1 + e0abs - c0);
     const int b0 = min(h, nk);
     const int a1 = h, b1 = min(min(e0, lim0), nk);
     const int a2 = e0, b2 = min(nk, lim1);

@@ -224,6 +224,7 @@ cdsp_segments segments_for(const ChunkInfo& ci, int r, int src) {
     sgm.kv_len0 = ci.m;
     sgm.kv_pos0 = shard_pos0(ci, src);
     sgm.kv_pos1 = shard_pos1(ci, src);
+    sgm.pos_stride = shard_stride(ci);
     return sgm;
 }
 
@@ -303,6 +304,7 @@ cdsp_status phase_append(cdsp_comm c, const ChunkInfo& ci, int r, int layer, con
     a.len0 = ci.m;
     a.pos0 = shard_pos0(ci, r);
     a.pos1 = shard_pos1(ci, r);
+    a.pos_stride = shard_stride(ci);
     CDSP_CHECK_STATUS(launch_store_append(a, st));
     n += 2 * ci.m;
     return CDSP_OK;
@@ -703,8 +705,14 @@ cdsp_status cdsp_plan_partition(const cdsp_plan* plan, int32_t c, int32_t* tok_r
     ChunkInfo ci;
     CDSP_CHECK_STATUS(plan_chunk_info(plan, c, &ci));
     const int64_t m = ci.m;
+    const bool striped = ci.interleave == CDSP_STRIPED;
     if (tok_rank || tok_slot) {
         for (int64_t t = 0; t < ci.L; ++t) {
+            if (striped) {  // round-robin stripes (R20)
+                if (tok_rank) tok_rank[t] = static_cast<int32_t>(t % ci.s);
+                if (tok_slot) tok_slot[t] = static_cast<int32_t>(t / ci.s);
+                continue;
+            }
             const int64_t j = t / m;  // shard S_j
             const bool first = j < ci.s;
             if (tok_rank) tok_rank[t] = static_cast<int32_t>(first ? j : 2 * ci.s - 1 - j);
@@ -712,11 +720,12 @@ cdsp_status cdsp_plan_partition(const cdsp_plan* plan, int32_t c, int32_t* tok_r
         }
     }
     if (rank_pos) {
+        const int64_t st = shard_stride(ci);
         for (int r = 0; r < ci.s; ++r) {
             int64_t* p = rank_pos + static_cast<size_t>(r) * 2 * m;
             for (int64_t i = 0; i < m; ++i) {
-                p[i] = shard_pos0(ci, r) + i;
-                p[m + i] = shard_pos1(ci, r) + i;
+                p[i] = shard_pos0(ci, r) + i * st;
+                p[m + i] = shard_pos1(ci, r) + i * st;
             }
         }
     }
@@ -820,7 +829,7 @@ cdsp_status cdsp_prefill_chunk_layer(const cdsp_tensor* q, const cdsp_tensor* k,
         CDSP_CUDA(cudaMemcpyAsync(layer_v(c, c->self, layer), v->ptr, m2 * c->row_bytes, cudaMemcpyDeviceToDevice,
                                   c->comm_stream));
         CDSP_CHECK_STATUS(launch_fill_positions(c->self.pos, m2, ci.m, shard_pos0(ci, r), shard_pos1(ci, r),
-                                                c->comm_stream));
+                                                shard_stride(ci), c->comm_stream));
         n = m2;
         prev_kv->n = n;
         CDSP_CHECK_STATUS(run_attention_timed(c, q->ptr, k->ptr, v->ptr, c->dtype, Hq, c->Hkv, c->D,
@@ -897,6 +906,7 @@ cdsp_status cdsp_kv_transfer_to_decode(const cdsp_tensor* k, const cdsp_tensor* 
     a.len0 = ci.m;
     a.pos0 = shard_pos0(ci, r);
     a.pos1 = shard_pos1(ci, r);
+    a.pos_stride = shard_stride(ci);
     a.tp = dst->tp;
     a.block_size = dst->block_size;
     a.num_blocks = dst->num_blocks;
@@ -928,6 +938,10 @@ cdsp_status cdsp_attention_fwd(const cdsp_tensor* q, const cdsp_tensor* k, const
                                const cdsp_segments* seg, float softmax_scale, int32_t mode, float* o_acc,
                                float* lse_acc, cdsp_tensor* out, float* lse, void* cuda_stream) {
     CDSP_REQUIRE(seg != nullptr, CDSP_ERR_INVALID, "NULL segments");
+    CDSP_REQUIRE(seg->pos_stride >= 0 && seg->pos_stride <= 8, CDSP_ERR_SHAPE, "pos_stride %lld not in [0,8]",
+                 static_cast<long long>(seg->pos_stride));
+    cdsp_segments sg = *seg;
+    if (sg.pos_stride == 0) sg.pos_stride = 1;  // 0 = contiguous (ABI 1 callers)
     CDSP_CHECK_STATUS(check_tensor(q, "q"));
     CDSP_CHECK_STATUS(check_tensor(k, "k"));
     CDSP_CHECK_STATUS(check_tensor(v, "v"));
@@ -951,7 +965,7 @@ cdsp_status cdsp_attention_fwd(const cdsp_tensor* q, const cdsp_tensor* k, const
                  "accumulator buffers required for mode %d", mode);
     const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf(static_cast<float>(q->D));
     return run_attention(q->ptr, k->ptr, v->ptr, q->dtype, static_cast<int>(q->H), static_cast<int>(k->H),
-                         static_cast<int>(q->D), *seg, scale, mode, o_acc, lse_acc, final_out ? out->ptr : nullptr,
+                         static_cast<int>(q->D), sg, scale, mode, o_acc, lse_acc, final_out ? out->ptr : nullptr,
                          lse, static_cast<cudaStream_t>(cuda_stream));
 }
 
@@ -977,6 +991,31 @@ static cdsp_status zigzag_copy(const cdsp_tensor* full, int32_t s, int32_t r, cd
         segs[1] = RowCopy{shard->ptr, full->ptr, m, f1, m};
     }
     return launch_row_copy(segs, 2, row_bytes, st);
+}
+
+static cdsp_status striped_copy(const cdsp_tensor* full, int32_t s, int32_t r, cdsp_tensor* shard, bool gather,
+                                cudaStream_t st) {
+    CDSP_CHECK_STATUS(check_tensor(full, "full"));
+    CDSP_CHECK_STATUS(check_tensor(shard, "shard"));
+    CDSP_REQUIRE(s == 1 || s == 2 || s == 4 || s == 8, CDSP_ERR_PLAN, "s=%d not in {1,2,4,8}", s);
+    CDSP_REQUIRE(r >= 0 && r < s, CDSP_ERR_INVALID, "rank %d not in [0,%d)", r, s);
+    CDSP_REQUIRE(full->dtype == shard->dtype, CDSP_ERR_DTYPE, "dtype mismatch");
+    CDSP_REQUIRE(full->H == shard->H && full->D == shard->D, CDSP_ERR_SHAPE, "H/D mismatch");
+    CDSP_REQUIRE(full->T % (2 * s) == 0, CDSP_ERR_SHAPE, "L=%lld not a multiple of 2s", static_cast<long long>(full->T));
+    const int64_t n = full->T / s;
+    CDSP_REQUIRE(shard->T == n, CDSP_ERR_SHAPE, "shard must have L/s=%lld rows", static_cast<long long>(n));
+    const int64_t row_bytes = full->H * full->D * static_cast<int64_t>(dtype_size(full->dtype));
+    RowCopy seg = gather ? RowCopy{full->ptr, shard->ptr, r, 0, n, s, 1} : RowCopy{shard->ptr, full->ptr, 0, r, n, 1, s};
+    return launch_row_copy(&seg, 1, row_bytes, st);
+}
+
+cdsp_status cdsp_striped_gather(const cdsp_tensor* full, int32_t s, int32_t r, cdsp_tensor* shard, void* cuda_stream) {
+    return striped_copy(full, s, r, shard, true, static_cast<cudaStream_t>(cuda_stream));
+}
+
+cdsp_status cdsp_striped_scatter(const cdsp_tensor* shard, int32_t s, int32_t r, cdsp_tensor* full,
+                                 void* cuda_stream) {
+    return striped_copy(full, s, r, const_cast<cdsp_tensor*>(shard), false, static_cast<cudaStream_t>(cuda_stream));
 }
 
 cdsp_status cdsp_zigzag_gather(const cdsp_tensor* full, int32_t s, int32_t r, cdsp_tensor* shard, void* cuda_stream) {

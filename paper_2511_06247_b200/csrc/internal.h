@@ -38,6 +38,7 @@ struct RowCopy {
     const void* src;
     void* dst;
     int64_t src_row0, dst_row0, n_rows;
+    int64_t src_stride = 1, dst_stride = 1;  // row i: src_row0 + i src_stride -> dst_row0 + i dst_stride
 };
 cdsp_status launch_row_copy(const RowCopy* segs, int n_segs, int64_t row_bytes, cudaStream_t st);
 
@@ -49,11 +50,13 @@ struct AppendArgs {
     void* v_dst;
     int32_t* pos_dst;
     int64_t n_rows, row_bytes;
-    int64_t len0, pos0, pos1;  // row i < len0 -> pos0 + i, else pos1 + (i - len0)
+    int64_t len0, pos0, pos1;  // row i < len0 -> pos0 + i st, else pos1 + (i - len0) st
+    int64_t pos_stride = 1;    // st: 1 zigzag, s striped
 };
 cdsp_status launch_store_append(const AppendArgs& a, cudaStream_t st);
-// Store positions only: dst[i] = i < len0 ? pos0 + i : pos1 + (i - len0).
-cdsp_status launch_fill_positions(int32_t* dst, int64_t n, int64_t len0, int64_t pos0, int64_t pos1, cudaStream_t st);
+// Store positions only: dst[i] = i < len0 ? pos0 + i st : pos1 + (i - len0) st.
+cdsp_status launch_fill_positions(int32_t* dst, int64_t n, int64_t len0, int64_t pos0, int64_t pos1, int64_t pst,
+                                  cudaStream_t st);
 
 cdsp_status launch_zigzag_map(int64_t L, int s, int32_t* tok_rank, int32_t* tok_slot, cudaStream_t st);
 
@@ -64,6 +67,7 @@ struct PagedArgs {
     int64_t n_tok;
     int Hkv, D, esize;
     int64_t len0, pos0, pos1;  // row -> position, as AppendArgs
+    int64_t pos_stride;
     int tp, block_size;
     int64_t num_blocks, n_table;
     const int32_t* block_table;

@@ -109,8 +109,10 @@ __global__ void __launch_bounds__(256) row_copy_kernel(const RowCopyParams p) {
         void* dp = s ? p.seg[1].dst : p.seg[0].dst;
         const int64_t sr0 = s ? p.seg[1].src_row0 : p.seg[0].src_row0;
         const int64_t dr0 = s ? p.seg[1].dst_row0 : p.seg[0].dst_row0;
-        const uint4* src = static_cast<const uint4*>(sp) + (sr0 + r) * p.row_vec + c;
-        uint4* dst = static_cast<uint4*>(dp) + (dr0 + r) * p.row_vec + c;
+        const int64_t ss = s ? p.seg[1].src_stride : p.seg[0].src_stride;
+        const int64_t ds = s ? p.seg[1].dst_stride : p.seg[0].dst_stride;
+        const uint4* src = static_cast<const uint4*>(sp) + (sr0 + r * ss) * p.row_vec + c;
+        uint4* dst = static_cast<uint4*>(dp) + (dr0 + r * ds) * p.row_vec + c;
         *dst = __ldg(src);
     }
 }
@@ -122,13 +124,16 @@ __global__ void __launch_bounds__(256) store_append_kernel(const AppendArgs a) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
         static_cast<uint4*>(a.k_dst)[i] = __ldg(static_cast<const uint4*>(a.k_src) + i);
         static_cast<uint4*>(a.v_dst)[i] = __ldg(static_cast<const uint4*>(a.v_src) + i);
-        if (i < a.n_rows) a.pos_dst[i] = static_cast<int32_t>(i < a.len0 ? a.pos0 + i : a.pos1 + (i - a.len0));
+        if (i < a.n_rows)
+            a.pos_dst[i] = static_cast<int32_t>(i < a.len0 ? a.pos0 + i * a.pos_stride
+                                                           : a.pos1 + (i - a.len0) * a.pos_stride);
     }
 }
 
-__global__ void fill_positions_kernel(int32_t* dst, int64_t n, int64_t len0, int64_t pos0, int64_t pos1) {
+__global__ void fill_positions_kernel(int32_t* dst, int64_t n, int64_t len0, int64_t pos0, int64_t pos1,
+                                      int64_t pst) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) dst[i] = static_cast<int32_t>(i < len0 ? pos0 + i : pos1 + (i - len0));
+    if (i < n) dst[i] = static_cast<int32_t>(i < len0 ? pos0 + i * pst : pos1 + (i - len0) * pst);
 }
 
 // ------------------------------------------------------------------ K*5 zigzag map
@@ -152,7 +157,7 @@ __global__ void __launch_bounds__(256) paged_scatter_kernel(const PagedArgs a) {
     if (w >= 2 * a.n_tok) return;
     const int which = w >= a.n_tok;  // 0: K, 1: V
     const int64_t tok = which ? w - a.n_tok : w;
-    const int64_t pos = tok < a.len0 ? a.pos0 + tok : a.pos1 + (tok - a.len0);
+    const int64_t pos = tok < a.len0 ? a.pos0 + tok * a.pos_stride : a.pos1 + (tok - a.len0) * a.pos_stride;
     const int64_t lb = pos / a.block_size;
     const int32_t blk = lb < a.n_table ? __ldg(a.block_table + lb) : -1;
     if (blk < 0 || blk >= a.num_blocks) {
@@ -238,7 +243,7 @@ cdsp_status launch_row_copy(const RowCopy* segs, int n_segs, int64_t row_bytes, 
     p.n_segs = n_segs;
     p.row_vec = row_bytes / 16;
     p.seg[0] = segs[0];
-    p.seg[1] = n_segs > 1 ? segs[1] : RowCopy{nullptr, nullptr, 0, 0, 0};
+    p.seg[1] = n_segs > 1 ? segs[1] : RowCopy{nullptr, nullptr, 0, 0, 0, 1, 1};
     p.seg0_vec = segs[0].n_rows * p.row_vec;
     p.total = p.seg0_vec + (n_segs > 1 ? segs[1].n_rows * p.row_vec : 0);
     if (p.total == 0) return CDSP_OK;
@@ -256,9 +261,10 @@ cdsp_status launch_store_append(const AppendArgs& a, cudaStream_t st) {
     return CDSP_OK;
 }
 
-cdsp_status launch_fill_positions(int32_t* dst, int64_t n, int64_t len0, int64_t pos0, int64_t pos1, cudaStream_t st) {
+cdsp_status launch_fill_positions(int32_t* dst, int64_t n, int64_t len0, int64_t pos0, int64_t pos1, int64_t pst,
+                                  cudaStream_t st) {
     if (n == 0) return CDSP_OK;
-    fill_positions_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(dst, n, len0, pos0, pos1);
+    fill_positions_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(dst, n, len0, pos0, pos1, pst);
     CDSP_CUDA(cudaGetLastError());
     return CDSP_OK;
 }

@@ -33,6 +33,8 @@ cdsp_status plan_chunk_info(const cdsp_plan* plan, int c, ChunkInfo* info) {
     for (int i = 0; i < plan->n_chunks; ++i) {
         const cdsp_chunk& ch = plan->chunks[i];
         CDSP_REQUIRE(ch.ranks != nullptr, CDSP_ERR_INVALID, "chunk %d: NULL ranks", i);
+        CDSP_REQUIRE(ch.interleave == CDSP_ZIGZAG || ch.interleave == CDSP_STRIPED, CDSP_ERR_PLAN,
+                     "chunk %d: interleave %d not zigzag (0) / striped (1)", i, ch.interleave);
         CDSP_REQUIRE(pow2_sp(ch.sp), CDSP_ERR_PLAN, "chunk %d: sp=%d not in {1,2,4,8}", i, ch.sp);
         CDSP_REQUIRE(ch.len > 0 && ch.len % (2 * static_cast<int64_t>(ch.sp)) == 0, CDSP_ERR_PLAN,
                      "chunk %d: len=%lld not a positive multiple of 2*sp", i, static_cast<long long>(ch.len));
@@ -67,6 +69,7 @@ cdsp_status plan_chunk_info(const cdsp_plan* plan, int c, ChunkInfo* info) {
             info->L = ch.len;
             info->m = ch.len / (2 * s);
             info->C = C;
+            info->interleave = ch.interleave;
             for (int r = 0; r < s; ++r) {
                 info->ranks[r] = ch.ranks[r];
                 info->store_before[r] = size[r];

@@ -8,7 +8,8 @@ copy-engine pulls are the same code the multi-process path runs over NVLink.
 ``run_plan_distributed``: one process per GPU (torch.distributed for the IPC handle
 exchange only); this process executes the chunks whose group contains its rank.
 
-Input sharding (cdsp_zigzag_gather) and output reassembly (cdsp_zigzag_scatter) use the
+Input sharding (cdsp_zigzag_gather / cdsp_striped_gather, per the chunk's interleave) and
+output reassembly (cdsp_zigzag_scatter / cdsp_striped_scatter) use the
 library's kernels; the LSE reassembly for tests is harness code (index_copy).
 """
 from __future__ import annotations
@@ -73,7 +74,7 @@ def run_plan_loopback(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: a
         for r, inst in enumerate(ranks):
             with torch.cuda.stream(streams[inst]):
                 o_r, l_r = outs[c][r]
-                api.zigzag_scatter(o_r, len(ranks), r, out[C:C + L], stream=streams[inst])
+                api.shard_scatter(o_r, len(ranks), r, out[C:C + L], plan.interleave[c], stream=streams[inst])
                 if want_lse:
                     idx = _rank_lse_index(plan, c, r, device)
                     lse.index_copy_(1, idx, l_r)
@@ -85,15 +86,16 @@ def run_plan_loopback(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: a
 
 
 def prepare_shards(q, k, v, plan: api.Plan, streams=None):
-    """Per chunk, per ring rank: (q, k, v) zigzag shards (cdsp_zigzag_gather)."""
+    """Per chunk, per ring rank: (q, k, v) shards under the chunk's interleave."""
     shards = []
     for c, (L, ranks) in enumerate(plan.chunks):
         C = plan.chunk_start(c)
         s = len(ranks)
         per = []
         for r in range(s):
-            per.append((api.zigzag_gather(q[C:C + L], s, r), api.zigzag_gather(k[C:C + L], s, r),
-                        api.zigzag_gather(v[C:C + L], s, r)))
+            il = plan.interleave[c]
+            per.append((api.shard_gather(q[C:C + L], s, r, il), api.shard_gather(k[C:C + L], s, r, il),
+                        api.shard_gather(v[C:C + L], s, r, il)))
         shards.append(per)
     return shards
 
@@ -170,7 +172,7 @@ def run_plan_loopback_layers(qkv_layers, plan: api.Plan, comms: List[api.Comm], 
             for l in range(n_layers):
                 o_r, l_r = outs[l][c][r]
                 with torch.cuda.stream(streams[inst]):
-                    api.zigzag_scatter(o_r, len(ranks), r, res[l][0][C:C + L], stream=streams[inst])
+                    api.shard_scatter(o_r, len(ranks), r, res[l][0][C:C + L], plan.interleave[c], stream=streams[inst])
                     res[l][1].index_copy_(1, idx, l_r)
         C += L
     for s in streams:

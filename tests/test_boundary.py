@@ -30,7 +30,7 @@ def test_exports_every_declared_symbol(lib):
     for n in names:
         assert hasattr(lib, n), f"libcdsp.so does not export {n}"
     assert set(names) == set(api.EXPORTED_SYMBOLS)
-    assert api.abi_version() == 1
+    assert api.abi_version() == 2
 
 
 def test_no_oracle_in_product():
@@ -70,6 +70,39 @@ def test_plan_partition_matches_oracle(lib, plan):
         _, _, omoves = oracle.plan_stores(plan, c)
         assert sorted(moves) == sorted(omoves)
         C += L
+
+
+STRIPED_PLANS = [
+    [(1024, [0, 1], "striped")],
+    [(512, [0]), (512, [0, 1], "striped"), (1024, [0, 1, 2, 3])],
+    [(256, [0, 1], "striped"), (512, [0, 1, 2, 3], "striped"), (1024, list(range(8)), "striped")],
+    [(64, [3]), (64, [3, 0], "striped"), (128, [3, 0, 5, 1]), (96, [3, 0, 5, 1, 2, 4, 6, 7], "striped")],
+]
+
+
+@pytest.mark.parametrize("plan", STRIPED_PLANS)
+def test_striped_plan_partition_matches_oracle(lib, plan):
+    """Chunks interleaved by stripes (R20): maps and shard positions bit-exact vs the oracle;
+    balancing moves and store capacity unchanged by the interleave."""
+    P = api.Plan(plan)
+    C = 0
+    for c, chunk in enumerate(plan):
+        L, ranks = chunk[0], chunk[1]
+        il = chunk[2] if len(chunk) > 2 else "zigzag"
+        s = len(ranks)
+        tr, ts, rp, moves = api.plan_partition(P, c)
+        otr, ots = (oracle.striped_map if il == "striped" else oracle.zigzag_map)(L, s)
+        np.testing.assert_array_equal(tr, otr)
+        np.testing.assert_array_equal(ts, ots)
+        np.testing.assert_array_equal(rp, oracle.rank_positions(L, s, C, interleave=il))
+        _, _, omoves = oracle.plan_stores(plan, c)
+        assert sorted(moves) == sorted(omoves)
+        C += L
+    need = 0
+    for c, chunk in enumerate(plan):
+        n, _, _ = oracle.plan_stores(plan, c)
+        need = max(need, int(n.max()) + chunk[0] // len(chunk[1]))
+    assert api.plan_capacity(P) == need
 
 
 @pytest.mark.parametrize("plan", PLANS)
