@@ -274,6 +274,48 @@ CDSP_API cdsp_status cdsp_kv_transfer_to_decode(const cdsp_tensor* k, const cdsp
                                                 const cdsp_decode_target* dst, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------------
+ * CDSP prefill scheduler (§5.1).  Host-only, pure.
+ * ------------------------------------------------------------------------------- */
+
+/* Eq. (1): T_s(R) = a + b L + c (C L) + d L^2 for a chunk of L tokens with C
+ * historical tokens at SP size s (a: constant, b: FC layers, c: attention to history,
+ * d: attention within the chunk), in any time unit. */
+typedef struct {
+    double a, b, c, d;
+} cdsp_latency_model;
+
+/* Least-squares fit of Eq. (1) to n >= 4 measured (C[i], L[i], T[i]).
+ * Errors: CDSP_ERR_INVALID (NULL, too few or rank-deficient samples). */
+CDSP_API cdsp_status cdsp_fit_latency_model(int32_t n, const double* C, const double* L, const double* T,
+                                            cdsp_latency_model* out);
+
+#define CDSP_MAX_CHUNKS 8
+/* A scheduled plan: chunk c has len[c] tokens on the sp[c] instances ranks[c][0..sp) (ring
+ * order, nested: chunk c's list starts with chunk c-1's, R9) — the plan A of Alg. 1, ready
+ * for cdsp_plan (zigzag chunks); ttft = its Eq. (1) time to first token. */
+typedef struct {
+    int32_t n_chunks;
+    int64_t len[CDSP_MAX_CHUNKS];
+    int32_t sp[CDSP_MAX_CHUNKS];
+    int32_t ranks[CDSP_MAX_CHUNKS][CDSP_MAX_SP];
+    double ttft;
+} cdsp_schedule;
+
+/* Algorithm 1 (with Alg. 2 single-chunk scheduling, the GetGroup extension of P:269,
+ * Alg. 3 chunk plan solving and the queue update Eq. (2); readings R21-R27) for a new
+ * request of L tokens:
+ *   queue[n_instances]: each prefill instance's queuing latency T_i (>= 0; model time unit);
+ *     instance i lives on node i / node_size;
+ *   sizes[n_sizes] (subset of {1,2,4,8}) with models[n_sizes] their Eq. (1) coefficients;
+ *   improvement_rate in [0, 1): a larger SP size is taken only if it cuts the estimated TTFT
+ *     by more than this fraction (Alg. 2 line 13);
+ *   granule: chunk lengths are multiples of it (a multiple of 2 max(sizes), R6/R25); L must be.
+ * Errors: CDSP_ERR_INVALID, CDSP_ERR_SHAPE, CDSP_ERR_PLAN (no size fits the pool). */
+CDSP_API cdsp_status cdsp_schedule_prefill(int64_t L, int32_t n_instances, const double* queue, int32_t node_size,
+                                           int32_t n_sizes, const int32_t* sizes, const cdsp_latency_model* models,
+                                           double improvement_rate, int64_t granule, cdsp_schedule* out);
+
+/* ---------------------------------------------------------------------------------
  * Decode consumer of the transferred cache
  * ------------------------------------------------------------------------------- */
 

@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "cdsp_kv_transfer_errors", "cdsp_last_error", "cdsp_abi_version", "cdsp_comm_profile",
     "cdsp_comm_profile_read", "cdsp_decode_workspace_bytes", "cdsp_decode_attention", "cdsp_comm_profile_ring",
     "cdsp_comm_create_layers", "cdsp_kvstore_get_layer", "cdsp_prefill_chunk_layer",
-    "cdsp_striped_gather", "cdsp_striped_scatter",
+    "cdsp_striped_gather", "cdsp_striped_scatter", "cdsp_fit_latency_model", "cdsp_schedule_prefill",
 )
 
 
@@ -83,6 +83,18 @@ class Segments(ctypes.Structure):
                                               "kv_len0", "kv_pos0", "kv_pos1", "pos_stride")]
 
 
+class LatencyModel(ctypes.Structure):
+    _fields_ = [("a", ctypes.c_double), ("b", ctypes.c_double), ("c", ctypes.c_double), ("d", ctypes.c_double)]
+
+
+MAX_CHUNKS = 8
+
+
+class ScheduleC(ctypes.Structure):
+    _fields_ = [("n_chunks", ctypes.c_int32), ("len", ctypes.c_int64 * MAX_CHUNKS), ("sp", ctypes.c_int32 * MAX_CHUNKS),
+                ("ranks", (ctypes.c_int32 * 8) * MAX_CHUNKS), ("ttft", ctypes.c_double)]
+
+
 _lib = None
 
 
@@ -129,6 +141,8 @@ def lib():
             "cdsp_comm_profile": [P, i32],
             "cdsp_comm_profile_read": [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)],
             "cdsp_decode_workspace_bytes": [i32, i32, i32, ctypes.POINTER(ctypes.c_size_t)],
+            "cdsp_fit_latency_model": [i32, P, P, P, ctypes.POINTER(LatencyModel)],
+            "cdsp_schedule_prefill": [i64, i32, P, i32, i32, P, P, ctypes.c_double, i64, ctypes.POINTER(ScheduleC)],
             "cdsp_comm_profile_ring": [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(i64), ctypes.POINTER(i32)],
             "cdsp_decode_attention": [ctypes.POINTER(Tensor), ctypes.POINTER(DecodeTargetC), i32, i32, i64, f32,
@@ -203,6 +217,28 @@ class Plan:
 
     def __len__(self):
         return len(self.chunks)
+
+
+def fit_latency_model(C, L, T):
+    """cdsp_fit_latency_model: Eq. (1) coefficients (a, b, c, d) from samples."""
+    C, L, T = (np.ascontiguousarray(x, dtype=np.float64) for x in (C, L, T))
+    out = LatencyModel()
+    _check(lib().cdsp_fit_latency_model(len(T), C.ctypes.data, L.ctypes.data, T.ctypes.data, ctypes.byref(out)))
+    return (out.a, out.b, out.c, out.d)
+
+
+def schedule_prefill(L: int, queue, node_size: int, models: dict, improvement_rate: float, granule: int):
+    """cdsp_schedule_prefill: -> ([(len, ring-order ranks)], ttft).  models: {s: (a, b, c, d)}."""
+    q = np.ascontiguousarray(queue, dtype=np.float64)
+    sizes = sorted(models)
+    sz = np.array(sizes, np.int32)
+    ms = (LatencyModel * len(sizes))(*[LatencyModel(*models[s]) for s in sizes])
+    out = ScheduleC()
+    _check(lib().cdsp_schedule_prefill(int(L), len(q), q.ctypes.data, node_size, len(sizes), sz.ctypes.data,
+                                       ctypes.cast(ms, ctypes.c_void_p), float(improvement_rate), int(granule),
+                                       ctypes.byref(out)))
+    plan = [(int(out.len[c]), [int(out.ranks[c][r]) for r in range(out.sp[c])]) for c in range(out.n_chunks)]
+    return plan, float(out.ttft)
 
 
 def plan_capacity(plan: Plan) -> int:
