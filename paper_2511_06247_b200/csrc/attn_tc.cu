@@ -107,7 +107,7 @@ struct Layout {
     // each MMA group commits once: s_full[b] (S(n) done) also frees K stage n % 3, and
     // v_empty[s] (PV(n) done) also tells a rescaling softmax group that O is stable.
     static constexpr int B_Q = 0, B_KF = 1, B_VF = B_KF + KST, B_VE = B_VF + VST, B_SF = B_VE + VST,
-                         B_PF = B_SF + NSB, B_OF = B_PF + NSB, NBAR = B_OF + 1;
+                         B_PF = B_SF + NSB, B_OF = B_PF + NSB, B_ACC = B_OF + 1, NBAR = B_ACC + 1;
     static_assert(KST == NSB, "K stages are released through s_full");
     static constexpr int OFF_TMEM_SLOT = OFF_BAR + NBAR * 8;
     static constexpr int OFF_JR = OFF_TMEM_SLOT + 16;   // used-tile range per setup warp: (min, max+1)
@@ -315,7 +315,8 @@ __device__ __forceinline__ void exp32_store(const uint32_t* s, float2 sc, float2
 template <int HD>
 __global__ void __maxnreg__(168)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                   const __grid_constant__ CUtensorMap tm_v, const TcParams p) {
+                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_acc,
+                   const __grid_constant__ CUtensorMap tm_out, const TcParams p) {
     using L = Layout<HD>;
     extern __shared__ uint8_t smem_raw[];
 #ifdef CDSP_KTRACE
@@ -356,10 +357,15 @@ __global__ void __maxnreg__(168)
                 mbar_init(bar(L::B_PF + b), 4);
             }
             mbar_init(bar(L::B_OF), 1);
+            mbar_init(bar(L::B_ACC), 1);
             fence_barrier_init();
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
+            if constexpr (HD == 128) {
+                tma_prefetch_desc(&tm_acc);
+                tma_prefetch_desc(&tm_out);
+            }
             // Q does not depend on the schedule: start its load now
             mbar_expect_tx(bar(L::B_Q), L::TILE);
             for (int b = 0; b < L::NBOX; ++b)
@@ -433,6 +439,23 @@ __global__ void __maxnreg__(168)
             }
             __syncwarp();
             ++it;
+        }
+        if constexpr (HD == 128) {
+            // merge modes: once the last S = Q K^T has read the K stages, stage this tile's
+            // fp32 accumulator rows there (4 boxes of 128 rows x 32 columns, 128B-swizzled) for
+            // the epilogue — under the tail of the main loop instead of after it
+            if (is_k && (p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST)) {
+                if (it > 0) {
+                    const int nl = it - 1;  // the last used tile's S buffer / phase
+                    mbar_wait(bar(L::B_SF + nl % NSB), (nl / NSB) & 1);
+                }
+                if (elect_one()) {
+                    mbar_expect_tx(bar(L::B_ACC), BM * HD * 4);
+                    for (int b = 0; b < HD / 32; ++b)
+                        tma_load_3d(sK + b * (BM * 128), &tm_acc, bar(L::B_ACC), b * 32, head, static_cast<int>(row0));
+                }
+                __syncwarp();
+            }
         }
     } else if (warp == W_MMA) {
         // ================= MMA issuer (warp-uniform loop, one lane issues) =================
@@ -653,6 +676,74 @@ __global__ void __maxnreg__(168)
         }
         const float sbw = wb * inv_l;
         const size_t orow = (static_cast<size_t>(row_ok ? row : 0) * p.Hq + head) * HD;
+        if constexpr (HD == 128) {
+            // Staged epilogue: thread = row, but global traffic goes through 128B-swizzled smem
+            // tiles moved by TMA (a thread-per-row store touches 32 rows per warp instruction).
+            // fp32 results (FIRST/MID) are written in place over the accumulator tile in the K
+            // stages; bf16 results (ONLY/LAST) into the V stages.  Group g owns columns
+            // [64 g, 64 g + 64): fp32 boxes 2g, 2g+1 (32 columns each), bf16 box g.
+            if (merge) mbar_wait(bar(L::B_ACC), 0);  // accumulator tile landed (K warp's TMA)
+            const uint32_t rsw = static_cast<uint32_t>(r & 7);
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                uint32_t o[32];
+                if (n_used > 0) {
+                    tmem_ld32p(tO + 32 * (2 * g + cc), o);
+                    tc_wait_ld();
+                    reg_tie32(o);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = 0u;
+                }
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]) * sbw;
+                const uint32_t fbox = sK + static_cast<uint32_t>(2 * g + cc) * (BM * 128) + static_cast<uint32_t>(r) * 128;
+                if (merge) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float4 av;
+                        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                     : "=f"(av.x), "=f"(av.y), "=f"(av.z), "=f"(av.w)
+                                     : "r"(fbox + ((j ^ rsw) << 4)));
+                        v[4 * j + 0] = fmaf(wa, av.x, v[4 * j + 0]);
+                        v[4 * j + 1] = fmaf(wa, av.y, v[4 * j + 1]);
+                        v[4 * j + 2] = fmaf(wa, av.z, v[4 * j + 2]);
+                        v[4 * j + 3] = fmaf(wa, av.w, v[4 * j + 3]);
+                    }
+                }
+                if (to_acc) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(fbox + ((j ^ rsw) << 4)),
+                                     "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                                     : "memory");
+                } else {
+                    const uint32_t hbox = sV + static_cast<uint32_t>(g) * (BM * 128) + static_cast<uint32_t>(r) * 128;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t ch = static_cast<uint32_t>(4 * cc + j);
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(hbox + ((ch ^ rsw) << 4)),
+                                     "r"(pack_bf16(v[8 * j + 0], v[8 * j + 1])), "r"(pack_bf16(v[8 * j + 2], v[8 * j + 3])),
+                                     "r"(pack_bf16(v[8 * j + 4], v[8 * j + 5])), "r"(pack_bf16(v[8 * j + 6], v[8 * j + 7]))
+                                     : "memory");
+                    }
+                }
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(4 + g, BM);  // this group's 128 rows are in smem
+            if (threadIdx.x == static_cast<unsigned>(g * BM)) {
+                if (to_acc) {
+                    for (int cc = 0; cc < 2; ++cc)
+                        tma_store_3d(&tm_acc, sK + static_cast<uint32_t>(2 * g + cc) * (BM * 128), 32 * (2 * g + cc), head,
+                                     static_cast<int>(row0));
+                } else {
+                    tma_store_3d(&tm_out, sV + static_cast<uint32_t>(g) * (BM * 128), 64 * g, head, static_cast<int>(row0));
+                }
+                bulk_commit();
+                bulk_wait_read0();  // smem stays valid until the store has read it
+            }
+        } else {
         // group g writes O columns [g*HD/2, (g+1)*HD/2)
 #pragma unroll 1
         for (int c = g * (HD / 64); c < (g + 1) * (HD / 64); ++c) {
@@ -693,6 +784,7 @@ __global__ void __maxnreg__(168)
                 }
             }
         }
+        }  // HD != 128
         if (row_ok && g == 0) {
             const size_t li = static_cast<size_t>(head) * nq + row;
             if (to_acc) {
@@ -743,6 +835,24 @@ EncodeTiledFn get_encode_fn() {
 }
 
 // [T, H, D] bf16 tensor, box = 128 rows x 1 head x 64 d, 128-byte swizzle.
+// fp32 [T, H, D], box = 128 rows x 1 head x 32 columns (128 B), 128-byte swizzle (epilogue staging).
+cdsp_status make_map_f32(CUtensorMap* m, const void* base, int64_t T, int H, int D) {
+    EncodeTiledFn enc = get_encode_fn();
+    CDSP_REQUIRE(enc != nullptr, CDSP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CDSP_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15u) == 0, CDSP_ERR_INVALID,
+                 "TMA base pointer must be 16-byte aligned");
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(H),
+                          static_cast<cuuint64_t>(T > 0 ? T : 1)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 4, static_cast<cuuint64_t>(H) * D * 4};
+    cuuint32_t box[3] = {32, 1, 128};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CDSP_REQUIRE(r == CUDA_SUCCESS, CDSP_ERR_CUDA, "cuTensorMapEncodeTiled(f32) failed (%d)", static_cast<int>(r));
+    return CDSP_OK;
+}
+
 cdsp_status make_map(CUtensorMap* m, const void* base, int64_t T, int H, int D) {
     EncodeTiledFn enc = get_encode_fn();
     CDSP_REQUIRE(enc != nullptr, CDSP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -776,6 +886,14 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     const void* vb = a.seg.nkv > 0 ? a.v : a.q;
     CDSP_CHECK_STATUS(make_map(&mk, kb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD));
     CDSP_CHECK_STATUS(make_map(&mv, vb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD));
+    // epilogue maps (HD = 128): fp32 accumulators (FIRST/MID/LAST) and the bf16 output
+    // (ONLY/LAST); a mode that does not use one gets a never-dereferenced stand-in
+    CUtensorMap macc = mq, mout = mq;
+    if (HD == 128 && a.seg.nq > 0) {
+        if (a.mode != CDSP_ATTN_ONLY) CDSP_CHECK_STATUS(make_map_f32(&macc, a.o_acc, a.seg.nq, a.Hq, HD));
+        if (a.mode == CDSP_ATTN_ONLY || a.mode == CDSP_ATTN_LAST)
+            CDSP_CHECK_STATUS(make_map(&mout, a.out, a.seg.nq, a.Hq, HD));
+    }
     TcParams p;
     p.seg = a.seg;
     p.Hq = a.Hq;
@@ -791,7 +909,7 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     const int64_t grid = static_cast<int64_t>(p.n_rb) * a.Hq;
     if (grid == 0) return CDSP_OK;
     CDSP_REQUIRE(grid < (1ll << 31), CDSP_ERR_SHAPE, "grid too large");
-    attn_tc_kernel<HD><<<static_cast<unsigned>(grid), kThreads, Lt::SMEM, st>>>(mq, mk, mv, p);
+    attn_tc_kernel<HD><<<static_cast<unsigned>(grid), kThreads, Lt::SMEM, st>>>(mq, mk, mv, macc, mout, p);
     CDSP_CUDA(cudaGetLastError());
 #ifdef CDSP_KTRACE
     if (const char* path = getenv("CDSP_TRACE")) {  // debug builds only: synchronous dump

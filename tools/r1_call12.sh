@@ -1,0 +1,3 @@
+CDSP_KTRACE=1 python paper_2511_06247_b200/build.py --force > /dev/null 2>&1; echo build=$?
+timeout 300 python tools/trace_ring_step.py gpurun_out 2>&1 | tail -30
+python paper_2511_06247_b200/build.py --force > /dev/null 2>&1
