@@ -44,6 +44,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd.insert(1, "-Xptxas=-v")
         if os.environ.get("CDSP_KTRACE"):
             cmd.insert(1, "-DCDSP_KTRACE")
+        for flag in os.environ.get("CDSP_NVCC_EXTRA", "").split():  # dev experiments (-D...)
+            cmd.insert(1, flag)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     failed = []

@@ -88,7 +88,6 @@ constexpr int NSB = 3;                  // S/P buffers in TMEM
 constexpr int kBox = 128 * 128;         // TMA box: 128 rows x 64 bf16 (128-byte swizzle rows)
 constexpr int kSchedMax = 8192;         // KV tiles per launch (1M keys)
 constexpr int W_K = 8, W_V = 9, W_MMA = 10;
-constexpr int kSchedWarps = 8;          // warps 0-7 classify the KV tiles at setup
 
 template <int HD>
 struct Layout {
@@ -98,21 +97,23 @@ struct Layout {
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = OFF_Q + TILE;
     static constexpr int OFF_V = OFF_K + KST * TILE;
-    static constexpr int OFF_M = OFF_V + VST * TILE;       // running row max m(n): [2 parity][128] float
-    static constexpr int OFF_L = OFF_M + 2 * BM * 4;       // epilogue: per-group (m_used, l) [2][128] float2
-    static constexpr int OFF_QP = OFF_L + 2 * BM * 8;      // query position per row: [128] int64
-    static constexpr int OFF_BAR = OFF_QP + BM * 8;
-    // q_full, k_full[KST], v_full[VST], v_empty[VST], s_full[NSB], p_full[NSB], o_full.
-    // (m(n) goes from one softmax group to the other through named barriers 2, 3.)  Every tcgen05.commit costs the tensor pipe ~30 clk (tools/mma_pattern.cu), so
-    // each MMA group commits once: s_full[b] (S(n) done) also frees K stage n % 3, and
-    // v_empty[s] (PV(n) done) also tells a rescaling softmax group that O is stable.
-    static constexpr int B_Q = 0, B_KF = 1, B_VF = B_KF + KST, B_VE = B_VF + VST, B_SF = B_VE + VST,
-                         B_PF = B_SF + NSB, B_OF = B_PF + NSB, B_ACC = B_OF + 1, NBAR = B_ACC + 1;
+    static constexpr int OFF_M = OFF_V + VST * TILE;       // running row max m(n): [2 tile parity][128] float
+    static constexpr int OFF_L = OFF_M + 2 * BM * 4;       // epilogue (m_used, l): [2 unit parity][2 groups][128] float2
+    static constexpr int OFF_QP = OFF_L + 4 * BM * 8;      // query position per row: [2 unit buffer][128] int64
+    static constexpr int OFF_BAR = OFF_QP + 2 * BM * 8;
+    // u_full[2] (unit buffer published: schedule + Q tile), k_full[KST], v_full[VST], v_empty[VST],
+    // s_full[NSB], p_full[NSB], o_full, o_free, u_empty[2] (unit buffer read by every consumer).
+    // (m(n) goes from one softmax group to the other through named barriers 2, 3.)  Every
+    // tcgen05.commit costs the tensor pipe ~30 clk (tools/mma_pattern.cu), so each MMA group
+    // commits once: s_full[b] (S(n) done) also frees K stage n % 3 (and, for a unit's last
+    // tile, the Q buffer); v_empty[s] (PV(n) done) also tells a rescaling group that O is stable.
+    static constexpr int B_UF = 0, B_KF = 2, B_VF = B_KF + KST, B_VE = B_VF + VST, B_SF = B_VE + VST,
+                         B_PF = B_SF + NSB, B_OF = B_PF + NSB, B_OE = B_OF + 1, B_UE = B_OE + 1, NBAR = B_UE + 2;
     static_assert(KST == NSB, "K stages are released through s_full");
     static constexpr int OFF_TMEM_SLOT = OFF_BAR + NBAR * 8;
-    static constexpr int OFF_JR = OFF_TMEM_SLOT + 16;   // used-tile range per setup warp: (min, max+1)
-    static constexpr int OFF_SCHED = OFF_JR + 12 * kSchedWarps;
-    static constexpr int SMEM = OFF_SCHED + kSchedMax + 1024;  // + alignment slack
+    static constexpr int OFF_UNIT = OFF_TMEM_SLOT + 16;     // [2] x {unit, j_lo, j_hi, n_used}
+    static constexpr int OFF_SCHED = OFF_UNIT + 2 * 16;     // [2][kSchedMax] tile kinds
+    static constexpr int SMEM = OFF_SCHED + 2 * kSchedMax + 1024;  // + alignment slack
 };
 
 constexpr uint32_t COL_O = 0;
@@ -120,40 +121,41 @@ __host__ __device__ constexpr uint32_t col_s(int b) { return 128u + 128u * b; }
 
 struct TcParams {
     cdsp_segments seg;
-    int Hq, Hkv, g, n_rb;
+    int Hq, Hkv, g, n_rb, n_units;
     float scale_log2;
     int mode;
     float* o_acc;
     float* lse_acc;
     __nv_bfloat16* out;
     float* lse;
+    int* claim;  // [2]: dynamic unit counter, finished-CTA counter (both zero at launch; the last CTA re-zeroes them)
 };
 
-// Debug timeline (build with -DCDSP_KTRACE): per-CTA phase stamps (globaltimer) and SM id,
+// Debug timeline (build with -DCDSP_KTRACE): per-unit phase stamps (globaltimer) and SM id,
 // dumped by the host when CDSP_TRACE=<file> is set.
 #ifdef CDSP_KTRACE
-__device__ unsigned long long g_cta[65536 * 8];  // start, end, smid, used tiles, setup, 1st S, loop end, epi end
+__device__ unsigned long long g_cta[65536 * 8];  // per unit: published, epi end, smid, used tiles, published, 1st S, loop end, epi end
 __device__ __forceinline__ unsigned long long gtime_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-__device__ unsigned long long g_it[4 * 512 * 16];  // CTAs 0..3, first 512 iterations, 16 slots
+__device__ unsigned long long g_it[4 * 512 * 16];  // CTAs 0..3, first 512 tiles, 16 slots
 #define KTRACE(slot, iter)                                                                             \
     do {                                                                                               \
         if (blockIdx.x < 4 && (iter) < 512)                                                            \
             g_it[(static_cast<size_t>(blockIdx.x) * 512 + (iter)) * 16 + (slot)] = clock64();          \
     } while (0)
-#define CTA_STAMP(slot)                                                                           \
-    do {                                                                                          \
-        if (blockIdx.x < 65536) g_cta[static_cast<size_t>(blockIdx.x) * 8 + (slot)] = gtime_ns(); \
+#define UNIT_STAMP(unit, slot, val)                                                              \
+    do {                                                                                         \
+        if ((unit) < 65536) g_cta[static_cast<size_t>(unit) * 8 + (slot)] = (val);               \
     } while (0)
 #else
 #define KTRACE(slot, iter) \
     do {                   \
     } while (0)
-#define CTA_STAMP(slot) \
-    do {                \
+#define UNIT_STAMP(unit, slot, val) \
+    do {                            \
     } while (0)
 #endif
 
@@ -302,26 +304,38 @@ __device__ __forceinline__ void exp32_store(const uint32_t* s, float2 sc, float2
             if ((CDSP_EMU_MASK >> (i % 8)) & 1) {
                 pp = ex2_fma2(x);
             } else {
+#if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 3
+                pp = x;
+#else
                 pp.x = ex2(x.x);
                 pp.y = ex2(x.y);
+#endif
             }
             lacc = fadd2(lacc, pp);
             pk[ii] = pack_bf16(pp.x, pp.y);
         }
+#if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 2
+        lacc.x += __uint_as_float(pk[0] ^ pk[1] ^ pk[2] ^ pk[3] ^ pk[4] ^ pk[5] ^ pk[6] ^ pk[7]);
+#else
         tmem_st8(tP + 8 * h, pk);
+#endif
     }
 }
+
+// Work unit x in [0, n_units): head-major (the ~148 units in flight share one head's K/V,
+// which stays L2-resident), heavy row blocks first within a head (causal work grows with
+// the row).  Units are handed out dynamically (first one = blockIdx.x, then an atomic
+// counter), like the hardware's own CTA scheduler but without a CTA's fixed costs per unit.
+struct UnitInfo {
+    int x, j_lo, j_hi, n_used;  // x < 0: no more units
+};
 
 template <int HD>
 __global__ void __maxnreg__(168)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_acc,
-                   const __grid_constant__ CUtensorMap tm_out, const TcParams p) {
+                   const __grid_constant__ CUtensorMap tm_v, const TcParams p) {
     using L = Layout<HD>;
     extern __shared__ uint8_t smem_raw[];
-#ifdef CDSP_KTRACE
-    const unsigned long long t_start = gtime_ns();
-#endif
     // 1024-byte alignment for the 128B-swizzle atoms
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
@@ -330,23 +344,20 @@ __global__ void __maxnreg__(168)
     const uint32_t bar0 = sbase + L::OFF_BAR;
     auto bar = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM_SLOT);
-    uint8_t* sched = smem + L::OFF_SCHED;
+    UnitInfo* uinfo = reinterpret_cast<UnitInfo*>(smem + L::OFF_UNIT);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const cdsp_segments& sg = p.seg;
-
-    // ---- work unit: head-major (the ~148 CTAs in flight share one head's K/V, which stays
-    // L2-resident), heavy row blocks first within a head (causal work grows with the row)
-    const int head = static_cast<int>(blockIdx.x) / p.n_rb;
-    const int rb = p.n_rb - 1 - static_cast<int>(blockIdx.x) % p.n_rb;
-    const int kvh = head / p.g;
-    const int64_t row0 = static_cast<int64_t>(rb) * BM;
     const int n_kv_tiles = static_cast<int>((sg.nkv + BN - 1) / BN);
+    const int G = static_cast<int>(gridDim.x);
 
-    // ---- setup
+    // ---- setup (once per CTA)
     if (warp == W_K) {
         if (lane == 0) {
-            mbar_init(bar(L::B_Q), 1);
+            for (int i = 0; i < 2; ++i) {
+                mbar_init(bar(L::B_UF + i), 1);
+                mbar_init(bar(L::B_UE + i), 10);  // 8 softmax warps, V producer, MMA warp
+            }
             for (int i = 0; i < L::KST; ++i) mbar_init(bar(L::B_KF + i), 1);
             for (int i = 0; i < L::VST; ++i) {
                 mbar_init(bar(L::B_VF + i), 1);
@@ -357,105 +368,141 @@ __global__ void __maxnreg__(168)
                 mbar_init(bar(L::B_PF + b), 4);
             }
             mbar_init(bar(L::B_OF), 1);
-            mbar_init(bar(L::B_ACC), 1);
+            mbar_init(bar(L::B_OE), 8);
             fence_barrier_init();
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
-            if constexpr (HD == 128) {
-                tma_prefetch_desc(&tm_acc);
-                tma_prefetch_desc(&tm_out);
-            }
-            // Q does not depend on the schedule: start its load now
-            mbar_expect_tx(bar(L::B_Q), L::TILE);
-            for (int b = 0; b < L::NBOX; ++b)
-                tma_load_3d(sQ + b * kBox, &tm_q, bar(L::B_Q), b * 64, head, static_cast<int>(row0));
         }
     } else if (warp == W_MMA) {
         tmem_alloc(smem_u32(tmem_slot), 512);
         tmem_relinquish();
-    } else if (warp < kSchedWarps) {
-        // KV-tile schedule: sched[j] = tile kind (0 = skip)
-        int64_t qlo, qhi;
-        bool qany;
-        seg_qrange(sg, row0, row0 + BM, qlo, qhi, qany);
-        int jmin = INT_MAX, jmax = 0, cnt = 0;
-        for (int j = warp * 32 + lane; j < n_kv_tiles; j += kSchedWarps * 32) {
-            const int k = seg_tile_kind(sg, qany, qlo, qhi, static_cast<int64_t>(j) * BN, BN);
-            sched[j] = static_cast<uint8_t>(k);
-            if (k != 0) {
-                jmin = min(jmin, j);
-                jmax = max(jmax, j + 1);
-                ++cnt;
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            jmin = min(jmin, __shfl_xor_sync(0xFFFFFFFFu, jmin, o));
-            jmax = max(jmax, __shfl_xor_sync(0xFFFFFFFFu, jmax, o));
-            cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
-        }
-        if (lane == 0) {
-            reinterpret_cast<int*>(smem + L::OFF_JR)[3 * warp] = jmin;
-            reinterpret_cast<int*>(smem + L::OFF_JR)[3 * warp + 1] = jmax;
-            reinterpret_cast<int*>(smem + L::OFF_JR)[3 * warp + 2] = cnt;
-        }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    // the n_used used KV tiles lie in [j_lo, j_hi) (sched[j] == 0 marks skipped tiles inside)
-    int j_lo = INT_MAX, j_hi = 0, n_used = 0;
-    {
-        const int* jr = reinterpret_cast<const int*>(smem + L::OFF_JR);
-#pragma unroll
-        for (int w = 0; w < kSchedWarps; ++w) {
-            j_lo = min(j_lo, jr[3 * w]);
-            j_hi = max(j_hi, jr[3 * w + 1]);
-            n_used += jr[3 * w + 2];
-        }
-    }
-    if (threadIdx.x == 0) CTA_STAMP(4);
 
-    if (warp == W_K || warp == W_V) {
-        // ======== TMA producers: K and V in independent rings (a K load never waits behind a
-        // V stage); one lane issues, the warp runs the loop ========
-        const bool is_k = warp == W_K;
-        const int nst = is_k ? L::KST : L::VST;
-        const uint32_t s0 = is_k ? sK : sV;
-        const int bfull = is_k ? L::B_KF : L::B_VF, bempty = is_k ? L::B_SF : L::B_VE;
-        const void* map = is_k ? static_cast<const void*>(&tm_k) : static_cast<const void*>(&tm_v);
+    if (warp == W_K) {
+        // ======== unit scheduler + TMA producer of Q and K: for each unit, classify its KV
+        // tiles (sched[j], 0 = skip), publish the unit (u_full[i&1]; the Q tile rides on the
+        // same barrier) and stream its K tiles into 3 stages ========
         const uint64_t pol_kv = policy_evict_last();
-        int it = 0;
-        for (int j = j_lo; j < j_hi; ++j) {
-            if (sched[j] == 0) continue;
-            const int st = it % nst;
-            // stage st last held tile it - nst: free once S(it - nst) (K) / PV(it - nst) (V) is done
-            if (it >= nst) mbar_wait(bar(bempty + st), ((it - nst) / nst) & 1);
-            if (elect_one()) {
-                mbar_expect_tx(bar(bfull + st), L::TILE);
-                for (int b = 0; b < L::NBOX; ++b)
-                    tma_load_3d_hint(s0 + st * L::TILE + b * kBox, map, bar(bfull + st), b * 64, kvh, j * BN, pol_kv);
+        int x = static_cast<int>(blockIdx.x);
+        int x_pre = 0;  // lane 0: the unit after x, claimed one unit ahead
+        if (lane == 0) x_pre = G + atomicAdd(p.claim, 1);
+        int it = 0;        // used tiles loaded so far (all units)
+        int last_gn = -1;  // the previous non-empty unit's last tile: its S frees the Q buffer
+        for (int i = 0;; ++i) {
+            const int ub = i & 1;
+            if (i >= 2) mbar_wait(bar(L::B_UE + ub), ((i - 2) >> 1) & 1);  // every consumer is done with unit i-2
+            if (x >= p.n_units) {
+                if (lane == 0) {
+                    uinfo[ub].x = -1;
+                    mbar_arrive(bar(L::B_UF + ub));
+                }
+                break;
+            }
+            const int head = x / p.n_rb;
+            const int kvh = head / p.g;
+            const int64_t row0 = static_cast<int64_t>(p.n_rb - 1 - x % p.n_rb) * BM;
+            uint8_t* sched = smem + L::OFF_SCHED + ub * kSchedMax;
+            int64_t qlo, qhi;
+            bool qany;
+            seg_qrange(sg, row0, row0 + BM, qlo, qhi, qany);
+            int jmin = INT_MAX, jmax = 0, cnt = 0;
+            for (int j = lane; j < n_kv_tiles; j += 32) {
+                const int k = seg_tile_kind(sg, qany, qlo, qhi, static_cast<int64_t>(j) * BN, BN);
+                sched[j] = static_cast<uint8_t>(k);
+                if (k != 0) {
+                    jmin = min(jmin, j);
+                    jmax = max(jmax, j + 1);
+                    ++cnt;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                jmin = min(jmin, __shfl_xor_sync(0xFFFFFFFFu, jmin, o));
+                jmax = max(jmax, __shfl_xor_sync(0xFFFFFFFFu, jmax, o));
+                cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+            }
+            // query positions (only read on partial tiles)
+            int64_t* qp = reinterpret_cast<int64_t*>(smem + L::OFF_QP) + ub * BM;
+            for (int rr = lane; rr < BM; rr += 32) {
+                const int64_t row = row0 + rr;
+                qp[rr] = row < sg.nq ? seg_qpos(sg, row) : (INT64_MAX >> 2);
+            }
+            if (lane == 0) uinfo[ub] = UnitInfo{x, jmin, jmax, cnt};
+            __threadfence_block();
+            __syncwarp();
+            if (cnt > 0) {
+                if (last_gn >= 0) mbar_wait(bar(L::B_SF + last_gn % NSB), (last_gn / NSB) & 1);  // Q buffer free
+                if (lane == 0) {
+                    UNIT_STAMP(x, 0, gtime_ns());
+                    UNIT_STAMP(x, 4, gtime_ns());
+                    mbar_expect_tx(bar(L::B_UF + ub), L::TILE);  // publishes the unit (release) + Q bytes
+                    for (int b = 0; b < L::NBOX; ++b)
+                        tma_load_3d(sQ + b * kBox, &tm_q, bar(L::B_UF + ub), b * 64, head, static_cast<int>(row0));
+                }
+                // merge modes: pull this unit's accumulator rows into L2 for the epilogue
+                if (p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST) {
+                    for (int rr = lane; rr < BM; rr += 32) {
+                        const int64_t row = row0 + rr;
+                        if (row < sg.nq) {
+                            const float* src = p.o_acc + (static_cast<size_t>(row) * p.Hq + head) * HD;
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(HD * 4) : "memory");
+                        }
+                    }
+                }
+            } else if (lane == 0) {
+                mbar_arrive(bar(L::B_UF + ub));
             }
             __syncwarp();
-            ++it;
-        }
-        if constexpr (HD == 128) {
-            // merge modes: once the last S = Q K^T has read the K stages, stage this tile's
-            // fp32 accumulator rows there (4 boxes of 128 rows x 32 columns, 128B-swizzled) for
-            // the epilogue — under the tail of the main loop instead of after it
-            if (is_k && (p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST)) {
-                if (it > 0) {
-                    const int nl = it - 1;  // the last used tile's S buffer / phase
-                    mbar_wait(bar(L::B_SF + nl % NSB), (nl / NSB) & 1);
-                }
+            for (int j = jmin; j < jmax; ++j) {
+                if (sched[j] == 0) continue;
+                const int st = it % L::KST;
+                // stage st last held tile it - 3: free once S(it - 3) is done
+                if (it >= L::KST) mbar_wait(bar(L::B_SF + st), ((it - L::KST) / L::KST) & 1);
+                if (lane == 0) KTRACE(15, it);
                 if (elect_one()) {
-                    mbar_expect_tx(bar(L::B_ACC), BM * HD * 4);
-                    for (int b = 0; b < HD / 32; ++b)
-                        tma_load_3d(sK + b * (BM * 128), &tm_acc, bar(L::B_ACC), b * 32, head, static_cast<int>(row0));
+                    mbar_expect_tx(bar(L::B_KF + st), L::TILE);
+                    for (int b = 0; b < L::NBOX; ++b)
+                        tma_load_3d_hint(sK + st * L::TILE + b * kBox, &tm_k, bar(L::B_KF + st), b * 64, kvh, j * BN,
+                                         pol_kv);
                 }
                 __syncwarp();
+                ++it;
             }
+            if (cnt > 0) last_gn = it - 1;
+            x = __shfl_sync(0xFFFFFFFFu, x_pre, 0);
+            if (lane == 0 && x < p.n_units) x_pre = G + atomicAdd(p.claim, 1);
+        }
+    } else if (warp == W_V) {
+        // ======== TMA producer of V (2 stages), following the published units ========
+        const uint64_t pol_kv = policy_evict_last();
+        int it = 0;
+        for (int i = 0;; ++i) {
+            const int ub = i & 1;
+            mbar_wait(bar(L::B_UF + ub), (i >> 1) & 1);
+            const UnitInfo u = uinfo[ub];
+            if (u.x < 0) break;
+            const int kvh = (u.x / p.n_rb) / p.g;
+            const uint8_t* sched = smem + L::OFF_SCHED + ub * kSchedMax;
+            for (int j = u.j_lo; j < u.j_hi; ++j) {
+                if (sched[j] == 0) continue;
+                const int st = it % L::VST;
+                if (it >= L::VST) mbar_wait(bar(L::B_VE + st), ((it - L::VST) / L::VST) & 1);
+                if (lane == 0) KTRACE(14, it);
+                if (elect_one()) {
+                    mbar_expect_tx(bar(L::B_VF + st), L::TILE);
+                    for (int b = 0; b < L::NBOX; ++b)
+                        tma_load_3d_hint(sV + st * L::TILE + b * kBox, &tm_v, bar(L::B_VF + st), b * 64, kvh, j * BN,
+                                         pol_kv);
+                }
+                __syncwarp();
+                ++it;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(L::B_UE + ub));
         }
     } else if (warp == W_MMA) {
         // ================= MMA issuer (warp-uniform loop, one lane issues) =================
@@ -482,331 +529,298 @@ __global__ void __maxnreg__(168)
                 mma_ts(tmem + COL_O, tmem + col_s(b) + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4),
                        idesc_pv, (acc || kk > 0) ? 1u : 0u);
         };
-        auto issue_s = [&](int n) {  // S(n) into buffer n % NSB; K stage n % KST
-            const int ks = n % L::KST;
-            MMA_WAIT(bar(L::B_KF + ks), (n / L::KST) & 1);
+        auto issue_s = [&](int gn) {  // S(gn) into buffer gn % NSB; K stage gn % KST
+            const int ks = gn % L::KST;
+            MMA_WAIT(bar(L::B_KF + ks), (gn / L::KST) & 1);
             tc_fence_after();
             if (elect_one()) {
-                KTRACE(9, n);
-                issue_qk(ks, n % NSB);
-                mma_commit(bar(L::B_SF + n % NSB));  // S(n) ready; K stage ks free
+                KTRACE(9, gn);
+                issue_qk(ks, gn % NSB);
+                mma_commit(bar(L::B_SF + gn % NSB));  // S(gn) ready; K stage ks free
             }
             __syncwarp();
         };
-        if (n_used > 0) {
-            MMA_WAIT(bar(L::B_Q), 0);
-            for (int n = 0; n < NSB && n < n_used; ++n) issue_s(n);
-        }
-        for (int n = 0; n < n_used; ++n) {
-            const int b = n % NSB, vs = n % L::VST;
-            MMA_WAIT(bar(L::B_VF + vs), (n / L::VST) & 1);
-            MMA_WAIT(bar(L::B_PF + b), (n / NSB) & 1);
+        int gn0 = 0, n_units_done = 0;
+        for (int i = 0;; ++i) {
+            const int ub = i & 1;
+            MMA_WAIT(bar(L::B_UF + ub), (i >> 1) & 1);  // unit published, Q landed
+            const UnitInfo u = uinfo[ub];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(L::B_UE + ub));
+            if (u.x < 0) break;
+            const int N = u.n_used;
+            if (N == 0) continue;
             tc_fence_after();
-            if (elect_one()) {
-                KTRACE(8, n);
-                issue_pv(vs, b, n > 0);
-                mma_commit(bar(L::B_VE + vs));  // V stage free; O includes PV(n)
-                if (n == n_used - 1) mma_commit(bar(L::B_OF));
+            // this unit's first S tiles go in only after the previous unit's last PV: its
+            // buffers are the ones those PVs read
+            for (int n = 0; n < NSB && n < N; ++n) issue_s(gn0 + n);
+            for (int n = 0; n < N; ++n) {
+                const int gn = gn0 + n;
+                const int b = gn % NSB, vs = gn % L::VST;
+                if (lane == 0) KTRACE(10, gn);
+                MMA_WAIT(bar(L::B_VF + vs), (gn / L::VST) & 1);
+                if (lane == 0) KTRACE(11, gn);
+                MMA_WAIT(bar(L::B_PF + b), (gn / NSB) & 1);
+                if (n == 0 && n_units_done > 0) MMA_WAIT(bar(L::B_OE), (n_units_done - 1) & 1);  // O drained
+                tc_fence_after();
+                if (elect_one()) {
+                    KTRACE(8, gn);
+                    issue_pv(vs, b, n > 0);
+                    mma_commit(bar(L::B_VE + vs));  // V stage free; O includes PV(gn)
+                    if (n == N - 1) mma_commit(bar(L::B_OF));
+                }
+                __syncwarp();
+                if (n + NSB < N) issue_s(gn + NSB);  // into the buffer P(gn) just left
             }
-            __syncwarp();
-            if (n + NSB < n_used) issue_s(n + NSB);  // into the buffer P(n) just left
-        }
-        if (n_used == 0) {
-            if (elect_one()) mma_commit(bar(L::B_OF));
-            __syncwarp();
+            gn0 += N;
+            ++n_units_done;
         }
     } else if (warp < 8) {
-        // ========= softmax group g (tiles n = g, g+2, ...): thread = one query row =========
+        // ========= softmax group g (tiles gn = g, g+2, ... over all units): thread = one query row =========
         const int g = warp >> 2;
         const int quad = warp & 3;  // TMEM lane quadrant
         const int r = quad * 32 + lane;
-        const int64_t row = row0 + r;
-        const bool row_ok = row < sg.nq;
-        // the row's query position is only needed on partial tiles: keep it out of registers
-        int64_t* qpos_sh = reinterpret_cast<int64_t*>(smem + L::OFF_QP);
-        if (g == 0) qpos_sh[r] = row_ok ? seg_qpos(sg, row) : (INT64_MAX >> 2);
-        asm volatile("bar.sync 1, 256;" ::: "memory");
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
         const uint32_t tO = tmem + lane_off + COL_O;
         float* msh = reinterpret_cast<float*>(smem + L::OFF_M);  // [2][BM]
         const float sl2 = p.scale_log2;
-        float m = -INFINITY;       // m(n) of the last tile this thread has seen
-        float m_used = -INFINITY;  // max that this group's l is relative to
-        float2 lacc = make_float2(0.f, 0.f);
-        // group g takes used tiles n = g, g+2, ...; jc = KV tile index of tile n
-        auto next_used = [&](int jj) {
-            ++jj;
-            while (jj < j_hi && sched[jj] == 0) ++jj;
-            return jj;
-        };
-        int jc = j_lo;
-        if (g == 1 && n_used > 1) jc = next_used(jc);
-        for (int n = g; n < n_used; n += 2, jc = next_used(next_used(jc))) {
-            const int j = jc;
-            const int kind = sched[j];
-            const int b = n % NSB;
-            const uint32_t tS = tmem + lane_off + col_s(b);
-            if (lane == 0 && quad == 0) KTRACE(12 + g, n);
-            mbar_wait(bar(L::B_SF + b), (n / NSB) & 1);
-            if (lane == 0 && quad == 0) KTRACE(4 * g + 0, n);
-            tc_fence_after();
-#if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 0
-            // debug: MMA pipeline alone (no TMEM traffic from the softmax; results garbage)
-            if (n > 0) named_bar_sync(2 + ((n - 1) & 1), 2 * BM);
-            named_bar_arrive(2 + (n & 1), 2 * BM);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar(L::B_PF + b));
-            continue;
-#endif
-            // 64 score registers: columns 64-127 first (max only), then 0-63 (max, kept for the
-            // exponentials); 64-127 are re-read from TMEM for their exponentials (P(n) only ever
-            // overwrites S columns 0-63)
-            uint32_t s[64];
-            tmem_ld32p(tS + 64, s);
-            tmem_ld32p(tS + 96, s + 32);
-            tc_wait_ld();
-            reg_tie32(s);
-            reg_tie32(s + 32);
-            if (threadIdx.x == 0 && n == 0) CTA_STAMP(5);
-            const bool partial = kind == TILE_PARTIAL;
-            if (partial) mask_cols<2>(s, sg, j, qpos_sh[r], 64);
-            const float mx_hi = max64(s);
-            tmem_ld32p(tS, s);
-            tmem_ld32p(tS + 32, s + 32);
-            tc_wait_ld();
-            reg_tie32(s);
-            reg_tie32(s + 32);
-            if (partial) mask_cols<2>(s, sg, j, qpos_sh[r], 0);
-            const float mx = fmaxf(mx_hi, max64(s)) * sl2;
-            // ---- the serial link: m(n) = lazy max(m(n-1), rowmax(S(n))) ----
-            if (n > 0) {  // m(n-1) from the other group (named barrier 2 + parity: 128 + 128 threads)
-                named_bar_sync(2 + ((n - 1) & 1), 2 * BM);
-                m = msh[((n - 1) & 1) * BM + r];
-            }
-            const bool need = mx > m + 8.0f;
-            const float m_prev = m;
-            if (need) m = mx;
-            if (lane == 0 && quad == 0) KTRACE(4 * g + 1, n);
-            // O holds PV up to n-1 relative to m(n-1): rescale it once PV(n-1) completed, before
-            // m(n) is published (so no later PV can be issued meanwhile)
-            if (n > 0 && __any_sync(0xFFFFFFFFu, need)) {
-                mbar_wait(bar(L::B_VE + (n - 1) % L::VST), ((n - 1) / L::VST) & 1);  // PV(n-1) done
-                tc_fence_after();
-                const float alpha = need ? ex2(m_prev - m) : 1.0f;
-#pragma unroll 1
-                for (int c = 0; c < HD / 16; ++c) {
-                    uint32_t o[16];
-                    tmem_ld16(tO + 16 * c, o);
-                    tc_wait_ld();
-                    reg_tie16(o);
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                    tmem_st16(tO + 16 * c, o);
-                }
-            }
-            msh[(n & 1) * BM + r] = m;
-            __threadfence_block();
-            named_bar_arrive(2 + (n & 1), 2 * BM);
-#if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 1
-            // debug: S read + row max only, no exponentials / P stores
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar(L::B_PF + b));
-            continue;
-#endif
-            // this group's row sum follows m
-            if (m != m_used) {
-                const float beta = ex2(m_used - m);  // m_used = -inf: l is 0 anyway
-                lacc.x *= beta;
-                lacc.y *= beta;
-                m_used = m;
-            }
-            const float m_use = (m == -INFINITY) ? 0.f : m;
-            const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m_use, -m_use);
-            // keys 0-63 from registers -> P columns 0-31; keys 64-127 re-read in two pieces,
-            // each load in flight behind the previous piece's exponentials
-            exp32_store(s, sc, nm, lacc, tS);
-            tmem_ld32p(tS + 64, s);
-            exp32_store(s + 32, sc, nm, lacc, tS + 16);
-            tc_wait_ld();
-            reg_tie32(s);
-            tmem_ld32p(tS + 96, s + 32);
-            if (partial) mask_cols<1>(s, sg, j, qpos_sh[r], 64);
-            exp32_store(s, sc, nm, lacc, tS + 32);
-            tc_wait_ld();
-            reg_tie32(s + 32);
-            if (partial) mask_cols<1>(s + 32, sg, j, qpos_sh[r], 96);
-            exp32_store(s + 32, sc, nm, lacc, tS + 48);
-            if (lane == 0 && quad == 0) KTRACE(4 * g + 2, n);
-            tc_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar(L::B_PF + b));
-            if (lane == 0 && quad == 0) KTRACE(4 * g + 3, n);
-        }
-
-        // ---------------- epilogue: normalise, then write / LSE-merge (R3) ----------------
-        if (threadIdx.x == 0) CTA_STAMP(6);
-        // final m = m(n_used-1); combine the two groups' row sums relative to it
-        float2* lsh = reinterpret_cast<float2*>(smem + L::OFF_L);  // [2][BM] (m_used, l)
-        lsh[g * BM + r] = make_float2(m_used, lacc.x + lacc.y);
-        if (n_used > 0 && ((n_used - 1) & 1) != g) {  // the other group made the last m: take it
-            named_bar_sync(2 + ((n_used - 1) & 1), 2 * BM);  // (pairs with its last arrive)
-            m = msh[((n_used - 1) & 1) * BM + r];
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");  // both groups' (m_used, l) visible
-        float l = 0.f;
-#pragma unroll
-        for (int gg = 0; gg < 2; ++gg) {
-            const float2 ml = lsh[gg * BM + r];
-            if (ml.y > 0.f) l += ml.y * ex2(ml.x - m);
-        }
-        mbar_wait(bar(L::B_OF), 0);
-        tc_fence_after();
-        const float inv_l = l > 0.f ? 1.0f / l : 0.f;
-        const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
         const int64_t nq = sg.nq;
-        float wa = 0.f, wb = 1.f, lse_out = lse_b;
         const bool merge = p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST;
         const bool to_acc = p.mode == CDSP_ATTN_FIRST || p.mode == CDSP_ATTN_MID;
-        if (merge) {
-            const float lse_a = row_ok ? p.lse_acc[static_cast<size_t>(head) * nq + row] : -INFINITY;
-            merge_weights(lse_a, lse_b, wa, wb, lse_out);
-        }
-        const float sbw = wb * inv_l;
-        const size_t orow = (static_cast<size_t>(row_ok ? row : 0) * p.Hq + head) * HD;
-        if constexpr (HD == 128) {
-            // Staged epilogue: thread = row, but global traffic goes through 128B-swizzled smem
-            // tiles moved by TMA (a thread-per-row store touches 32 rows per warp instruction).
-            // fp32 results (FIRST/MID) are written in place over the accumulator tile in the K
-            // stages; bf16 results (ONLY/LAST) into the V stages.  Group g owns columns
-            // [64 g, 64 g + 64): fp32 boxes 2g, 2g+1 (32 columns each), bf16 box g.
-            if (merge) mbar_wait(bar(L::B_ACC), 0);  // accumulator tile landed (K warp's TMA)
-            const uint32_t rsw = static_cast<uint32_t>(r & 7);
-#pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-                uint32_t o[32];
-                if (n_used > 0) {
-                    tmem_ld32p(tO + 32 * (2 * g + cc), o);
-                    tc_wait_ld();
-                    reg_tie32(o);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) o[i] = 0u;
+        int gn0 = 0, n_units_done = 0;
+        for (int i = 0;; ++i) {
+            const int ub = i & 1;
+            mbar_wait(bar(L::B_UF + ub), (i >> 1) & 1);
+            const UnitInfo u = uinfo[ub];
+            if (u.x < 0) break;
+            const int N = u.n_used;
+            const int head = u.x / p.n_rb;
+            const int64_t row = static_cast<int64_t>(p.n_rb - 1 - u.x % p.n_rb) * BM + r;
+            const bool row_ok = row < nq;
+            const uint8_t* sched = smem + L::OFF_SCHED + ub * kSchedMax;
+            const int64_t* qp = reinterpret_cast<const int64_t*>(smem + L::OFF_QP) + ub * BM;
+            float lse_a = -INFINITY;  // issued early: only needed in the epilogue
+            if (merge && row_ok) lse_a = p.lse_acc[static_cast<size_t>(head) * nq + row];
+
+            float m = -INFINITY;       // m(n) of the last tile this thread has seen
+            float m_used = -INFINITY;  // max that this group's l is relative to
+            float2 lacc = make_float2(0.f, 0.f);
+            // this group's tiles: local n with (gn0 + n) & 1 == g; jc = KV tile index of tile n
+            auto next_used = [&](int jj) {
+                ++jj;
+                while (jj < u.j_hi && sched[jj] == 0) ++jj;
+                return jj;
+            };
+            const int n_first = (g - gn0) & 1;
+            int jc = u.j_lo;
+            if (n_first == 1 && N > 1) jc = next_used(jc);
+            for (int n = n_first; n < N; n += 2, jc = next_used(next_used(jc))) {
+                const int gn = gn0 + n;
+                const int j = jc;
+                const int kind = sched[j];
+                const int b = gn % NSB;
+                const uint32_t tS = tmem + lane_off + col_s(b);
+                if (lane == 0 && quad == 0) KTRACE(12 + g, gn);
+                mbar_wait(bar(L::B_SF + b), (gn / NSB) & 1);
+                if (lane == 0 && quad == 0) KTRACE(4 * g + 0, gn);
+                tc_fence_after();
+#if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 0
+                // debug: MMA pipeline alone (no TMEM traffic from the softmax; results garbage)
+                if (n > 0) named_bar_sync(2 + ((gn - 1) & 1), 2 * BM);
+                named_bar_arrive(2 + (gn & 1), 2 * BM);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar(L::B_PF + b));
+                continue;
+#endif
+                // 64 score registers: columns 64-127 first (max only), then 0-63 (max, kept for the
+                // exponentials); 64-127 are re-read from TMEM for their exponentials (P(n) only ever
+                // overwrites S columns 0-63)
+                uint32_t s[64];
+                tmem_ld32p(tS + 64, s);
+                tmem_ld32p(tS + 96, s + 32);
+                tc_wait_ld();
+                reg_tie32(s);
+                reg_tie32(s + 32);
+#ifdef CDSP_KTRACE
+                if (r == 0 && n == 0) UNIT_STAMP(u.x, 5, gtime_ns());
+#endif
+                const bool partial = kind == TILE_PARTIAL;
+                if (partial) mask_cols<2>(s, sg, j, qp[r], 64);
+                const float mx_hi = max64(s);
+                tmem_ld32p(tS, s);
+                tmem_ld32p(tS + 32, s + 32);
+                tc_wait_ld();
+                reg_tie32(s);
+                reg_tie32(s + 32);
+                if (partial) mask_cols<2>(s, sg, j, qp[r], 0);
+                const float mx = fmaxf(mx_hi, max64(s)) * sl2;
+                // ---- the serial link: m(n) = lazy max(m(n-1), rowmax(S(n))) ----
+                if (n > 0) {  // m(n-1) from the other group (named barrier 2 + parity: 128 + 128 threads)
+                    named_bar_sync(2 + ((gn - 1) & 1), 2 * BM);
+                    m = msh[((gn - 1) & 1) * BM + r];
                 }
-                float v[32];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]) * sbw;
-                const uint32_t fbox = sK + static_cast<uint32_t>(2 * g + cc) * (BM * 128) + static_cast<uint32_t>(r) * 128;
-                if (merge) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        float4 av;
-                        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                     : "=f"(av.x), "=f"(av.y), "=f"(av.z), "=f"(av.w)
-                                     : "r"(fbox + ((j ^ rsw) << 4)));
-                        v[4 * j + 0] = fmaf(wa, av.x, v[4 * j + 0]);
-                        v[4 * j + 1] = fmaf(wa, av.y, v[4 * j + 1]);
-                        v[4 * j + 2] = fmaf(wa, av.z, v[4 * j + 2]);
-                        v[4 * j + 3] = fmaf(wa, av.w, v[4 * j + 3]);
-                    }
-                }
-                if (to_acc) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(fbox + ((j ^ rsw) << 4)),
-                                     "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
-                                     : "memory");
-                } else {
-                    const uint32_t hbox = sV + static_cast<uint32_t>(g) * (BM * 128) + static_cast<uint32_t>(r) * 128;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint32_t ch = static_cast<uint32_t>(4 * cc + j);
-                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(hbox + ((ch ^ rsw) << 4)),
-                                     "r"(pack_bf16(v[8 * j + 0], v[8 * j + 1])), "r"(pack_bf16(v[8 * j + 2], v[8 * j + 3])),
-                                     "r"(pack_bf16(v[8 * j + 4], v[8 * j + 5])), "r"(pack_bf16(v[8 * j + 6], v[8 * j + 7]))
-                                     : "memory");
-                    }
-                }
-            }
-            fence_proxy_async_smem();
-            named_bar_sync(4 + g, BM);  // this group's 128 rows are in smem
-            if (threadIdx.x == static_cast<unsigned>(g * BM)) {
-                if (to_acc) {
-                    for (int cc = 0; cc < 2; ++cc)
-                        tma_store_3d(&tm_acc, sK + static_cast<uint32_t>(2 * g + cc) * (BM * 128), 32 * (2 * g + cc), head,
-                                     static_cast<int>(row0));
-                } else {
-                    tma_store_3d(&tm_out, sV + static_cast<uint32_t>(g) * (BM * 128), 64 * g, head, static_cast<int>(row0));
-                }
-                bulk_commit();
-                bulk_wait_read0();  // smem stays valid until the store has read it
-            }
-        } else {
-        // group g writes O columns [g*HD/2, (g+1)*HD/2)
+                const bool need = mx > m + 8.0f;
+                const float m_prev = m;
+                if (need) m = mx;
+                if (lane == 0 && quad == 0) KTRACE(4 * g + 1, gn);
+                // O holds PV up to n-1 relative to m(n-1): rescale it once PV(n-1) completed, before
+                // m(n) is published (so no later PV can be issued meanwhile)
+                if (n > 0 && __any_sync(0xFFFFFFFFu, need)) {
+                    mbar_wait(bar(L::B_VE + (gn - 1) % L::VST), ((gn - 1) / L::VST) & 1);  // PV(n-1) done
+                    tc_fence_after();
+                    const float alpha = need ? ex2(m_prev - m) : 1.0f;
 #pragma unroll 1
-        for (int c = g * (HD / 64); c < (g + 1) * (HD / 64); ++c) {
-            uint32_t o[32];
-            if (n_used > 0) {
-                tmem_ld32p(tO + 32 * c, o);
+                    for (int c = 0; c < HD / 16; ++c) {
+                        uint32_t o[16];
+                        tmem_ld16(tO + 16 * c, o);
+                        tc_wait_ld();
+                        reg_tie16(o);
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha);
+                        tmem_st16(tO + 16 * c, o);
+                    }
+                }
+                msh[(gn & 1) * BM + r] = m;
+                __threadfence_block();
+                named_bar_arrive(2 + (gn & 1), 2 * BM);
+#if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 1
+                // debug: S read + row max only, no exponentials / P stores
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar(L::B_PF + b));
+                continue;
+#endif
+                // this group's row sum follows m
+                if (m != m_used) {
+                    const float beta = ex2(m_used - m);  // m_used = -inf: l is 0 anyway
+                    lacc.x *= beta;
+                    lacc.y *= beta;
+                    m_used = m;
+                }
+                const float m_use = (m == -INFINITY) ? 0.f : m;
+                const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m_use, -m_use);
+                // keys 0-63 from registers -> P columns 0-31; keys 64-127 re-read in two pieces,
+                // each load in flight behind the previous piece's exponentials
+                exp32_store(s, sc, nm, lacc, tS);
+                tmem_ld32p(tS + 64, s);
+                exp32_store(s + 32, sc, nm, lacc, tS + 16);
+                tc_wait_ld();
+                reg_tie32(s);
+                tmem_ld32p(tS + 96, s + 32);
+                if (partial) mask_cols<1>(s, sg, j, qp[r], 64);
+                exp32_store(s, sc, nm, lacc, tS + 32);
+                tc_wait_ld();
+                reg_tie32(s + 32);
+                if (partial) mask_cols<1>(s + 32, sg, j, qp[r], 96);
+                exp32_store(s + 32, sc, nm, lacc, tS + 48);
+                if (lane == 0 && quad == 0) KTRACE(4 * g + 2, gn);
+                tc_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar(L::B_PF + b));
+                if (lane == 0 && quad == 0) KTRACE(4 * g + 3, gn);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(L::B_UE + ub));  // done with the unit's schedule / positions
+#ifdef CDSP_KTRACE
+            if (r == 0 && g == 0) UNIT_STAMP(u.x, 6, gtime_ns());
+#endif
+            if (N == 0 && p.mode == CDSP_ATTN_MID) continue;  // merging an empty block is the identity
+
+            // ---------------- epilogue: normalise, then write / LSE-merge (R3) ----------------
+            float l = 0.f;
+            uint32_t o[HD / 2];  // this group's O columns [g HD/2, (g+1) HD/2)
+            if (N > 0) {
+                // final m = m(last); combine the two groups' row sums relative to it
+                const int last = gn0 + N - 1;
+                float2* lsh = reinterpret_cast<float2*>(smem + L::OFF_L) + (n_units_done & 1) * 2 * BM;
+                lsh[g * BM + r] = make_float2(m_used, lacc.x + lacc.y);
+                if ((last & 1) != g) {  // the other group made the last m: take it
+                    named_bar_sync(2 + (last & 1), 2 * BM);  // (pairs with its last arrive)
+                    m = msh[(last & 1) * BM + r];
+                }
+                asm volatile("bar.sync 1, 256;" ::: "memory");  // both groups' (m_used, l) visible
+#pragma unroll
+                for (int gg = 0; gg < 2; ++gg) {
+                    const float2 ml = lsh[gg * BM + r];
+                    if (ml.y > 0.f) l += ml.y * ex2(ml.x - m);
+                }
+                // drain O to registers and hand TMEM back to the next unit's PV
+                mbar_wait(bar(L::B_OF), n_units_done & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < HD / 64; ++c) tmem_ld32p(tO + (HD / 2) * g + 32 * c, o + 32 * c);
                 tc_wait_ld();
                 reg_tie32(o);
+                if constexpr (HD == 128) reg_tie32(o + 32);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar(L::B_OE));
+                gn0 += N;
+                ++n_units_done;
             } else {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) o[i] = 0u;
+                for (int q = 0; q < HD / 2; ++q) o[q] = 0u;
             }
+            const float inv_l = l > 0.f ? 1.0f / l : 0.f;
+            const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+            float wa = 0.f, wb = 1.f, lse_out = lse_b;
+            if (merge) merge_weights(lse_a, lse_b, wa, wb, lse_out);
+            const float sbw = wb * inv_l;
             if (row_ok) {
-                float v[32];
+                const size_t orow = (static_cast<size_t>(row) * p.Hq + head) * HD + (HD / 2) * g;
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(o[i]) * sbw;
-                if (merge) {
-                    const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
+                for (int c = 0; c < HD / 64; ++c) {
+                    float v[32];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const float4 av = a4[i];
-                        v[4 * i + 0] = fmaf(wa, av.x, v[4 * i + 0]);
-                        v[4 * i + 1] = fmaf(wa, av.y, v[4 * i + 1]);
-                        v[4 * i + 2] = fmaf(wa, av.z, v[4 * i + 2]);
-                        v[4 * i + 3] = fmaf(wa, av.w, v[4 * i + 3]);
+                    for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(o[32 * c + q]) * sbw;
+                    if (merge) {
+                        const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 av = a4[q];
+                            v[4 * q + 0] = fmaf(wa, av.x, v[4 * q + 0]);
+                            v[4 * q + 1] = fmaf(wa, av.y, v[4 * q + 1]);
+                            v[4 * q + 2] = fmaf(wa, av.z, v[4 * q + 2]);
+                            v[4 * q + 3] = fmaf(wa, av.w, v[4 * q + 3]);
+                        }
+                    }
+                    if (to_acc) {
+                        float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow + 32 * c);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    } else {
+                        uint4* d4 = reinterpret_cast<uint4*>(p.out + orow + 32 * c);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            d4[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                               pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
                     }
                 }
-                if (to_acc) {
-                    float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow + 32 * c);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                } else {
-                    uint4* d4 = reinterpret_cast<uint4*>(p.out + orow + 32 * c);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        d4[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                                           pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+                if (g == 0) {
+                    const size_t li = static_cast<size_t>(head) * nq + row;
+                    if (to_acc) {
+                        p.lse_acc[li] = lse_out;
+                    } else if (p.lse) {
+                        p.lse[li] = lse_out;
+                    }
                 }
             }
-        }
-        }  // HD != 128
-        if (row_ok && g == 0) {
-            const size_t li = static_cast<size_t>(head) * nq + row;
-            if (to_acc) {
-                p.lse_acc[li] = lse_out;
-            } else if (p.lse) {
-                p.lse[li] = lse_out;
+#ifdef CDSP_KTRACE
+            if (r == 0 && g == 0) {
+                const unsigned long long t = gtime_ns();
+                unsigned smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                UNIT_STAMP(u.x, 7, t);
+                UNIT_STAMP(u.x, 1, t);
+                UNIT_STAMP(u.x, 2, smid);
+                UNIT_STAMP(u.x, 3, N);
             }
+#endif
         }
-        if (threadIdx.x == 0) CTA_STAMP(7);
     }
 
-#ifdef CDSP_KTRACE
-    if (threadIdx.x == 0 && blockIdx.x < 65536) {
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        int nu = 0;
-        for (int j = 0; j < n_kv_tiles; ++j) nu += sched[j] != 0;
-        g_cta[blockIdx.x * 8 + 0] = t_start;
-        g_cta[blockIdx.x * 8 + 2] = smid;
-        g_cta[blockIdx.x * 8 + 3] = nu;
-    }
-#endif
     // ---- teardown
     tc_fence_before();
     __syncthreads();
@@ -814,7 +828,13 @@ __global__ void __maxnreg__(168)
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
-    if (threadIdx.x == 0) CTA_STAMP(1);
+    if (threadIdx.x == 0) {  // the last CTA out re-arms the unit counter for a later launch
+        __threadfence();
+        if (atomicAdd(p.claim + 1, 1) == G - 1) {
+            atomicExch(p.claim, 0);
+            atomicExch(p.claim + 1, 0);
+        }
+    }
 }
 
 // ------------------------------------------------------------------ host side
@@ -835,24 +855,6 @@ EncodeTiledFn get_encode_fn() {
 }
 
 // [T, H, D] bf16 tensor, box = 128 rows x 1 head x 64 d, 128-byte swizzle.
-// fp32 [T, H, D], box = 128 rows x 1 head x 32 columns (128 B), 128-byte swizzle (epilogue staging).
-cdsp_status make_map_f32(CUtensorMap* m, const void* base, int64_t T, int H, int D) {
-    EncodeTiledFn enc = get_encode_fn();
-    CDSP_REQUIRE(enc != nullptr, CDSP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    CDSP_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15u) == 0, CDSP_ERR_INVALID,
-                 "TMA base pointer must be 16-byte aligned");
-    cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(H),
-                          static_cast<cuuint64_t>(T > 0 ? T : 1)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 4, static_cast<cuuint64_t>(H) * D * 4};
-    cuuint32_t box[3] = {32, 1, 128};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    CDSP_REQUIRE(r == CUDA_SUCCESS, CDSP_ERR_CUDA, "cuTensorMapEncodeTiled(f32) failed (%d)", static_cast<int>(r));
-    return CDSP_OK;
-}
-
 cdsp_status make_map(CUtensorMap* m, const void* base, int64_t T, int H, int D) {
     EncodeTiledFn enc = get_encode_fn();
     CDSP_REQUIRE(enc != nullptr, CDSP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -870,6 +872,33 @@ cdsp_status make_map(CUtensorMap* m, const void* base, int64_t T, int H, int D) 
     return CDSP_OK;
 }
 
+// Unit counters of the persistent kernel: one [claim, done] pair per launch, taken round-robin
+// from a zeroed ring (each launch's last CTA re-zeroes its pair; a pair is reused only after
+// kClaimSlots later launches, far more than can run concurrently).
+constexpr int kClaimSlots = 4096;
+cdsp_status claim_slot(int** out) {
+    static int* ring[64] = {};
+    static unsigned counter[64] = {};
+    int dev = 0;
+    CDSP_CUDA(cudaGetDevice(&dev));
+    CDSP_REQUIRE(dev >= 0 && dev < 64, CDSP_ERR_CUDA, "device ordinal %d", dev);
+    if (!ring[dev]) {
+        CDSP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ring[dev]), kClaimSlots * 2 * sizeof(int)));
+        CDSP_CUDA(cudaMemset(ring[dev], 0, kClaimSlots * 2 * sizeof(int)));
+        CDSP_CUDA(cudaDeviceSynchronize());
+    }
+    *out = ring[dev] + 2 * (__atomic_fetch_add(&counter[dev], 1u, __ATOMIC_RELAXED) % kClaimSlots);
+    return CDSP_OK;
+}
+
+int sm_count() {
+    static int n[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (n[dev] == 0 && cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n[dev] = 148;
+    return n[dev];
+}
+
 template <int HD>
 cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     using Lt = Layout<HD>;
@@ -880,36 +909,32 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     }
     CDSP_REQUIRE((a.seg.nkv + BN - 1) / BN <= kSchedMax, CDSP_ERR_CAPACITY, "KV block of %lld rows exceeds %d",
                  static_cast<long long>(a.seg.nkv), kSchedMax * BN);
-    CUtensorMap mq, mk, mv;
-    CDSP_CHECK_STATUS(make_map(&mq, a.q, a.seg.nq, a.Hq, HD));
-    const void* kb = a.seg.nkv > 0 ? a.k : a.q;  // nkv == 0: map never dereferenced
-    const void* vb = a.seg.nkv > 0 ? a.v : a.q;
-    CDSP_CHECK_STATUS(make_map(&mk, kb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD));
-    CDSP_CHECK_STATUS(make_map(&mv, vb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD));
-    // epilogue maps (HD = 128): fp32 accumulators (FIRST/MID/LAST) and the bf16 output
-    // (ONLY/LAST); a mode that does not use one gets a never-dereferenced stand-in
-    CUtensorMap macc = mq, mout = mq;
-    if (HD == 128 && a.seg.nq > 0) {
-        if (a.mode != CDSP_ATTN_ONLY) CDSP_CHECK_STATUS(make_map_f32(&macc, a.o_acc, a.seg.nq, a.Hq, HD));
-        if (a.mode == CDSP_ATTN_ONLY || a.mode == CDSP_ATTN_LAST)
-            CDSP_CHECK_STATUS(make_map(&mout, a.out, a.seg.nq, a.Hq, HD));
-    }
     TcParams p;
     p.seg = a.seg;
     p.Hq = a.Hq;
     p.Hkv = a.Hkv;
     p.g = a.Hq / a.Hkv;
     p.n_rb = static_cast<int>((a.seg.nq + BM - 1) / BM);
+    const int64_t units = static_cast<int64_t>(p.n_rb) * a.Hq;
+    if (units == 0) return CDSP_OK;
+    CDSP_REQUIRE(units < (1ll << 30), CDSP_ERR_SHAPE, "too many query tiles");
+    p.n_units = static_cast<int>(units);
     p.scale_log2 = a.scale * 1.4426950408889634f;
     p.mode = a.mode;
     p.o_acc = a.o_acc;
     p.lse_acc = a.lse_acc;
     p.out = static_cast<__nv_bfloat16*>(a.out);
     p.lse = a.lse;
-    const int64_t grid = static_cast<int64_t>(p.n_rb) * a.Hq;
-    if (grid == 0) return CDSP_OK;
-    CDSP_REQUIRE(grid < (1ll << 31), CDSP_ERR_SHAPE, "grid too large");
-    attn_tc_kernel<HD><<<static_cast<unsigned>(grid), kThreads, Lt::SMEM, st>>>(mq, mk, mv, macc, mout, p);
+    CDSP_CHECK_STATUS(claim_slot(&p.claim));
+    CUtensorMap mq, mk, mv;
+    CDSP_CHECK_STATUS(make_map(&mq, a.q, a.seg.nq, a.Hq, HD));
+    const void* kb = a.seg.nkv > 0 ? a.k : a.q;  // nkv == 0: map never dereferenced
+    const void* vb = a.seg.nkv > 0 ? a.v : a.q;
+    CDSP_CHECK_STATUS(make_map(&mk, kb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD));
+    CDSP_CHECK_STATUS(make_map(&mv, vb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD));
+    // persistent: one CTA per SM (TMEM and shared memory admit one), units claimed dynamically
+    const int grid = static_cast<int>(units < sm_count() ? units : sm_count());
+    attn_tc_kernel<HD><<<grid, kThreads, Lt::SMEM, st>>>(mq, mk, mv, p);
     CDSP_CUDA(cudaGetLastError());
 #ifdef CDSP_KTRACE
     if (const char* path = getenv("CDSP_TRACE")) {  // debug builds only: synchronous dump
