@@ -73,7 +73,7 @@
 #endif
 
 #ifndef CDSP_EMU_MASK
-#define CDSP_EMU_MASK 0x02
+#define CDSP_EMU_MASK 0x22
 #endif
 
 namespace cdsp {
@@ -89,31 +89,46 @@ constexpr int kBox = 128 * 128;         // TMA box: 128 rows x 64 bf16 (128-byte
 constexpr int kSchedMax = 8192;         // KV tiles per launch (1M keys)
 constexpr int W_K = 8, W_V = 9, W_MMA = 10;
 
-template <int HD>
+// PAIR: 2-SM variant (HD = 128).  A CTA pair (cluster of 2) runs M = 256 MMAs (cta_group::2):
+// each CTA holds its own 128 query rows of Q and of S / P / O in its TMEM, and HALF of every
+// K tile (64 keys) and V tile (64 of the 128 d columns) — so each SM streams 32 KB per KV tile
+// from L2 instead of 64 KB.  The even CTA issues the MMAs; S / V / O completions are
+// multicast to both CTAs' barriers, both CTAs' TMA bytes and softmax arrivals land on the even
+// CTA's barriers.
+template <int HD, bool PAIR>
 struct Layout {
     static constexpr int NBOX = HD / 64;
-    static constexpr int TILE = kBox * NBOX;  // one 128-row tile of Q, K or V
-    static constexpr int KST = 3, VST = CDSP_VST;  // KST == NSB: K stage n%3 is free once S(n) is
+    static constexpr int TILE = kBox * NBOX;            // one 128-row tile of Q (this CTA's rows)
+    static constexpr int KTILE = PAIR ? TILE / 2 : TILE;  // this CTA's part of a K tile
+    static constexpr int VTILE = PAIR ? TILE / 2 : TILE;  // this CTA's part of a V tile
+    static constexpr int KST = 3, VST = PAIR ? 4 : CDSP_VST;  // KST == NSB: K stage n%3 is free once S(n) is
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = OFF_Q + TILE;
-    static constexpr int OFF_V = OFF_K + KST * TILE;
-    static constexpr int OFF_M = OFF_V + VST * TILE;       // running row max m(n): [2 tile parity][128] float
+    static constexpr int OFF_V = OFF_K + KST * KTILE;
+    static constexpr int OFF_M = OFF_V + VST * VTILE;      // running row max m(n): [2 tile parity][128] float
     static constexpr int OFF_L = OFF_M + 2 * BM * 4;       // epilogue (m_used, l): [2 unit parity][2 groups][128] float2
     static constexpr int OFF_QP = OFF_L + 4 * BM * 8;      // query position per row: [2 unit buffer][128] int64
     static constexpr int OFF_BAR = OFF_QP + 2 * BM * 8;
-    // u_full[2] (unit buffer published: schedule + Q tile), k_full[KST], v_full[VST], v_empty[VST],
-    // s_full[NSB], p_full[NSB], o_full, o_free, u_empty[2] (unit buffer read by every consumer).
+    // Local: u_full[2] (unit buffer published), u_empty[2] (read by every consumer), s_full[NSB],
+    // v_empty[VST], o_full (the last three arrive by MMA commit, multicast to both CTAs of a pair).
+    // Leader (the even CTA; the only one in a 1-SM launch): q_full, k_full[KST], v_full[VST]
+    // (TMA bytes of both CTAs), p_full[NSB], o_free (softmax warps of both CTAs).
+    // Pair bookkeeping: c_full[2] (odd CTA: next unit id arrived), c_empty[2] (even CTA: consumed).
     // (m(n) goes from one softmax group to the other through named barriers 2, 3.)  Every
     // tcgen05.commit costs the tensor pipe ~30 clk (tools/mma_pattern.cu), so each MMA group
     // commits once: s_full[b] (S(n) done) also frees K stage n % 3 (and, for a unit's last
     // tile, the Q buffer); v_empty[s] (PV(n) done) also tells a rescaling group that O is stable.
-    static constexpr int B_UF = 0, B_KF = 2, B_VF = B_KF + KST, B_VE = B_VF + VST, B_SF = B_VE + VST,
-                         B_PF = B_SF + NSB, B_OF = B_PF + NSB, B_OE = B_OF + 1, B_UE = B_OE + 1, NBAR = B_UE + 2;
+    static constexpr int B_UF = 0, B_UE = 2, B_QF = 4, B_KF = 5, B_VF = B_KF + KST, B_VE = B_VF + VST,
+                         B_SF = B_VE + VST, B_PF = B_SF + NSB, B_OF = B_PF + NSB, B_OE = B_OF + 1, B_CF = B_OE + 1,
+                         B_CE = B_CF + 2, NBAR = B_CE + 2;
     static_assert(KST == NSB, "K stages are released through s_full");
     static constexpr int OFF_TMEM_SLOT = OFF_BAR + NBAR * 8;
-    static constexpr int OFF_UNIT = OFF_TMEM_SLOT + 16;     // [2] x {unit, j_lo, j_hi, n_used}
-    static constexpr int OFF_SCHED = OFF_UNIT + 2 * 16;     // [2][kSchedMax] tile kinds
-    static constexpr int SMEM = OFF_SCHED + 2 * kSchedMax + 1024;  // + alignment slack
+    static constexpr int OFF_CLAIM = OFF_TMEM_SLOT + 8;     // [2] next unit id (odd CTA of a pair)
+    static constexpr int OFF_UNIT = OFF_CLAIM + 8;          // [2] x {unit, n_used}
+    // [2][LISTMAX] used KV tiles of the unit in order: tile index | 0x8000 if partial
+    static constexpr int LISTMAX = (PAIR || HD == 64) ? kSchedMax : kSchedMax / 2;
+    static constexpr int OFF_SCHED = OFF_UNIT + 2 * 16;
+    static constexpr int SMEM = OFF_SCHED + 2 * LISTMAX * 2 + 1024;  // + alignment slack
 };
 
 constexpr uint32_t COL_O = 0;
@@ -129,6 +144,7 @@ struct TcParams {
     __nv_bfloat16* out;
     float* lse;
     int* claim;  // [2]: dynamic unit counter, finished-CTA counter (both zero at launch; the last CTA re-zeroes them)
+    int n_pb;    // row blocks per head in units of the CTA group (PAIR: pairs of 128-row blocks)
 };
 
 // Debug timeline (build with -DCDSP_KTRACE): per-unit phase stamps (globaltimer) and SM id,
@@ -324,17 +340,19 @@ __device__ __forceinline__ void exp32_store(const uint32_t* s, float2 sc, float2
 
 // Work unit x in [0, n_units): head-major (the ~148 units in flight share one head's K/V,
 // which stays L2-resident), heavy row blocks first within a head (causal work grows with
-// the row).  Units are handed out dynamically (first one = blockIdx.x, then an atomic
-// counter), like the hardware's own CTA scheduler but without a CTA's fixed costs per unit.
+// the row).  Units are handed out dynamically (first one = the CTA group's index, then an
+// atomic counter), like the hardware's own CTA scheduler but without a CTA's fixed costs
+// per unit.  PAIR: a unit is two adjacent 128-row blocks (the even CTA takes the lower).
 struct UnitInfo {
-    int x, j_lo, j_hi, n_used;  // x < 0: no more units
+    int x, n_used;  // x < 0: no more units
 };
+constexpr uint16_t kPartialBit = 0x8000;
 
-template <int HD>
+template <int HD, bool PAIR>
 __global__ void __maxnreg__(168)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const TcParams p) {
-    using L = Layout<HD>;
+    using L = Layout<HD, PAIR>;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
     const uint32_t raw_addr = smem_u32(smem_raw);
@@ -349,7 +367,17 @@ __global__ void __maxnreg__(168)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const cdsp_segments& sg = p.seg;
     const int n_kv_tiles = static_cast<int>((sg.nkv + BN - 1) / BN);
-    const int G = static_cast<int>(gridDim.x);
+    constexpr int CL = PAIR ? 2 : 1;
+    const int crank = PAIR ? static_cast<int>(cluster_ctarank()) : 0;
+    const bool leader = crank == 0;
+    const int G = static_cast<int>(gridDim.x) / CL;  // CTA groups
+    // the leader's barrier i as seen from this CTA (TMA bytes / arrivals of both CTAs land there)
+    auto lbar = [&](int i) { return PAIR ? mapa_shared(bar(i), 0) : bar(i); };
+    auto unit_rows = [&](int x, int c, int& head, int64_t& row0) {
+        head = x / p.n_pb;
+        const int pb = p.n_pb - 1 - x % p.n_pb;
+        row0 = static_cast<int64_t>(PAIR ? 2 * pb + c : pb) * BM;
+    };
 
     // ---- setup (once per CTA)
     if (warp == W_K) {
@@ -357,7 +385,10 @@ __global__ void __maxnreg__(168)
             for (int i = 0; i < 2; ++i) {
                 mbar_init(bar(L::B_UF + i), 1);
                 mbar_init(bar(L::B_UE + i), 10);  // 8 softmax warps, V producer, MMA warp
+                mbar_init(bar(L::B_CF + i), 1);
+                mbar_init(bar(L::B_CE + i), 1);
             }
+            mbar_init(bar(L::B_QF), 1);
             for (int i = 0; i < L::KST; ++i) mbar_init(bar(L::B_KF + i), 1);
             for (int i = 0; i < L::VST; ++i) {
                 mbar_init(bar(L::B_VF + i), 1);
@@ -365,36 +396,54 @@ __global__ void __maxnreg__(168)
             }
             for (int b = 0; b < NSB; ++b) {
                 mbar_init(bar(L::B_SF + b), 1);
-                mbar_init(bar(L::B_PF + b), 4);
+                mbar_init(bar(L::B_PF + b), 4 * CL);
             }
             mbar_init(bar(L::B_OF), 1);
-            mbar_init(bar(L::B_OE), 8);
+            mbar_init(bar(L::B_OE), 8 * CL);
             fence_barrier_init();
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
         }
     } else if (warp == W_MMA) {
-        tmem_alloc(smem_u32(tmem_slot), 512);
-        tmem_relinquish();
+        if constexpr (PAIR) {
+            tmem_alloc2(smem_u32(tmem_slot), 512);
+            tmem_relinquish2();
+        } else {
+            tmem_alloc(smem_u32(tmem_slot), 512);
+            tmem_relinquish();
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) cluster_sync_all();  // both CTAs' barriers exist before any remote arrive
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
     if (warp == W_K) {
-        // ======== unit scheduler + TMA producer of Q and K: for each unit, classify its KV
-        // tiles (sched[j], 0 = skip), publish the unit (u_full[i&1]; the Q tile rides on the
-        // same barrier) and stream its K tiles into 3 stages ========
+        // ======== unit scheduler + TMA producer of Q and K: for each unit, list its used KV
+        // tiles in order (empty ones skipped), publish the unit (u_full[i&1]) and stream its
+        // Q tile and K tiles (3 stages) ========
         const uint64_t pol_kv = policy_evict_last();
-        int x = static_cast<int>(blockIdx.x);
-        int x_pre = 0;  // lane 0: the unit after x, claimed one unit ahead
-        if (lane == 0) x_pre = G + atomicAdd(p.claim, 1);
+        const uint64_t pol_q = policy_evict_first();
+        int x = static_cast<int>(blockIdx.x) / CL;
+        int x_pre = 0;  // leader lane 0: the unit after x, claimed one unit ahead
+        if (leader && lane == 0) x_pre = G + atomicAdd(p.claim, 1);
         int it = 0;        // used tiles loaded so far (all units)
         int last_gn = -1;  // the previous non-empty unit's last tile: its S frees the Q buffer
+        int n_ne = 0;      // non-empty units so far
+        int* claim_slot = reinterpret_cast<int*>(smem + L::OFF_CLAIM);
         for (int i = 0;; ++i) {
             const int ub = i & 1;
+            if constexpr (PAIR) {
+                if (!leader && i >= 1) {  // unit id from the even CTA (message i)
+                    const int s = (i - 1) & 1, use = (i - 1) >> 1;
+                    mbar_wait(bar(L::B_CF + s), use & 1);
+                    x = *reinterpret_cast<volatile int*>(claim_slot + s);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(mapa_shared(bar(L::B_CE + s), 0));
+                }
+            }
             if (i >= 2) mbar_wait(bar(L::B_UE + ub), ((i - 2) >> 1) & 1);  // every consumer is done with unit i-2
             if (x >= p.n_units) {
                 if (lane == 0) {
@@ -403,27 +452,35 @@ __global__ void __maxnreg__(168)
                 }
                 break;
             }
-            const int head = x / p.n_rb;
+            int head;
+            int64_t row0;
+            unit_rows(x, crank, head, row0);
             const int kvh = head / p.g;
-            const int64_t row0 = static_cast<int64_t>(p.n_rb - 1 - x % p.n_rb) * BM;
-            uint8_t* sched = smem + L::OFF_SCHED + ub * kSchedMax;
-            int64_t qlo, qhi;
-            bool qany;
+            uint16_t* list = reinterpret_cast<uint16_t*>(smem + L::OFF_SCHED) + ub * L::LISTMAX;
+            int64_t qlo, qhi, plo = 0, phi = 0;
+            bool qany, pany = false;
             seg_qrange(sg, row0, row0 + BM, qlo, qhi, qany);
-            int jmin = INT_MAX, jmax = 0, cnt = 0;
-            for (int j = lane; j < n_kv_tiles; j += 32) {
-                const int k = seg_tile_kind(sg, qany, qlo, qhi, static_cast<int64_t>(j) * BN, BN);
-                sched[j] = static_cast<uint8_t>(k);
-                if (k != 0) {
-                    jmin = min(jmin, j);
-                    jmax = max(jmax, j + 1);
-                    ++cnt;
-                }
+            if constexpr (PAIR) {  // the peer's rows: the pair walks the union of both schedules
+                int ph;
+                int64_t prow0;
+                unit_rows(x, 1 - crank, ph, prow0);
+                seg_qrange(sg, prow0, prow0 + BM, plo, phi, pany);
             }
-            for (int o = 16; o > 0; o >>= 1) {
-                jmin = min(jmin, __shfl_xor_sync(0xFFFFFFFFu, jmin, o));
-                jmax = max(jmax, __shfl_xor_sync(0xFFFFFFFFu, jmax, o));
-                cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+            int cnt = 0;
+            for (int j0 = 0; j0 < n_kv_tiles; j0 += 32) {  // 32 tiles per step, compacted in order
+                const int j = j0 + lane;
+                int k = TILE_EMPTY;
+                if (j < n_kv_tiles) {
+                    k = seg_tile_kind(sg, qany, qlo, qhi, static_cast<int64_t>(j) * BN, BN);
+                    if (PAIR && k == TILE_EMPTY &&
+                        seg_tile_kind(sg, pany, plo, phi, static_cast<int64_t>(j) * BN, BN) != TILE_EMPTY)
+                        k = TILE_PARTIAL;  // needed by the peer only: fully masked here
+                }
+                const uint32_t used = __ballot_sync(0xFFFFFFFFu, k != TILE_EMPTY);
+                if (k != TILE_EMPTY)
+                    list[cnt + __popc(used & ((1u << lane) - 1u))] =
+                        static_cast<uint16_t>(j | (k == TILE_PARTIAL ? kPartialBit : 0));
+                cnt += __popc(used);
             }
             // query positions (only read on partial tiles)
             int64_t* qp = reinterpret_cast<int64_t*>(smem + L::OFF_QP) + ub * BM;
@@ -431,17 +488,21 @@ __global__ void __maxnreg__(168)
                 const int64_t row = row0 + rr;
                 qp[rr] = row < sg.nq ? seg_qpos(sg, row) : (INT64_MAX >> 2);
             }
-            if (lane == 0) uinfo[ub] = UnitInfo{x, jmin, jmax, cnt};
+            if (lane == 0) uinfo[ub] = UnitInfo{x, cnt};
             __threadfence_block();
             __syncwarp();
+            if (lane == 0) mbar_arrive(bar(L::B_UF + ub));  // publish (release)
             if (cnt > 0) {
                 if (last_gn >= 0) mbar_wait(bar(L::B_SF + last_gn % NSB), (last_gn / NSB) & 1);  // Q buffer free
                 if (lane == 0) {
-                    UNIT_STAMP(x, 0, gtime_ns());
-                    UNIT_STAMP(x, 4, gtime_ns());
-                    mbar_expect_tx(bar(L::B_UF + ub), L::TILE);  // publishes the unit (release) + Q bytes
-                    for (int b = 0; b < L::NBOX; ++b)
-                        tma_load_3d(sQ + b * kBox, &tm_q, bar(L::B_UF + ub), b * 64, head, static_cast<int>(row0));
+                    UNIT_STAMP(x * CL + crank, 0, gtime_ns());
+                    if (leader) mbar_expect_tx(bar(L::B_QF), CL * L::TILE);
+                    for (int b = 0; b < L::NBOX; ++b) {
+                        if constexpr (PAIR)
+                            tma_load_3d_2sm(sQ + b * kBox, &tm_q, lbar(L::B_QF), b * 64, head, static_cast<int>(row0), pol_q);
+                        else
+                            tma_load_3d(sQ + b * kBox, &tm_q, bar(L::B_QF), b * 64, head, static_cast<int>(row0));
+                    }
                 }
                 // merge modes: pull this unit's accumulator rows into L2 for the epilogue
                 if (p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST) {
@@ -453,31 +514,47 @@ __global__ void __maxnreg__(168)
                         }
                     }
                 }
-            } else if (lane == 0) {
-                mbar_arrive(bar(L::B_UF + ub));
+                ++n_ne;
             }
             __syncwarp();
-            for (int j = jmin; j < jmax; ++j) {
-                if (sched[j] == 0) continue;
+            for (int n = 0; n < cnt; ++n) {
+                const int j = list[n] & ~kPartialBit;
                 const int st = it % L::KST;
-                // stage st last held tile it - 3: free once S(it - 3) is done
+                // stage st last held tile it - 3: free once S(it - 3) is done (in both CTAs)
                 if (it >= L::KST) mbar_wait(bar(L::B_SF + st), ((it - L::KST) / L::KST) & 1);
                 if (lane == 0) KTRACE(15, it);
                 if (elect_one()) {
-                    mbar_expect_tx(bar(L::B_KF + st), L::TILE);
-                    for (int b = 0; b < L::NBOX; ++b)
-                        tma_load_3d_hint(sK + st * L::TILE + b * kBox, &tm_k, bar(L::B_KF + st), b * 64, kvh, j * BN,
-                                         pol_kv);
+                    if constexpr (PAIR) {
+                        // this CTA's 64 keys of the tile, both d halves
+                        if (leader) mbar_expect_tx(bar(L::B_KF + st), 2 * L::KTILE);
+                        for (int b = 0; b < L::NBOX; ++b)
+                            tma_load_3d_2sm(sK + st * L::KTILE + b * (kBox / 2), &tm_k, lbar(L::B_KF + st), b * 64, kvh,
+                                            j * BN + crank * (BN / 2), pol_kv);
+                    } else {
+                        mbar_expect_tx(bar(L::B_KF + st), L::KTILE);
+                        for (int b = 0; b < L::NBOX; ++b)
+                            tma_load_3d_hint(sK + st * L::KTILE + b * kBox, &tm_k, bar(L::B_KF + st), b * 64, kvh, j * BN,
+                                             pol_kv);
+                    }
                 }
                 __syncwarp();
                 ++it;
             }
             if (cnt > 0) last_gn = it - 1;
             x = __shfl_sync(0xFFFFFFFFu, x_pre, 0);
-            if (lane == 0 && x < p.n_units) x_pre = G + atomicAdd(p.claim, 1);
+            if (leader && lane == 0) {
+                if (x < p.n_units) x_pre = G + atomicAdd(p.claim, 1);
+                if constexpr (PAIR) {  // message i+1 to the odd CTA: the unit it runs next
+                    const int s = i & 1, use = i >> 1;
+                    if (use >= 1) mbar_wait(bar(L::B_CE + s), (use - 1) & 1);  // slot consumed
+                    st_cluster_u32(mapa_shared(smem_u32(claim_slot + s), 1), static_cast<uint32_t>(x));
+                    mbar_arrive_cluster(mapa_shared(bar(L::B_CF + s), 1));
+                }
+            }
+            __syncwarp();
         }
     } else if (warp == W_V) {
-        // ======== TMA producer of V (2 stages), following the published units ========
+        // ======== TMA producer of V, following the published units ========
         const uint64_t pol_kv = policy_evict_last();
         int it = 0;
         for (int i = 0;; ++i) {
@@ -485,18 +562,23 @@ __global__ void __maxnreg__(168)
             mbar_wait(bar(L::B_UF + ub), (i >> 1) & 1);
             const UnitInfo u = uinfo[ub];
             if (u.x < 0) break;
-            const int kvh = (u.x / p.n_rb) / p.g;
-            const uint8_t* sched = smem + L::OFF_SCHED + ub * kSchedMax;
-            for (int j = u.j_lo; j < u.j_hi; ++j) {
-                if (sched[j] == 0) continue;
+            const int kvh = (u.x / p.n_pb) / p.g;
+            const uint16_t* list = reinterpret_cast<const uint16_t*>(smem + L::OFF_SCHED) + ub * L::LISTMAX;
+            for (int n = 0; n < u.n_used; ++n) {
+                const int j = list[n] & ~kPartialBit;
                 const int st = it % L::VST;
                 if (it >= L::VST) mbar_wait(bar(L::B_VE + st), ((it - L::VST) / L::VST) & 1);
                 if (lane == 0) KTRACE(14, it);
                 if (elect_one()) {
-                    mbar_expect_tx(bar(L::B_VF + st), L::TILE);
-                    for (int b = 0; b < L::NBOX; ++b)
-                        tma_load_3d_hint(sV + st * L::TILE + b * kBox, &tm_v, bar(L::B_VF + st), b * 64, kvh, j * BN,
-                                         pol_kv);
+                    if constexpr (PAIR) {  // all 128 keys, this CTA's 64 d columns
+                        if (leader) mbar_expect_tx(bar(L::B_VF + st), 2 * L::VTILE);
+                        tma_load_3d_2sm(sV + st * L::VTILE, &tm_v, lbar(L::B_VF + st), crank * 64, kvh, j * BN, pol_kv);
+                    } else {
+                        mbar_expect_tx(bar(L::B_VF + st), L::VTILE);
+                        for (int b = 0; b < L::NBOX; ++b)
+                            tma_load_3d_hint(sV + st * L::VTILE + b * kBox, &tm_v, bar(L::B_VF + st), b * 64, kvh, j * BN,
+                                             pol_kv);
+                    }
                 }
                 __syncwarp();
                 ++it;
@@ -505,29 +587,41 @@ __global__ void __maxnreg__(168)
             if (lane == 0) mbar_arrive(bar(L::B_UE + ub));
         }
     } else if (warp == W_MMA) {
-        // ================= MMA issuer (warp-uniform loop, one lane issues) =================
-        constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, false, false);
-        constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, HD, false, true);
+        // ================= MMA issuer (warp-uniform loop, one lane issues; PAIR: the even CTA) =================
+        constexpr uint32_t idesc_qk = idesc_bf16_f32(BM * CL, BN, false, false);
+        constexpr uint32_t idesc_pv = idesc_bf16_f32(BM * CL, HD, false, true);
+        constexpr uint32_t KBOX = PAIR ? kBox / 2 : kBox;  // bytes of one 64-column box of a K stage
         const uint64_t dq = umma_desc_sw128(sQ, 16, 1024);
         const uint64_t dk0 = umma_desc_sw128(sK, 16, 1024);
         const uint64_t dv0 = umma_desc_sw128(sV, kBox, 1024);
-        // S(b) = Q K^T: M=128, N=128, K=HD in steps of 16 (32 B inside a 128-B swizzle row)
+        auto commit = [&](int b) {
+            if constexpr (PAIR) mma_commit2_mc(bar(b), 0x3);
+            else mma_commit(bar(b));
+        };
+        // S(b) = Q K^T: M=128 (x2), N=128, K=HD in steps of 16 (32 B inside a 128-B swizzle row)
         auto issue_qk = [&](int ks, int b) {
-            const uint64_t dk = dk0 + static_cast<uint64_t>((ks * L::TILE) >> 4);
+            const uint64_t dk = dk0 + static_cast<uint64_t>((ks * L::KTILE) >> 4);
 #pragma unroll
             for (int kk = 0; kk < HD / 16; ++kk) {
-                const uint64_t off = static_cast<uint64_t>(((kk / 4) * kBox + (kk % 4) * 32) >> 4);
-                mma_ss(tmem + col_s(b), dq + off, dk + off, idesc_qk, kk > 0 ? 1u : 0u);
+                const uint64_t offq = static_cast<uint64_t>(((kk / 4) * kBox + (kk % 4) * 32) >> 4);
+                const uint64_t offk = static_cast<uint64_t>(((kk / 4) * KBOX + (kk % 4) * 32) >> 4);
+                if constexpr (PAIR) mma_ss2(tmem + col_s(b), dq + offq, dk + offk, idesc_qk, kk > 0 ? 1u : 0u);
+                else mma_ss(tmem + col_s(b), dq + offq, dk + offk, idesc_qk, kk > 0 ? 1u : 0u);
             }
         };
-        // O += P(b) V: M=128, N=HD, K=128 keys in steps of 16 (V rows, 2048 B); P(b) is bf16
+        // O += P(b) V: M=128 (x2), N=HD, K=128 keys in steps of 16 (V rows, 2048 B); P(b) is bf16
         // in the S(b) columns (8 TMEM columns per 16 keys)
         auto issue_pv = [&](int vs, int b, bool acc) {
-            const uint64_t dv = dv0 + static_cast<uint64_t>((vs * L::TILE) >> 4);
+            const uint64_t dv = dv0 + static_cast<uint64_t>((vs * L::VTILE) >> 4);
 #pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk)
-                mma_ts(tmem + COL_O, tmem + col_s(b) + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4),
-                       idesc_pv, (acc || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < BN / 16; ++kk) {
+                if constexpr (PAIR)
+                    mma_ts2(tmem + COL_O, tmem + col_s(b) + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4),
+                            idesc_pv, (acc || kk > 0) ? 1u : 0u);
+                else
+                    mma_ts(tmem + COL_O, tmem + col_s(b) + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4),
+                           idesc_pv, (acc || kk > 0) ? 1u : 0u);
+            }
         };
         auto issue_s = [&](int gn) {  // S(gn) into buffer gn % NSB; K stage gn % KST
             const int ks = gn % L::KST;
@@ -536,20 +630,22 @@ __global__ void __maxnreg__(168)
             if (elect_one()) {
                 KTRACE(9, gn);
                 issue_qk(ks, gn % NSB);
-                mma_commit(bar(L::B_SF + gn % NSB));  // S(gn) ready; K stage ks free
+                commit(L::B_SF + gn % NSB);  // S(gn) ready; K stage ks free
             }
             __syncwarp();
         };
+        auto wait_softmax = [&](int b, uint32_t parity) { MMA_WAIT(bar(b), parity); };
         int gn0 = 0, n_units_done = 0;
         for (int i = 0;; ++i) {
             const int ub = i & 1;
-            MMA_WAIT(bar(L::B_UF + ub), (i >> 1) & 1);  // unit published, Q landed
+            MMA_WAIT(bar(L::B_UF + ub), (i >> 1) & 1);  // unit published
             const UnitInfo u = uinfo[ub];
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(L::B_UE + ub));
             if (u.x < 0) break;
             const int N = u.n_used;
-            if (N == 0) continue;
+            if (N == 0 || !leader) continue;
+            MMA_WAIT(bar(L::B_QF), n_units_done & 1);  // Q tile(s) landed
             tc_fence_after();
             // this unit's first S tiles go in only after the previous unit's last PV: its
             // buffers are the ones those PVs read
@@ -560,14 +656,14 @@ __global__ void __maxnreg__(168)
                 if (lane == 0) KTRACE(10, gn);
                 MMA_WAIT(bar(L::B_VF + vs), (gn / L::VST) & 1);
                 if (lane == 0) KTRACE(11, gn);
-                MMA_WAIT(bar(L::B_PF + b), (gn / NSB) & 1);
-                if (n == 0 && n_units_done > 0) MMA_WAIT(bar(L::B_OE), (n_units_done - 1) & 1);  // O drained
+                wait_softmax(L::B_PF + b, (gn / NSB) & 1);
+                if (n == 0 && n_units_done > 0) wait_softmax(L::B_OE, (n_units_done - 1) & 1);  // O drained
                 tc_fence_after();
                 if (elect_one()) {
                     KTRACE(8, gn);
                     issue_pv(vs, b, n > 0);
-                    mma_commit(bar(L::B_VE + vs));  // V stage free; O includes PV(gn)
-                    if (n == N - 1) mma_commit(bar(L::B_OF));
+                    commit(L::B_VE + vs);  // V stage free; O includes PV(gn)
+                    if (n == N - 1) commit(L::B_OF);
                 }
                 __syncwarp();
                 if (n + NSB < N) issue_s(gn + NSB);  // into the buffer P(gn) just left
@@ -587,6 +683,10 @@ __global__ void __maxnreg__(168)
         const int64_t nq = sg.nq;
         const bool merge = p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST;
         const bool to_acc = p.mode == CDSP_ATTN_FIRST || p.mode == CDSP_ATTN_MID;
+        auto arrive_leader = [&](int b) {  // lane 0, after the warp's tcgen05 ops are fenced
+            if constexpr (PAIR) mbar_arrive_remote(lbar(b));
+            else mbar_arrive(bar(b));
+        };
         int gn0 = 0, n_units_done = 0;
         for (int i = 0;; ++i) {
             const int ub = i & 1;
@@ -594,10 +694,12 @@ __global__ void __maxnreg__(168)
             const UnitInfo u = uinfo[ub];
             if (u.x < 0) break;
             const int N = u.n_used;
-            const int head = u.x / p.n_rb;
-            const int64_t row = static_cast<int64_t>(p.n_rb - 1 - u.x % p.n_rb) * BM + r;
+            int head;
+            int64_t row0;
+            unit_rows(u.x, crank, head, row0);
+            const int64_t row = row0 + r;
             const bool row_ok = row < nq;
-            const uint8_t* sched = smem + L::OFF_SCHED + ub * kSchedMax;
+            const uint16_t* list = reinterpret_cast<const uint16_t*>(smem + L::OFF_SCHED) + ub * L::LISTMAX;
             const int64_t* qp = reinterpret_cast<const int64_t*>(smem + L::OFF_QP) + ub * BM;
             float lse_a = -INFINITY;  // issued early: only needed in the epilogue
             if (merge && row_ok) lse_a = p.lse_acc[static_cast<size_t>(head) * nq + row];
@@ -605,19 +707,13 @@ __global__ void __maxnreg__(168)
             float m = -INFINITY;       // m(n) of the last tile this thread has seen
             float m_used = -INFINITY;  // max that this group's l is relative to
             float2 lacc = make_float2(0.f, 0.f);
-            // this group's tiles: local n with (gn0 + n) & 1 == g; jc = KV tile index of tile n
-            auto next_used = [&](int jj) {
-                ++jj;
-                while (jj < u.j_hi && sched[jj] == 0) ++jj;
-                return jj;
-            };
+            // this group's tiles: local n with (gn0 + n) & 1 == g
             const int n_first = (g - gn0) & 1;
-            int jc = u.j_lo;
-            if (n_first == 1 && N > 1) jc = next_used(jc);
-            for (int n = n_first; n < N; n += 2, jc = next_used(next_used(jc))) {
+            for (int n = n_first; n < N; n += 2) {
                 const int gn = gn0 + n;
-                const int j = jc;
-                const int kind = sched[j];
+                const uint32_t e = list[n];
+                const int j = static_cast<int>(e & ~kPartialBit);
+                const bool partial = (e & kPartialBit) != 0;
                 const int b = gn % NSB;
                 const uint32_t tS = tmem + lane_off + col_s(b);
                 if (lane == 0 && quad == 0) KTRACE(12 + g, gn);
@@ -630,7 +726,7 @@ __global__ void __maxnreg__(168)
                 named_bar_arrive(2 + (gn & 1), 2 * BM);
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar(L::B_PF + b));
+                if (lane == 0) arrive_leader(L::B_PF + b);
                 continue;
 #endif
                 // 64 score registers: columns 64-127 first (max only), then 0-63 (max, kept for the
@@ -643,9 +739,8 @@ __global__ void __maxnreg__(168)
                 reg_tie32(s);
                 reg_tie32(s + 32);
 #ifdef CDSP_KTRACE
-                if (r == 0 && n == 0) UNIT_STAMP(u.x, 5, gtime_ns());
+                if (r == 0 && n == 0) UNIT_STAMP(u.x * CL + crank, 5, gtime_ns());
 #endif
-                const bool partial = kind == TILE_PARTIAL;
                 if (partial) mask_cols<2>(s, sg, j, qp[r], 64);
                 const float mx_hi = max64(s);
                 tmem_ld32p(tS, s);
@@ -684,11 +779,16 @@ __global__ void __maxnreg__(168)
                 msh[(gn & 1) * BM + r] = m;
                 __threadfence_block();
                 named_bar_arrive(2 + (gn & 1), 2 * BM);
+                // the exponentials below must not be hoisted above the arrive (the other group
+                // waits for m(n)): tie their inputs to a volatile asm after it
+                reg_tie32(s);
+                reg_tie32(s + 32);
+                asm volatile("" : "+f"(m));
 #if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 1
                 // debug: S read + row max only, no exponentials / P stores
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar(L::B_PF + b));
+                if (lane == 0) arrive_leader(L::B_PF + b);
                 continue;
 #endif
                 // this group's row sum follows m
@@ -718,13 +818,13 @@ __global__ void __maxnreg__(168)
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar(L::B_PF + b));
+                if (lane == 0) arrive_leader(L::B_PF + b);
                 if (lane == 0 && quad == 0) KTRACE(4 * g + 3, gn);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(L::B_UE + ub));  // done with the unit's schedule / positions
 #ifdef CDSP_KTRACE
-            if (r == 0 && g == 0) UNIT_STAMP(u.x, 6, gtime_ns());
+            if (r == 0 && g == 0) UNIT_STAMP(u.x * CL + crank, 6, gtime_ns());
 #endif
             if (N == 0 && p.mode == CDSP_ATTN_MID) continue;  // merging an empty block is the identity
 
@@ -756,7 +856,7 @@ __global__ void __maxnreg__(168)
                 if constexpr (HD == 128) reg_tie32(o + 32);
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar(L::B_OE));
+                if (lane == 0) arrive_leader(L::B_OE);
                 gn0 += N;
                 ++n_units_done;
             } else {
@@ -812,10 +912,11 @@ __global__ void __maxnreg__(168)
                 const unsigned long long t = gtime_ns();
                 unsigned smid;
                 asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-                UNIT_STAMP(u.x, 7, t);
-                UNIT_STAMP(u.x, 1, t);
-                UNIT_STAMP(u.x, 2, smid);
-                UNIT_STAMP(u.x, 3, N);
+                const int ux = u.x * CL + crank;
+                UNIT_STAMP(ux, 7, t);
+                UNIT_STAMP(ux, 1, t);
+                UNIT_STAMP(ux, 2, smid);
+                UNIT_STAMP(ux, 3, N);
             }
 #endif
         }
@@ -823,14 +924,16 @@ __global__ void __maxnreg__(168)
 
     // ---- teardown
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) cluster_sync_all();  // no remote arrive / DSMEM access into a CTA that exits
+    else __syncthreads();
     if (warp == W_MMA) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        if constexpr (PAIR) tmem_dealloc2(tmem, 512);
+        else tmem_dealloc(tmem, 512);
     }
     if (threadIdx.x == 0) {  // the last CTA out re-arms the unit counter for a later launch
         __threadfence();
-        if (atomicAdd(p.claim + 1, 1) == G - 1) {
+        if (atomicAdd(p.claim + 1, 1) == static_cast<int>(gridDim.x) - 1) {
             atomicExch(p.claim, 0);
             atomicExch(p.claim + 1, 0);
         }
@@ -855,7 +958,7 @@ EncodeTiledFn get_encode_fn() {
 }
 
 // [T, H, D] bf16 tensor, box = 128 rows x 1 head x 64 d, 128-byte swizzle.
-cdsp_status make_map(CUtensorMap* m, const void* base, int64_t T, int H, int D) {
+cdsp_status make_map(CUtensorMap* m, const void* base, int64_t T, int H, int D, int box_rows = 128) {
     EncodeTiledFn enc = get_encode_fn();
     CDSP_REQUIRE(enc != nullptr, CDSP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     CDSP_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15u) == 0, CDSP_ERR_INVALID,
@@ -863,7 +966,7 @@ cdsp_status make_map(CUtensorMap* m, const void* base, int64_t T, int H, int D) 
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(H),
                           static_cast<cuuint64_t>(T > 0 ? T : 1)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(H) * D * 2};
-    cuuint32_t box[3] = {64, 1, 128};
+    cuuint32_t box[3] = {64, 1, static_cast<cuuint32_t>(box_rows)};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -899,23 +1002,42 @@ int sm_count() {
     return n[dev];
 }
 
-template <int HD>
+template <int HD, bool PAIR>
 cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
-    using Lt = Layout<HD>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        CDSP_CUDA(cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lt::SMEM));
-        attr_set = true;
+    using Lt = Layout<HD, PAIR>;
+    auto kern = attn_tc_kernel<HD, PAIR>;
+    static int max_groups = 0;  // co-resident CTA groups (PAIR: clusters of 2 need 2 SMs of one GPC)
+    if (max_groups == 0) {
+        CDSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lt::SMEM));
+        if (PAIR) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(2 * sm_count(), 1, 1);
+            cfg.blockDim = dim3(kThreads, 1, 1);
+            cfg.dynamicSmemBytes = Lt::SMEM;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int n = 0;
+            CDSP_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+            max_groups = n > 0 ? n : sm_count() / 2;
+        } else {
+            max_groups = sm_count();
+        }
     }
-    CDSP_REQUIRE((a.seg.nkv + BN - 1) / BN <= kSchedMax, CDSP_ERR_CAPACITY, "KV block of %lld rows exceeds %d",
-                 static_cast<long long>(a.seg.nkv), kSchedMax * BN);
+    CDSP_REQUIRE((a.seg.nkv + BN - 1) / BN <= Lt::LISTMAX, CDSP_ERR_CAPACITY, "KV block of %lld rows exceeds %d",
+                 static_cast<long long>(a.seg.nkv), Lt::LISTMAX * BN);
     TcParams p;
     p.seg = a.seg;
     p.Hq = a.Hq;
     p.Hkv = a.Hkv;
     p.g = a.Hq / a.Hkv;
     p.n_rb = static_cast<int>((a.seg.nq + BM - 1) / BM);
-    const int64_t units = static_cast<int64_t>(p.n_rb) * a.Hq;
+    p.n_pb = PAIR ? (p.n_rb + 1) / 2 : p.n_rb;
+    const int64_t units = static_cast<int64_t>(p.n_pb) * a.Hq;
     if (units == 0) return CDSP_OK;
     CDSP_REQUIRE(units < (1ll << 30), CDSP_ERR_SHAPE, "too many query tiles");
     p.n_units = static_cast<int>(units);
@@ -930,12 +1052,24 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     CDSP_CHECK_STATUS(make_map(&mq, a.q, a.seg.nq, a.Hq, HD));
     const void* kb = a.seg.nkv > 0 ? a.k : a.q;  // nkv == 0: map never dereferenced
     const void* vb = a.seg.nkv > 0 ? a.v : a.q;
-    CDSP_CHECK_STATUS(make_map(&mk, kb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD));
+    // PAIR: each CTA loads 64 of a K tile's 128 keys (and 64 of V's 128 d columns)
+    CDSP_CHECK_STATUS(make_map(&mk, kb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD, PAIR ? BN / 2 : BN));
     CDSP_CHECK_STATUS(make_map(&mv, vb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD));
     // persistent: one CTA per SM (TMEM and shared memory admit one), units claimed dynamically
-    const int grid = static_cast<int>(units < sm_count() ? units : sm_count());
-    attn_tc_kernel<HD><<<grid, kThreads, Lt::SMEM, st>>>(mq, mk, mv, p);
-    CDSP_CUDA(cudaGetLastError());
+    const int groups = static_cast<int>(units < max_groups ? units : max_groups);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = PAIR ? 2 : 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(static_cast<unsigned>(groups * (PAIR ? 2 : 1)), 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = Lt::SMEM;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = PAIR ? 1 : 0;
+    CDSP_CUDA(cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, p));
 #ifdef CDSP_KTRACE
     if (const char* path = getenv("CDSP_TRACE")) {  // debug builds only: synchronous dump
         static unsigned long long c[65536 * 8], it[4 * 512 * 16];
@@ -955,8 +1089,13 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
 }  // namespace
 
 cdsp_status launch_attention_tc(const AttnArgs& a, cudaStream_t st) {
-    if (a.D == 128) return launch_tc<128>(a, st);
-    if (a.D == 64) return launch_tc<64>(a, st);
+#ifndef CDSP_NO_PAIR
+    static const bool no_pair = getenv("CDSP_ATTN_1SM") != nullptr;  // measurement control: 1-SM kernel
+#else
+    const bool no_pair = true;
+#endif
+    if (a.D == 128) return no_pair ? launch_tc<128, false>(a, st) : launch_tc<128, true>(a, st);
+    if (a.D == 64) return launch_tc<64, false>(a, st);
     CDSP_FAIL(CDSP_ERR_SHAPE, "head dim %d not supported (64 or 128)", a.D);
 }
 
