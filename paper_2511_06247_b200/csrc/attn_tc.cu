@@ -101,24 +101,29 @@ struct Layout {
     static constexpr int TILE = kBox * NBOX;            // one 128-row tile of Q (this CTA's rows)
     static constexpr int KTILE = PAIR ? TILE / 2 : TILE;  // this CTA's part of a K tile
     static constexpr int VTILE = PAIR ? TILE / 2 : TILE;  // this CTA's part of a V tile
-    static constexpr int KST = 3, VST = PAIR ? 4 : CDSP_VST;  // KST == NSB: K stage n%3 is free once S(n) is
+    static constexpr int KST = 3, VST = PAIR ? 3 : CDSP_VST;  // KST == NSB: K stage n%3 is free once S(n) is
+    static constexpr int QST = PAIR ? 2 : 1;  // Q buffers: the next unit's Q lands under this unit's tail
     static constexpr int OFF_Q = 0;
-    static constexpr int OFF_K = OFF_Q + TILE;
+    static constexpr int OFF_K = OFF_Q + QST * TILE;
     static constexpr int OFF_V = OFF_K + KST * KTILE;
-    static constexpr int OFF_M = OFF_V + VST * VTILE;      // running row max m(n): [2 tile parity][128] float
+    // PAIR: bf16 output staging, 128 rows x 64 columns (128B-swizzled) per softmax group, TMA-stored
+    static constexpr int STG = PAIR ? 2 * BM * 128 : 0;
+    static constexpr int OFF_STG = OFF_V + VST * VTILE;
+    static constexpr int OFF_M = OFF_STG + STG;            // running row max m(n): [2 tile parity][128] float
     static constexpr int OFF_L = OFF_M + 2 * BM * 4;       // epilogue (m_used, l): [2 unit parity][2 groups][128] float2
     static constexpr int OFF_QP = OFF_L + 4 * BM * 8;      // query position per row: [2 unit buffer][128] int64
     static constexpr int OFF_BAR = OFF_QP + 2 * BM * 8;
-    // Local: u_full[2] (unit buffer published), u_empty[2] (read by every consumer), s_full[NSB],
-    // v_empty[VST], o_full (the last three arrive by MMA commit, multicast to both CTAs of a pair).
-    // Leader (the even CTA; the only one in a 1-SM launch): q_full, k_full[KST], v_full[VST]
+    // Local: u_full[2] (unit buffer published), u_empty[2] (read by every consumer), q_empty[2],
+    // s_full[NSB], v_empty[VST], o_full (the last four arrive by MMA commit, multicast to both
+    // CTAs of a pair).
+    // Leader (the even CTA; the only one in a 1-SM launch): q_full[2], k_full[KST], v_full[VST]
     // (TMA bytes of both CTAs), p_full[NSB], o_free (softmax warps of both CTAs).
     // Pair bookkeeping: c_full[2] (odd CTA: next unit id arrived), c_empty[2] (even CTA: consumed).
     // (m(n) goes from one softmax group to the other through named barriers 2, 3.)  Every
     // tcgen05.commit costs the tensor pipe ~30 clk (tools/mma_pattern.cu), so each MMA group
     // commits once: s_full[b] (S(n) done) also frees K stage n % 3 (and, for a unit's last
     // tile, the Q buffer); v_empty[s] (PV(n) done) also tells a rescaling group that O is stable.
-    static constexpr int B_UF = 0, B_UE = 2, B_QF = 4, B_KF = 5, B_VF = B_KF + KST, B_VE = B_VF + VST,
+    static constexpr int B_UF = 0, B_UE = 2, B_QF = 4, B_QE = 6, B_KF = 8, B_VF = B_KF + KST, B_VE = B_VF + VST,
                          B_SF = B_VE + VST, B_PF = B_SF + NSB, B_OF = B_PF + NSB, B_OE = B_OF + 1, B_CF = B_OE + 1,
                          B_CE = B_CF + 2, NBAR = B_CE + 2;
     static_assert(KST == NSB, "K stages are released through s_full");
@@ -126,7 +131,7 @@ struct Layout {
     static constexpr int OFF_CLAIM = OFF_TMEM_SLOT + 8;     // [2] next unit id (odd CTA of a pair)
     static constexpr int OFF_UNIT = OFF_CLAIM + 8;          // [2] x {unit, n_used}
     // [2][LISTMAX] used KV tiles of the unit in order: tile index | 0x8000 if partial
-    static constexpr int LISTMAX = (PAIR || HD == 64) ? kSchedMax : kSchedMax / 2;
+    static constexpr int LISTMAX = HD == 64 ? kSchedMax : kSchedMax / 2;
     static constexpr int OFF_SCHED = OFF_UNIT + 2 * 16;
     static constexpr int SMEM = OFF_SCHED + 2 * LISTMAX * 2 + 1024;  // + alignment slack
 };
@@ -351,7 +356,8 @@ constexpr uint16_t kPartialBit = 0x8000;
 template <int HD, bool PAIR>
 __global__ void __maxnreg__(168)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                   const __grid_constant__ CUtensorMap tm_v, const TcParams p) {
+                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_out,
+                   const TcParams p) {
     using L = Layout<HD, PAIR>;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
@@ -388,7 +394,10 @@ __global__ void __maxnreg__(168)
                 mbar_init(bar(L::B_CF + i), 1);
                 mbar_init(bar(L::B_CE + i), 1);
             }
-            mbar_init(bar(L::B_QF), 1);
+            for (int i = 0; i < 2; ++i) {
+                mbar_init(bar(L::B_QF + i), 1);
+                mbar_init(bar(L::B_QE + i), 1);
+            }
             for (int i = 0; i < L::KST; ++i) mbar_init(bar(L::B_KF + i), 1);
             for (int i = 0; i < L::VST; ++i) {
                 mbar_init(bar(L::B_VF + i), 1);
@@ -404,6 +413,7 @@ __global__ void __maxnreg__(168)
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
+            if (PAIR) tma_prefetch_desc(&tm_out);
         }
     } else if (warp == W_MMA) {
         if constexpr (PAIR) {
@@ -430,7 +440,6 @@ __global__ void __maxnreg__(168)
         int x_pre = 0;  // leader lane 0: the unit after x, claimed one unit ahead
         if (leader && lane == 0) x_pre = G + atomicAdd(p.claim, 1);
         int it = 0;        // used tiles loaded so far (all units)
-        int last_gn = -1;  // the previous non-empty unit's last tile: its S frees the Q buffer
         int n_ne = 0;      // non-empty units so far
         int* claim_slot = reinterpret_cast<int*>(smem + L::OFF_CLAIM);
         for (int i = 0;; ++i) {
@@ -493,15 +502,19 @@ __global__ void __maxnreg__(168)
             __syncwarp();
             if (lane == 0) mbar_arrive(bar(L::B_UF + ub));  // publish (release)
             if (cnt > 0) {
-                if (last_gn >= 0) mbar_wait(bar(L::B_SF + last_gn % NSB), (last_gn / NSB) & 1);  // Q buffer free
+                // Q buffer qb is free once the last S of the unit that used it (n_ne - QST) is done
+                const int qb = n_ne % L::QST;
+                if (n_ne >= L::QST) mbar_wait(bar(L::B_QE + qb), ((n_ne - L::QST) / L::QST) & 1);
                 if (lane == 0) {
                     UNIT_STAMP(x * CL + crank, 0, gtime_ns());
-                    if (leader) mbar_expect_tx(bar(L::B_QF), CL * L::TILE);
+                    if (leader) mbar_expect_tx(bar(L::B_QF + qb), CL * L::TILE);
+                    const uint32_t dst = sQ + qb * L::TILE;
                     for (int b = 0; b < L::NBOX; ++b) {
                         if constexpr (PAIR)
-                            tma_load_3d_2sm(sQ + b * kBox, &tm_q, lbar(L::B_QF), b * 64, head, static_cast<int>(row0), pol_q);
+                            tma_load_3d_2sm(dst + b * kBox, &tm_q, lbar(L::B_QF + qb), b * 64, head, static_cast<int>(row0),
+                                            pol_q);
                         else
-                            tma_load_3d(sQ + b * kBox, &tm_q, bar(L::B_QF), b * 64, head, static_cast<int>(row0));
+                            tma_load_3d(dst + b * kBox, &tm_q, bar(L::B_QF + qb), b * 64, head, static_cast<int>(row0));
                     }
                 }
                 // merge modes: pull this unit's accumulator rows into L2 for the epilogue
@@ -540,7 +553,6 @@ __global__ void __maxnreg__(168)
                 __syncwarp();
                 ++it;
             }
-            if (cnt > 0) last_gn = it - 1;
             x = __shfl_sync(0xFFFFFFFFu, x_pre, 0);
             if (leader && lane == 0) {
                 if (x < p.n_units) x_pre = G + atomicAdd(p.claim, 1);
@@ -591,7 +603,8 @@ __global__ void __maxnreg__(168)
         constexpr uint32_t idesc_qk = idesc_bf16_f32(BM * CL, BN, false, false);
         constexpr uint32_t idesc_pv = idesc_bf16_f32(BM * CL, HD, false, true);
         constexpr uint32_t KBOX = PAIR ? kBox / 2 : kBox;  // bytes of one 64-column box of a K stage
-        const uint64_t dq = umma_desc_sw128(sQ, 16, 1024);
+        const uint64_t dq0 = umma_desc_sw128(sQ, 16, 1024);
+        uint64_t dq = dq0;
         const uint64_t dk0 = umma_desc_sw128(sK, 16, 1024);
         const uint64_t dv0 = umma_desc_sw128(sV, kBox, 1024);
         auto commit = [&](int b) {
@@ -623,7 +636,7 @@ __global__ void __maxnreg__(168)
                            idesc_pv, (acc || kk > 0) ? 1u : 0u);
             }
         };
-        auto issue_s = [&](int gn) {  // S(gn) into buffer gn % NSB; K stage gn % KST
+        auto issue_s = [&](int gn, int q_release) {  // S(gn) into buffer gn % NSB; K stage gn % KST
             const int ks = gn % L::KST;
             MMA_WAIT(bar(L::B_KF + ks), (gn / L::KST) & 1);
             tc_fence_after();
@@ -631,6 +644,7 @@ __global__ void __maxnreg__(168)
                 KTRACE(9, gn);
                 issue_qk(ks, gn % NSB);
                 commit(L::B_SF + gn % NSB);  // S(gn) ready; K stage ks free
+                if (q_release >= 0) commit(L::B_QE + q_release);  // the unit's last S: Q buffer free
             }
             __syncwarp();
         };
@@ -645,11 +659,13 @@ __global__ void __maxnreg__(168)
             if (u.x < 0) break;
             const int N = u.n_used;
             if (N == 0 || !leader) continue;
-            MMA_WAIT(bar(L::B_QF), n_units_done & 1);  // Q tile(s) landed
+            const int qb = n_units_done % L::QST;
+            MMA_WAIT(bar(L::B_QF + qb), (n_units_done / L::QST) & 1);  // Q tile(s) landed
             tc_fence_after();
+            dq = dq0 + static_cast<uint64_t>((qb * L::TILE) >> 4);
             // this unit's first S tiles go in only after the previous unit's last PV: its
             // buffers are the ones those PVs read
-            for (int n = 0; n < NSB && n < N; ++n) issue_s(gn0 + n);
+            for (int n = 0; n < NSB && n < N; ++n) issue_s(gn0 + n, n == N - 1 ? qb : -1);
             for (int n = 0; n < N; ++n) {
                 const int gn = gn0 + n;
                 const int b = gn % NSB, vs = gn % L::VST;
@@ -666,7 +682,7 @@ __global__ void __maxnreg__(168)
                     if (n == N - 1) commit(L::B_OF);
                 }
                 __syncwarp();
-                if (n + NSB < N) issue_s(gn + NSB);  // into the buffer P(gn) just left
+                if (n + NSB < N) issue_s(gn + NSB, n + NSB == N - 1 ? qb : -1);  // into the buffer P(gn) just left
             }
             gn0 += N;
             ++n_units_done;
@@ -831,6 +847,11 @@ __global__ void __maxnreg__(168)
             // ---------------- epilogue: normalise, then write / LSE-merge (R3) ----------------
             float l = 0.f;
             uint32_t o[HD / 2];  // this group's O columns [g HD/2, (g+1) HD/2)
+            // PAIR, bf16 result: rows go through the swizzled staging box of this group and one
+            // TMA store (a thread-per-row global store touches 32 rows per warp instruction)
+            const bool staged = PAIR && N > 0 && !to_acc;
+            const uint32_t stg = sbase + L::OFF_STG + static_cast<uint32_t>(g) * (BM * 128);
+            if (staged && threadIdx.x == static_cast<unsigned>(g * BM)) bulk_wait_read0();  // previous store read the box
             if (N > 0) {
                 // final m = m(last); combine the two groups' row sums relative to it
                 const int last = gn0 + N - 1;
@@ -868,7 +889,42 @@ __global__ void __maxnreg__(168)
             float wa = 0.f, wb = 1.f, lse_out = lse_b;
             if (merge) merge_weights(lse_a, lse_b, wa, wb, lse_out);
             const float sbw = wb * inv_l;
-            if (row_ok) {
+            if (staged) {
+                const size_t orow = (static_cast<size_t>(row_ok ? row : 0) * p.Hq + head) * HD + (HD / 2) * g;
+                const uint32_t rsw = static_cast<uint32_t>(r & 7), rowa = stg + static_cast<uint32_t>(r) * 128;
+#pragma unroll
+                for (int c = 0; c < HD / 64; ++c) {
+                    float v[32];
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(o[32 * c + q]) * sbw;
+                    if (merge && row_ok) {
+                        const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 av = a4[q];
+                            v[4 * q + 0] = fmaf(wa, av.x, v[4 * q + 0]);
+                            v[4 * q + 1] = fmaf(wa, av.y, v[4 * q + 1]);
+                            v[4 * q + 2] = fmaf(wa, av.z, v[4 * q + 2]);
+                            v[4 * q + 3] = fmaf(wa, av.w, v[4 * q + 3]);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t ch = static_cast<uint32_t>(4 * c + q);  // 16-byte chunk of the 128-byte row
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rowa + ((ch ^ rsw) << 4)),
+                                     "r"(pack_bf16(v[8 * q + 0], v[8 * q + 1])), "r"(pack_bf16(v[8 * q + 2], v[8 * q + 3])),
+                                     "r"(pack_bf16(v[8 * q + 4], v[8 * q + 5])), "r"(pack_bf16(v[8 * q + 6], v[8 * q + 7]))
+                                     : "memory");
+                    }
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(4 + g, BM);  // this group's 128 rows are in the box
+                if (threadIdx.x == static_cast<unsigned>(g * BM)) {
+                    tma_store_3d(&tm_out, stg, (HD / 2) * g, head, static_cast<int>(row0));  // rows >= nq clipped
+                    bulk_commit();
+                }
+                if (row_ok && g == 0 && p.lse) p.lse[static_cast<size_t>(head) * nq + row] = lse_out;
+            } else if (row_ok) {
                 const size_t orow = (static_cast<size_t>(row) * p.Hq + head) * HD + (HD / 2) * g;
 #pragma unroll
                 for (int c = 0; c < HD / 64; ++c) {
@@ -923,6 +979,7 @@ __global__ void __maxnreg__(168)
     }
 
     // ---- teardown
+    if (PAIR && (threadIdx.x == 0 || threadIdx.x == BM)) bulk_wait_all0();  // staged output stores done
     tc_fence_before();
     if constexpr (PAIR) cluster_sync_all();  // no remote arrive / DSMEM access into a CTA that exits
     else __syncthreads();
@@ -1055,6 +1112,9 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     // PAIR: each CTA loads 64 of a K tile's 128 keys (and 64 of V's 128 d columns)
     CDSP_CHECK_STATUS(make_map(&mk, kb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD, PAIR ? BN / 2 : BN));
     CDSP_CHECK_STATUS(make_map(&mv, vb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD));
+    CUtensorMap mo = mq;  // bf16 output (staged epilogue); never dereferenced in fp32-result modes
+    if (PAIR && (a.mode == CDSP_ATTN_ONLY || a.mode == CDSP_ATTN_LAST))
+        CDSP_CHECK_STATUS(make_map(&mo, a.out, a.seg.nq, a.Hq, HD));
     // persistent: one CTA per SM (TMEM and shared memory admit one), units claimed dynamically
     const int groups = static_cast<int>(units < max_groups ? units : max_groups);
     cudaLaunchConfig_t cfg = {};
@@ -1069,7 +1129,7 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     cfg.stream = st;
     cfg.attrs = at;
     cfg.numAttrs = PAIR ? 1 : 0;
-    CDSP_CUDA(cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, p));
+    CDSP_CUDA(cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, p));
 #ifdef CDSP_KTRACE
     if (const char* path = getenv("CDSP_TRACE")) {  // debug builds only: synchronous dump
         static unsigned long long c[65536 * 8], it[4 * 512 * 16];
