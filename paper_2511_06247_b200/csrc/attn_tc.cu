@@ -72,6 +72,18 @@
 #define CDSP_VST 2
 #endif
 
+#ifndef CDSP_MAXNREG  // 11 warps: 3 per sub-partition x 168 regs x 32 lanes fills its 16K registers
+#define CDSP_MAXNREG 168
+#endif
+
+#ifndef CDSP_FULL_ROW  // softmax holds the whole 128-score row (else two 64-score halves)
+#define CDSP_FULL_ROW 1
+#endif
+
+#ifndef CDSP_EPI_COALESCED  // fp32 accumulator epilogue through the warp-transpose tiles (PAIR)
+#define CDSP_EPI_COALESCED 1
+#endif
+
 #ifndef CDSP_EMU_MASK
 #define CDSP_EMU_MASK 0x22
 #endif
@@ -353,8 +365,58 @@ struct UnitInfo {
 };
 constexpr uint16_t kPartialBit = 0x8000;
 
+
+// Coalesced fp32 row I/O for a warp's 32 rows x 32 columns (row = lane) through a 4 KB
+// 128B-swizzled shared-memory tile: global traffic moves 4 whole 128-byte row pieces per warp
+// instruction instead of one 16-byte piece of 32 different rows.  base: row 0, first column;
+// rows >= nvalid do not exist (read as 0, not written).
+__device__ __forceinline__ void warp_rows_load(float (&a)[32], const float* base, size_t rstride, int nvalid,
+                                               uint32_t tile, int lane) {
+    float4 x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int rr = 4 * k + (lane >> 3), ch = lane & 7;
+        x[k] = rr < nvalid ? *reinterpret_cast<const float4*>(base + rr * rstride + ch * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int rr = 4 * k + (lane >> 3), ch = lane & 7;
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(tile + rr * 128 + ((ch ^ (rr & 7)) << 4)),
+                     "f"(x[k].x), "f"(x[k].y), "f"(x[k].z), "f"(x[k].w)
+                     : "memory");
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(a[4 * j]), "=f"(a[4 * j + 1]), "=f"(a[4 * j + 2]), "=f"(a[4 * j + 3])
+                     : "r"(tile + lane * 128 + ((j ^ (lane & 7)) << 4))
+                     : "memory");
+    __syncwarp();
+}
+__device__ __forceinline__ void warp_rows_store(const uint32_t* v, float* base, size_t rstride, int nvalid, uint32_t tile,
+                                                int lane) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(tile + lane * 128 + ((j ^ (lane & 7)) << 4)),
+                     "r"(v[4 * j]), "r"(v[4 * j + 1]), "r"(v[4 * j + 2]), "r"(v[4 * j + 3])
+                     : "memory");
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int rr = 4 * k + (lane >> 3), ch = lane & 7;
+        float4 x;
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                     : "r"(tile + rr * 128 + ((ch ^ (rr & 7)) << 4))
+                     : "memory");
+        if (rr < nvalid) *reinterpret_cast<float4*>(base + rr * rstride + ch * 4) = x;
+    }
+    __syncwarp();
+}
+
 template <int HD, bool PAIR>
-__global__ void __maxnreg__(168)
+__global__ void __maxnreg__(CDSP_MAXNREG)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_out,
                    const TcParams p) {
@@ -748,15 +810,27 @@ __global__ void __maxnreg__(168)
                 // 64 score registers: columns 64-127 first (max only), then 0-63 (max, kept for the
                 // exponentials); 64-127 are re-read from TMEM for their exponentials (P(n) only ever
                 // overwrites S columns 0-63)
+#if CDSP_FULL_ROW
+                // the whole score row in registers: one TMEM round trip, no re-reads
+                uint32_t s[128];
+                tmem_ld32p(tS, s);
+                tmem_ld32p(tS + 32, s + 32);
+                tmem_ld32p(tS + 64, s + 64);
+                tmem_ld32p(tS + 96, s + 96);
+                tc_wait_ld();
+                reg_tie32(s);
+                reg_tie32(s + 32);
+                reg_tie32(s + 64);
+                reg_tie32(s + 96);
+                if (partial) mask_cols<4>(s, sg, j, qp[r], 0);
+                const float mx = fmaxf(max64(s), max64(s + 64)) * sl2;
+#else
                 uint32_t s[64];
                 tmem_ld32p(tS + 64, s);
                 tmem_ld32p(tS + 96, s + 32);
                 tc_wait_ld();
                 reg_tie32(s);
                 reg_tie32(s + 32);
-#ifdef CDSP_KTRACE
-                if (r == 0 && n == 0) UNIT_STAMP(u.x * CL + crank, 5, gtime_ns());
-#endif
                 if (partial) mask_cols<2>(s, sg, j, qp[r], 64);
                 const float mx_hi = max64(s);
                 tmem_ld32p(tS, s);
@@ -766,6 +840,10 @@ __global__ void __maxnreg__(168)
                 reg_tie32(s + 32);
                 if (partial) mask_cols<2>(s, sg, j, qp[r], 0);
                 const float mx = fmaxf(mx_hi, max64(s)) * sl2;
+#endif
+#ifdef CDSP_KTRACE
+                if (r == 0 && n == 0) UNIT_STAMP(u.x * CL + crank, 5, gtime_ns());
+#endif
                 // ---- the serial link: m(n) = lazy max(m(n-1), rowmax(S(n))) ----
                 if (n > 0) {  // m(n-1) from the other group (named barrier 2 + parity: 128 + 128 threads)
                     named_bar_sync(2 + ((gn - 1) & 1), 2 * BM);
@@ -799,6 +877,10 @@ __global__ void __maxnreg__(168)
                 // waits for m(n)): tie their inputs to a volatile asm after it
                 reg_tie32(s);
                 reg_tie32(s + 32);
+#if CDSP_FULL_ROW
+                reg_tie32(s + 64);
+                reg_tie32(s + 96);
+#endif
                 asm volatile("" : "+f"(m));
 #if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 1
                 // debug: S read + row max only, no exponentials / P stores
@@ -818,6 +900,12 @@ __global__ void __maxnreg__(168)
                 const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m_use, -m_use);
                 // keys 0-63 from registers -> P columns 0-31; keys 64-127 re-read in two pieces,
                 // each load in flight behind the previous piece's exponentials
+#if CDSP_FULL_ROW
+                exp32_store(s, sc, nm, lacc, tS);
+                exp32_store(s + 32, sc, nm, lacc, tS + 16);
+                exp32_store(s + 64, sc, nm, lacc, tS + 32);
+                exp32_store(s + 96, sc, nm, lacc, tS + 48);
+#else
                 exp32_store(s, sc, nm, lacc, tS);
                 tmem_ld32p(tS + 64, s);
                 exp32_store(s + 32, sc, nm, lacc, tS + 16);
@@ -830,6 +918,7 @@ __global__ void __maxnreg__(168)
                 reg_tie32(s + 32);
                 if (partial) mask_cols<1>(s + 32, sg, j, qp[r], 96);
                 exp32_store(s + 32, sc, nm, lacc, tS + 48);
+#endif
                 if (lane == 0 && quad == 0) KTRACE(4 * g + 2, gn);
                 tc_wait_st();
                 tc_fence_before();
@@ -849,7 +938,7 @@ __global__ void __maxnreg__(168)
             uint32_t o[HD / 2];  // this group's O columns [g HD/2, (g+1) HD/2)
             // PAIR, bf16 result: rows go through the swizzled staging box of this group and one
             // TMA store (a thread-per-row global store touches 32 rows per warp instruction)
-            const bool staged = PAIR && N > 0 && !to_acc;
+            const bool staged = PAIR && N > 0 && !to_acc;  // TMA-stored bf16 (the box also serves as scratch)
             const uint32_t stg = sbase + L::OFF_STG + static_cast<uint32_t>(g) * (BM * 128);
             if (staged && threadIdx.x == static_cast<unsigned>(g * BM)) bulk_wait_read0();  // previous store read the box
             if (N > 0) {
@@ -889,41 +978,49 @@ __global__ void __maxnreg__(168)
             float wa = 0.f, wb = 1.f, lse_out = lse_b;
             if (merge) merge_weights(lse_a, lse_b, wa, wb, lse_out);
             const float sbw = wb * inv_l;
-            if (staged) {
-                const size_t orow = (static_cast<size_t>(row_ok ? row : 0) * p.Hq + head) * HD + (HD / 2) * g;
-                const uint32_t rsw = static_cast<uint32_t>(r & 7), rowa = stg + static_cast<uint32_t>(r) * 128;
+            if (PAIR && N > 0 && (CDSP_EPI_COALESCED || !to_acc)) {
+                // this warp's 32 rows: its 4 KB slice of the group's staging box (scratch for the
+                // coalesced fp32 accumulator I/O; for bf16 results also the rows of the TMA box)
+                const uint32_t wtile = stg + static_cast<uint32_t>(quad) * (32 * 128);
+                const int64_t wrow0 = row0 + 32 * quad;
+                const int nvalid = static_cast<int>(nq - wrow0 < 32 ? (nq - wrow0 > 0 ? nq - wrow0 : 0) : 32);
+                float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + (HD / 2) * g;
+                const size_t rstride = static_cast<size_t>(p.Hq) * HD;
 #pragma unroll
                 for (int c = 0; c < HD / 64; ++c) {
-                    float v[32];
+                    float a[32];
+                    if (merge) warp_rows_load(a, acc_w + 32 * c, rstride, nvalid, wtile, lane);
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(o[32 * c + q]) * sbw;
-                    if (merge && row_ok) {
-                        const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float4 av = a4[q];
-                            v[4 * q + 0] = fmaf(wa, av.x, v[4 * q + 0]);
-                            v[4 * q + 1] = fmaf(wa, av.y, v[4 * q + 1]);
-                            v[4 * q + 2] = fmaf(wa, av.z, v[4 * q + 2]);
-                            v[4 * q + 3] = fmaf(wa, av.w, v[4 * q + 3]);
-                        }
+                    for (int q = 0; q < 32; ++q) {
+                        float v = __uint_as_float(o[32 * c + q]) * sbw;
+                        if (merge) v = fmaf(wa, a[q], v);
+                        o[32 * c + q] = __float_as_uint(v);
                     }
+                }
+                if (to_acc) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t ch = static_cast<uint32_t>(4 * c + q);  // 16-byte chunk of the 128-byte row
-                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rowa + ((ch ^ rsw) << 4)),
-                                     "r"(pack_bf16(v[8 * q + 0], v[8 * q + 1])), "r"(pack_bf16(v[8 * q + 2], v[8 * q + 3])),
-                                     "r"(pack_bf16(v[8 * q + 4], v[8 * q + 5])), "r"(pack_bf16(v[8 * q + 6], v[8 * q + 7]))
+                    for (int c = 0; c < HD / 64; ++c) warp_rows_store(o + 32 * c, acc_w + 32 * c, rstride, nvalid, wtile, lane);
+                    if (row_ok && g == 0) p.lse_acc[static_cast<size_t>(head) * nq + row] = lse_out;
+                } else {
+                    const uint32_t rsw = static_cast<uint32_t>(r & 7), rowa = stg + static_cast<uint32_t>(r) * 128;
+#pragma unroll
+                    for (int q = 0; q < HD / 16; ++q) {  // 16-byte chunk q of the 128-byte row
+                        const uint32_t* w = o + 8 * q;
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rowa + ((static_cast<uint32_t>(q) ^ rsw) << 4)),
+                                     "r"(pack_bf16(__uint_as_float(w[0]), __uint_as_float(w[1]))),
+                                     "r"(pack_bf16(__uint_as_float(w[2]), __uint_as_float(w[3]))),
+                                     "r"(pack_bf16(__uint_as_float(w[4]), __uint_as_float(w[5]))),
+                                     "r"(pack_bf16(__uint_as_float(w[6]), __uint_as_float(w[7])))
                                      : "memory");
                     }
+                    fence_proxy_async_smem();
+                    named_bar_sync(4 + g, BM);  // this group's 128 rows are in the box
+                    if (threadIdx.x == static_cast<unsigned>(g * BM)) {
+                        tma_store_3d(&tm_out, stg, (HD / 2) * g, head, static_cast<int>(row0));  // rows >= nq clipped
+                        bulk_commit();
+                    }
+                    if (row_ok && g == 0 && p.lse) p.lse[static_cast<size_t>(head) * nq + row] = lse_out;
                 }
-                fence_proxy_async_smem();
-                named_bar_sync(4 + g, BM);  // this group's 128 rows are in the box
-                if (threadIdx.x == static_cast<unsigned>(g * BM)) {
-                    tma_store_3d(&tm_out, stg, (HD / 2) * g, head, static_cast<int>(row0));  // rows >= nq clipped
-                    bulk_commit();
-                }
-                if (row_ok && g == 0 && p.lse) p.lse[static_cast<size_t>(head) * nq + row] = lse_out;
             } else if (row_ok) {
                 const size_t orow = (static_cast<size_t>(row) * p.Hq + head) * HD + (HD / 2) * g;
 #pragma unroll

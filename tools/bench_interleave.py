@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--seq", type=int, default=32768)
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--zigzag-only", action="store_true")
     args = ap.parse_args()
     L, H, D = args.seq, args.heads, 128
     dev = torch.device("cuda:0")
@@ -32,7 +33,7 @@ def main():
     flops = 4.0 * D * H * L * (L + 1) / 2
     res = {}
     for s in (2, 4, 8):
-        for il in ("zigzag", "striped"):
+        for il in (("zigzag",) if args.zigzag_only else ("zigzag", "striped")):
             plan = api.Plan([(L, list(range(s)), il)])
             comms = make_loopback_comms(plan, H, D, torch.bfloat16)
             shards = prepare_shards(q, k, v, plan)
