@@ -85,7 +85,7 @@
 #endif
 
 #ifndef CDSP_EMU_MASK
-#define CDSP_EMU_MASK 0x22
+#define CDSP_EMU_MASK 0x02
 #endif
 
 namespace cdsp {
@@ -93,13 +93,18 @@ using namespace ptx;
 
 namespace {
 
-constexpr int kThreads = 352;           // 11 warps
+#ifndef CDSP_NGROUPS  // softmax groups (4 warps each); group g takes the KV tiles n = g (mod NG)
+#define CDSP_NGROUPS 2
+#endif
+constexpr int NG = CDSP_NGROUPS;
+static_assert(NG == 2 || NG == 3, "2 or 3 softmax groups");
+constexpr int kThreads = 32 * (4 * NG + 3);  // softmax groups + K producer + V producer + MMA
 constexpr int BM = 128;                 // query rows per CTA (TMEM lanes)
 constexpr int BN = 128;                 // KV rows per tile
 constexpr int NSB = 3;                  // S/P buffers in TMEM
 constexpr int kBox = 128 * 128;         // TMA box: 128 rows x 64 bf16 (128-byte swizzle rows)
 constexpr int kSchedMax = 8192;         // KV tiles per launch (1M keys)
-constexpr int W_K = 8, W_V = 9, W_MMA = 10;
+constexpr int W_K = 4 * NG, W_V = 4 * NG + 1, W_MMA = 4 * NG + 2;
 
 // PAIR: 2-SM variant (HD = 128).  A CTA pair (cluster of 2) runs M = 256 MMAs (cta_group::2):
 // each CTA holds its own 128 query rows of Q and of S / P / O in its TMEM, and HALF of every
@@ -121,9 +126,10 @@ struct Layout {
     // PAIR: bf16 output staging, 128 rows x 64 columns (128B-swizzled) per softmax group, TMA-stored
     static constexpr int STG = PAIR ? 2 * BM * 128 : 0;
     static constexpr int OFF_STG = OFF_V + VST * VTILE;
-    static constexpr int OFF_M = OFF_STG + STG;            // running row max m(n): [2 tile parity][128] float
-    static constexpr int OFF_L = OFF_M + 2 * BM * 4;       // epilogue (m_used, l): [2 unit parity][2 groups][128] float2
-    static constexpr int OFF_QP = OFF_L + 4 * BM * 8;      // query position per row: [2 unit buffer][128] int64
+    static constexpr int OFF_M = OFF_STG + STG;            // running row max m(n): [NG (tile mod NG)][128] float
+    static constexpr int OFF_L = OFF_M + NG * BM * 4;      // epilogue (m_used, l): [2 unit parity][NG groups][128] float2
+    static constexpr int OFF_ML = OFF_L + 2 * NG * BM * 8;  // epilogue: the unit's final m: [2 unit parity][128] float
+    static constexpr int OFF_QP = OFF_ML + 2 * BM * 4;     // query position per row: [2 unit buffer][128] int64
     static constexpr int OFF_BAR = OFF_QP + 2 * BM * 8;
     // Local: u_full[2] (unit buffer published), u_empty[2] (read by every consumer), q_empty[2],
     // s_full[NSB], v_empty[VST], o_full (the last four arrive by MMA commit, multicast to both
@@ -312,15 +318,23 @@ __device__ __forceinline__ void mask_cols(uint32_t* s, const cdsp_segments& sg, 
     }
 }
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {  // FMNMX3 (sm_100)
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
 __device__ __forceinline__ float max64(const uint32_t* s) {
+    // 8 independent chains over 64 scores: 24 FMNMX3 + 8 FMNMX + a 2-level tree
     float a[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = fmaxf(__uint_as_float(s[2 * k]), __uint_as_float(s[2 * k + 1]));
+    for (int k = 0; k < 8; ++k) a[k] = fmax3(__uint_as_float(s[k]), __uint_as_float(s[8 + k]), __uint_as_float(s[16 + k]));
 #pragma unroll
-    for (int i = 16; i < 64; i += 16)
+    for (int i = 24; i < 56; i += 16)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) a[k] = fmaxf(a[k], fmaxf(__uint_as_float(s[i + 2 * k]), __uint_as_float(s[i + 2 * k + 1])));
-    return fmaxf(fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])), fmaxf(fmaxf(a[4], a[5]), fmaxf(a[6], a[7])));
+        for (int k = 0; k < 8; ++k) a[k] = fmax3(a[k], __uint_as_float(s[i + k]), __uint_as_float(s[i + 8 + k]));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fmaxf(a[k], __uint_as_float(s[56 + k]));
+    return fmax3(fmax3(a[0], a[1], a[2]), fmax3(a[3], a[4], a[5]), fmaxf(a[6], a[7]));
 }
 
 // p = 2^(s*sl2 - m) for 32 scores -> 16 bf16 pairs stored to TMEM columns tP .. tP+15 (two
@@ -452,7 +466,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
         if (lane == 0) {
             for (int i = 0; i < 2; ++i) {
                 mbar_init(bar(L::B_UF + i), 1);
-                mbar_init(bar(L::B_UE + i), 10);  // 8 softmax warps, V producer, MMA warp
+                mbar_init(bar(L::B_UE + i), 4 * NG + 2);  // softmax warps, V producer, MMA warp
                 mbar_init(bar(L::B_CF + i), 1);
                 mbar_init(bar(L::B_CE + i), 1);
             }
@@ -749,7 +763,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             gn0 += N;
             ++n_units_done;
         }
-    } else if (warp < 8) {
+    } else if (warp < 4 * NG) {
         // ========= softmax group g (tiles gn = g, g+2, ... over all units): thread = one query row =========
         const int g = warp >> 2;
         const int quad = warp & 3;  // TMEM lane quadrant
@@ -786,8 +800,8 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             float m_used = -INFINITY;  // max that this group's l is relative to
             float2 lacc = make_float2(0.f, 0.f);
             // this group's tiles: local n with (gn0 + n) & 1 == g
-            const int n_first = (g - gn0) & 1;
-            for (int n = n_first; n < N; n += 2) {
+            const int n_first = ((g - gn0) % NG + NG) % NG;
+            for (int n = n_first; n < N; n += NG) {
                 const int gn = gn0 + n;
                 const uint32_t e = list[n];
                 const int j = static_cast<int>(e & ~kPartialBit);
@@ -800,8 +814,8 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 tc_fence_after();
 #if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 0
                 // debug: MMA pipeline alone (no TMEM traffic from the softmax; results garbage)
-                if (n > 0) named_bar_sync(2 + ((gn - 1) & 1), 2 * BM);
-                named_bar_arrive(2 + (gn & 1), 2 * BM);
+                if (n > 0) named_bar_sync(2 + (gn - 1) % NG, 2 * BM);
+                if (n < N - 1) named_bar_arrive(2 + gn % NG, 2 * BM);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) arrive_leader(L::B_PF + b);
@@ -845,9 +859,9 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 if (r == 0 && n == 0) UNIT_STAMP(u.x * CL + crank, 5, gtime_ns());
 #endif
                 // ---- the serial link: m(n) = lazy max(m(n-1), rowmax(S(n))) ----
-                if (n > 0) {  // m(n-1) from the other group (named barrier 2 + parity: 128 + 128 threads)
-                    named_bar_sync(2 + ((gn - 1) & 1), 2 * BM);
-                    m = msh[((gn - 1) & 1) * BM + r];
+                if (n > 0) {  // m(n-1) from the group of tile n-1 (named barrier 2 + (n-1) mod NG: 128 + 128 threads)
+                    named_bar_sync(2 + (gn - 1) % NG, 2 * BM);
+                    m = msh[((gn - 1) % NG) * BM + r];
                 }
                 const bool need = mx > m + 8.0f;
                 const float m_prev = m;
@@ -870,9 +884,11 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                         tmem_st16(tO + 16 * c, o);
                     }
                 }
-                msh[(gn & 1) * BM + r] = m;
-                __threadfence_block();
-                named_bar_arrive(2 + (gn & 1), 2 * BM);
+                if (n < N - 1) {  // (the unit's last m goes to the epilogue through OFF_ML)
+                    msh[(gn % NG) * BM + r] = m;
+                    __threadfence_block();
+                    named_bar_arrive(2 + gn % NG, 2 * BM);
+                }
                 // the exponentials below must not be hoisted above the arrive (the other group
                 // waits for m(n)): tie their inputs to a volatile asm after it
                 reg_tie32(s);
@@ -938,26 +954,29 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             uint32_t o[HD / 2];  // this group's O columns [g HD/2, (g+1) HD/2)
             // PAIR, bf16 result: rows go through the swizzled staging box of this group and one
             // TMA store (a thread-per-row global store touches 32 rows per warp instruction)
-            const bool staged = PAIR && N > 0 && !to_acc;  // TMA-stored bf16 (the box also serves as scratch)
+            const bool drains = g < 2;  // groups 0, 1 drain / write O columns [64 g, 64 g + 64)
+            const bool staged = PAIR && N > 0 && !to_acc && drains;  // TMA-stored bf16 (the box also serves as scratch)
             const uint32_t stg = sbase + L::OFF_STG + static_cast<uint32_t>(g) * (BM * 128);
             if (staged && threadIdx.x == static_cast<unsigned>(g * BM)) bulk_wait_read0();  // previous store read the box
             if (N > 0) {
-                // final m = m(last); combine the two groups' row sums relative to it
+                // final m = m(last); combine the groups' row sums relative to it
                 const int last = gn0 + N - 1;
-                float2* lsh = reinterpret_cast<float2*>(smem + L::OFF_L) + (n_units_done & 1) * 2 * BM;
+                float2* lsh = reinterpret_cast<float2*>(smem + L::OFF_L) + (n_units_done & 1) * NG * BM;
+                float* mlast = reinterpret_cast<float*>(smem + L::OFF_ML) + (n_units_done & 1) * BM;
                 lsh[g * BM + r] = make_float2(m_used, lacc.x + lacc.y);
-                if ((last & 1) != g) {  // the other group made the last m: take it
-                    named_bar_sync(2 + (last & 1), 2 * BM);  // (pairs with its last arrive)
-                    m = msh[(last & 1) * BM + r];
-                }
-                asm volatile("bar.sync 1, 256;" ::: "memory");  // both groups' (m_used, l) visible
+                if (last % NG == g) mlast[r] = m;
+                named_bar_sync(1, NG * BM);  // every group's (m_used, l) and the final m visible
+                m = mlast[r];
 #pragma unroll
-                for (int gg = 0; gg < 2; ++gg) {
+                for (int gg = 0; gg < NG; ++gg) {
                     const float2 ml = lsh[gg * BM + r];
                     if (ml.y > 0.f) l += ml.y * ex2(ml.x - m);
                 }
+                gn0 += N;
+                ++n_units_done;
+                if (!drains) continue;  // (group 2: l only)
                 // drain O to registers and hand TMEM back to the next unit's PV
-                mbar_wait(bar(L::B_OF), n_units_done & 1);
+                mbar_wait(bar(L::B_OF), (n_units_done - 1) & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < HD / 64; ++c) tmem_ld32p(tO + (HD / 2) * g + 32 * c, o + 32 * c);
@@ -967,9 +986,8 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) arrive_leader(L::B_OE);
-                gn0 += N;
-                ++n_units_done;
             } else {
+                if (!drains) continue;
 #pragma unroll
                 for (int q = 0; q < HD / 2; ++q) o[q] = 0u;
             }
@@ -1014,7 +1032,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                                      : "memory");
                     }
                     fence_proxy_async_smem();
-                    named_bar_sync(4 + g, BM);  // this group's 128 rows are in the box
+                    named_bar_sync(8 + g, BM);  // this group's 128 rows are in the box
                     if (threadIdx.x == static_cast<unsigned>(g * BM)) {
                         tma_store_3d(&tm_out, stg, (HD / 2) * g, head, static_cast<int>(row0));  // rows >= nq clipped
                         bulk_commit();
