@@ -371,7 +371,10 @@ typedef enum {
 
 /* One block-attention launch: q [nq, Hq, D]; k, v [nkv, Hkv, D]; o_acc fp32 [nq, Hq, D] and
  * lse_acc fp32 [Hq, nq] (FIRST/MID/LAST); out [nq, Hq, D] dtype of q and lse fp32 [Hq, nq]
- * (ONLY/LAST; lse may be NULL).  bf16 runs the tcgen05/TMEM/TMA kernel, f32 the FFMA kernel. */
+ * (ONLY/LAST; lse may be NULL).  bf16 runs the tcgen05/TMEM/TMA kernel, f32 the FFMA kernel.
+ * Errors: CDSP_ERR_INVALID/SHAPE/DTYPE (host validation); CDSP_ERR_CAPACITY when a bf16 block has
+ * more than 4096 KV tiles of 128 keys (512K keys per launch; split longer blocks with FIRST /
+ * MID / LAST); CDSP_ERR_CUDA. */
 CDSP_API cdsp_status cdsp_attention_fwd(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
                                         const cdsp_segments* seg, float softmax_scale, int32_t mode,
                                         float* o_acc, float* lse_acc, cdsp_tensor* out, float* lse,

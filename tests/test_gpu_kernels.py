@@ -24,8 +24,9 @@ def _np(x):
 
 def _check(out, lse, o_ref, l_ref, dtype, what=""):
     err = np.abs(_np(out).astype(np.float64) - o_ref).max() if o_ref.size else 0.0
-    lerr = np.abs(_np(lse).astype(np.float64) - l_ref)
-    lerr = lerr[np.isfinite(l_ref)].max() if np.isfinite(l_ref).any() else 0.0
+    fin = np.isfinite(l_ref)
+    lerr = np.abs(_np(lse).astype(np.float64)[fin] - l_ref[fin])
+    lerr = lerr.max() if fin.any() else 0.0
     assert np.array_equal(np.isfinite(_np(lse)), np.isfinite(l_ref)), f"{what}: -inf pattern differs"
     assert err <= TOL[dtype], f"{what}: out max-abs {err:.3e} > {TOL[dtype]}"
     assert lerr <= LSE_TOL, f"{what}: lse max-abs {lerr:.3e}"
@@ -189,3 +190,88 @@ def test_bench_config_sampled_rows():
     _check(out[torch.as_tensor(rows, device="cuda")], lse[:, torch.as_tensor(rows, device="cuda")], o_ref, l_ref,
            torch.bfloat16, "32K sampled")
     comm.close()
+
+
+# ---- persistent 2-SM kernel edge cases: units with no visible key, the unit counter ring, capacity
+def _empty_half_case(mode, dtype, m=200, Hq=4, Hkv=2, D=128, seed=11):
+    """Query rows of segment 0 (positions 0..m-1) see no key (keys at 5000..), segment 1 rows
+    (positions 20000..) see all: whole 128-row units have no visible tile."""
+    q, k, v = (t.cuda() for t in qkv(2 * m, Hq, Hkv, D, dtype, seed=seed))
+    seg = api.segments(2 * m, m, 0, 20000, 2 * m, 0, 2 * m, 5000, 0)
+    qpos = np.concatenate([np.arange(m), 20000 + np.arange(m)])
+    kpos = 5000 + np.arange(2 * m)
+    return q, k, v, seg, qpos, kpos
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_rows_without_keys_only_mode(dtype):
+    D = 128 if dtype == torch.bfloat16 else 64
+    q, k, v, seg, qpos, kpos = _empty_half_case(api.ATTN_ONLY, dtype, D=D)
+    scale = 1.0 / math.sqrt(D)
+    out = torch.full_like(q, 7.0)
+    lse = torch.full((q.shape[1], q.shape[0]), 7.0, dtype=torch.float32, device="cuda")
+    api.attention_fwd(q, k, v, seg, scale, api.ATTN_ONLY, out=out, lse=lse)
+    torch.cuda.synchronize()
+    o_ref, l_ref = oracle.attention(_np(q), qpos, _np(k), _np(v), kpos, scale)
+    o_ref = np.where(np.isfinite(l_ref).T[:, :, None], o_ref, 0.0)  # no key: out 0, lse -inf (R3, R16)
+    _check(out, lse, o_ref, l_ref, dtype, "ONLY, rows without keys")
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_rows_without_keys_first_and_last_modes(dtype):
+    """FIRST writes (0, -inf) for rows without keys; LAST merges (R3): such rows get the
+    accumulator unchanged (rounded to the output dtype), the others merge with the block."""
+    D = 128 if dtype == torch.bfloat16 else 64
+    q, k, v, seg, qpos, kpos = _empty_half_case(api.ATTN_LAST, dtype, D=D, seed=12)
+    n, Hq = q.shape[0], q.shape[1]
+    scale = 1.0 / math.sqrt(D)
+    o_ref, l_ref = oracle.attention(_np(q), qpos, _np(k), _np(v), kpos, scale)
+    o_blk = np.where(np.isfinite(l_ref).T[:, :, None], o_ref, 0.0)
+    # FIRST
+    o_acc = torch.full((n, Hq, D), 3.0, dtype=torch.float32, device="cuda")
+    l_acc = torch.full((Hq, n), 3.0, dtype=torch.float32, device="cuda")
+    api.attention_fwd(q, k, v, seg, scale, api.ATTN_FIRST, o_acc, l_acc)
+    torch.cuda.synchronize()
+    assert np.abs(_np(o_acc) - o_blk).max() <= 1e-2
+    assert np.array_equal(np.isfinite(_np(l_acc)), np.isfinite(l_ref))
+    fin = np.isfinite(l_ref)
+    assert np.abs(_np(l_acc)[fin] - l_ref[fin]).max() <= LSE_TOL
+    # LAST over a random accumulator
+    g = torch.Generator().manual_seed(5)
+    acc = torch.randn((n, Hq, D), generator=g).cuda()
+    lacc = torch.randn((Hq, n), generator=g).cuda()
+    out = torch.empty_like(q)
+    lse = torch.empty((Hq, n), dtype=torch.float32, device="cuda")
+    api.attention_fwd(q, k, v, seg, scale, api.ATTN_LAST, acc.clone(), lacc.clone(), out, lse)
+    torch.cuda.synchronize()
+    m_ref, ml_ref = oracle.lse_merge([_np(acc).astype(np.float64), o_blk], [_np(lacc).astype(np.float64), l_ref])
+    _check(out, lse, m_ref, ml_ref, dtype, "LAST, rows without keys")
+    rows0 = slice(0, n // 2)  # segment 0: no key -> exactly the accumulator, rounded once
+    assert torch.equal(out[rows0], acc[rows0].to(dtype))
+    assert torch.equal(lse[:, rows0], lacc[:, rows0])
+
+
+def test_unit_counter_ring_many_launches():
+    """> 4096 back-to-back launches cycle every slot of the persistent kernel's unit-counter
+    ring (each launch's last CTA re-arms its slot); results stay identical."""
+    N, Hq, D = 384, 2, 128
+    q, k, v = (t.cuda() for t in qkv(N, Hq, Hq, D, torch.bfloat16, seed=21))
+    ref = torch.empty_like(q)
+    api.attention_fwd(q, k, v, api.causal_segments(N, N), 0.0, api.ATTN_ONLY, out=ref)
+    out = torch.empty_like(q)
+    for _ in range(4200):
+        api.attention_fwd(q, k, v, api.causal_segments(N, N), 0.0, api.ATTN_ONLY, out=out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+
+
+def test_kv_block_capacity_error():
+    """One block-attention launch takes at most 4096 KV tiles (512K keys): more is
+    CDSP_ERR_CAPACITY before anything is launched."""
+    nkv = 4096 * 128 + 1
+    q = torch.zeros((128, 1, 128), dtype=torch.bfloat16, device="cuda")
+    k = torch.zeros((nkv, 1, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(api.CdspError) as ei:
+        api.attention_fwd(q, k, k, api.causal_segments(128, nkv, q_pos0=nkv - 128), 0.0, api.ATTN_ONLY,
+                          out=torch.empty_like(q))
+    assert ei.value.status == 5
