@@ -93,11 +93,9 @@ using namespace ptx;
 
 namespace {
 
-#ifndef CDSP_NGROUPS  // softmax groups (4 warps each); group g takes the KV tiles n = g (mod NG)
-#define CDSP_NGROUPS 2
-#endif
-constexpr int NG = CDSP_NGROUPS;
-static_assert(NG == 2 || NG == 3, "2 or 3 softmax groups");
+// two softmax groups of 4 warps (a third group, 15 warps, was measured: not faster, the
+// 128-register cap of 4 warps per sub-partition costs what the extra latency slack gains)
+constexpr int NG = 2;
 constexpr int kThreads = 32 * (4 * NG + 3);  // softmax groups + K producer + V producer + MMA
 constexpr int BM = 128;                 // query rows per CTA (TMEM lanes)
 constexpr int BN = 128;                 // KV rows per tile
@@ -127,9 +125,8 @@ struct Layout {
     static constexpr int STG = PAIR ? 2 * BM * 128 : 0;
     static constexpr int OFF_STG = OFF_V + VST * VTILE;
     static constexpr int OFF_M = OFF_STG + STG;            // running row max m(n): [NG (tile mod NG)][128] float
-    static constexpr int OFF_L = OFF_M + NG * BM * 4;      // epilogue (m_used, l): [2 unit parity][NG groups][128] float2
-    static constexpr int OFF_ML = OFF_L + 2 * NG * BM * 8;  // epilogue: the unit's final m: [2 unit parity][128] float
-    static constexpr int OFF_QP = OFF_ML + 2 * BM * 4;     // query position per row: [2 unit buffer][128] int64
+    static constexpr int OFF_L = OFF_M + NG * BM * 4;      // epilogue hand-over (m_used, l): [2 unit parity][NG][128] float2
+    static constexpr int OFF_QP = OFF_L + 2 * NG * BM * 8;  // query position per row: [2 unit buffer][128] int64
     static constexpr int OFF_BAR = OFF_QP + 2 * BM * 8;
     // Local: u_full[2] (unit buffer published), u_empty[2] (read by every consumer), q_empty[2],
     // s_full[NSB], v_empty[VST], o_full (the last four arrive by MMA commit, multicast to both
@@ -137,13 +134,15 @@ struct Layout {
     // Leader (the even CTA; the only one in a 1-SM launch): q_full[2], k_full[KST], v_full[VST]
     // (TMA bytes of both CTAs), p_full[NSB], o_free (softmax warps of both CTAs).
     // Pair bookkeeping: c_full[2] (odd CTA: next unit id arrived), c_empty[2] (even CTA: consumed).
+    // Epilogue hand-over: l_full[2] (the other softmax groups' row sums are in the unit-parity
+    // slot), l_empty[2] (the finishing group has read them).
     // (m(n) goes from one softmax group to the other through named barriers 2, 3.)  Every
     // tcgen05.commit costs the tensor pipe ~30 clk (tools/mma_pattern.cu), so each MMA group
     // commits once: s_full[b] (S(n) done) also frees K stage n % 3 (and, for a unit's last
     // tile, the Q buffer); v_empty[s] (PV(n) done) also tells a rescaling group that O is stable.
     static constexpr int B_UF = 0, B_UE = 2, B_QF = 4, B_QE = 6, B_KF = 8, B_VF = B_KF + KST, B_VE = B_VF + VST,
                          B_SF = B_VE + VST, B_PF = B_SF + NSB, B_OF = B_PF + NSB, B_OE = B_OF + 1, B_CF = B_OE + 1,
-                         B_CE = B_CF + 2, NBAR = B_CE + 2;
+                         B_CE = B_CF + 2, B_LF = B_CE + 2, B_LE = B_LF + 2, NBAR = B_LE + 2;
     static_assert(KST == NSB, "K stages are released through s_full");
     static constexpr int OFF_TMEM_SLOT = OFF_BAR + NBAR * 8;
     static constexpr int OFF_CLAIM = OFF_TMEM_SLOT + 8;     // [2] next unit id (odd CTA of a pair)
@@ -484,7 +483,11 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 mbar_init(bar(L::B_PF + b), 4 * CL);
             }
             mbar_init(bar(L::B_OF), 1);
-            mbar_init(bar(L::B_OE), 8 * CL);
+            mbar_init(bar(L::B_OE), 4 * CL);  // the finishing group's 4 warps (x CTAs of a pair)
+            for (int i = 0; i < 2; ++i) {
+                mbar_init(bar(L::B_LF + i), 4 * (NG - 1));
+                mbar_init(bar(L::B_LE + i), 4);
+            }
             fence_barrier_init();
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(&tm_k);
@@ -610,7 +613,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 const int j = list[n] & ~kPartialBit;
                 const int st = it % L::KST;
                 // stage st last held tile it - 3: free once S(it - 3) is done (in both CTAs)
-                if (it >= L::KST) mbar_wait(bar(L::B_SF + st), ((it - L::KST) / L::KST) & 1);
+                if (it >= L::KST) mbar_wait_backoff(bar(L::B_SF + st), ((it - L::KST) / L::KST) & 1);
                 if (lane == 0) KTRACE(15, it);
                 if (elect_one()) {
                     if constexpr (PAIR) {
@@ -655,7 +658,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             for (int n = 0; n < u.n_used; ++n) {
                 const int j = list[n] & ~kPartialBit;
                 const int st = it % L::VST;
-                if (it >= L::VST) mbar_wait(bar(L::B_VE + st), ((it - L::VST) / L::VST) & 1);
+                if (it >= L::VST) mbar_wait_backoff(bar(L::B_VE + st), ((it - L::VST) / L::VST) & 1);
                 if (lane == 0) KTRACE(14, it);
                 if (elect_one()) {
                     if constexpr (PAIR) {  // all 128 keys, this CTA's 64 d columns
@@ -799,7 +802,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             float m = -INFINITY;       // m(n) of the last tile this thread has seen
             float m_used = -INFINITY;  // max that this group's l is relative to
             float2 lacc = make_float2(0.f, 0.f);
-            // this group's tiles: local n with (gn0 + n) & 1 == g
+            // this group's tiles: tile gn of the CTA's sequence belongs to group gn mod NG
             const int n_first = ((g - gn0) % NG + NG) % NG;
             for (int n = n_first; n < N; n += NG) {
                 const int gn = gn0 + n;
@@ -859,7 +862,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 if (r == 0 && n == 0) UNIT_STAMP(u.x * CL + crank, 5, gtime_ns());
 #endif
                 // ---- the serial link: m(n) = lazy max(m(n-1), rowmax(S(n))) ----
-                if (n > 0) {  // m(n-1) from the group of tile n-1 (named barrier 2 + (n-1) mod NG: 128 + 128 threads)
+                if (n > 0) {  // m(n-1) from the group of tile n-1 (named barrier 2 + its index: 128 + 128 threads)
                     named_bar_sync(2 + (gn - 1) % NG, 2 * BM);
                     m = msh[((gn - 1) % NG) * BM + r];
                 }
@@ -884,7 +887,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                         tmem_st16(tO + 16 * c, o);
                     }
                 }
-                if (n < N - 1) {  // (the unit's last m goes to the epilogue through OFF_ML)
+                if (n < N - 1) {  // (the unit's last m stays with its group, which finishes the unit)
                     msh[(gn % NG) * BM + r] = m;
                     __threadfence_block();
                     named_bar_arrive(2 + gn % NG, 2 * BM);
@@ -950,136 +953,156 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             if (N == 0 && p.mode == CDSP_ATTN_MID) continue;  // merging an empty block is the identity
 
             // ---------------- epilogue: normalise, then write / LSE-merge (R3) ----------------
+            // One group finishes the unit: the group E that computed its last tile (it holds the
+            // final m; group 0 for a unit without tiles).  The other groups hand over their row
+            // sums and start the next unit at once, so its first tiles run under this epilogue.
+            const int E = N > 0 ? (gn0 + N - 1) % NG : 0;
             float l = 0.f;
-            uint32_t o[HD / 2];  // this group's O columns [g HD/2, (g+1) HD/2)
-            // PAIR, bf16 result: rows go through the swizzled staging box of this group and one
-            // TMA store (a thread-per-row global store touches 32 rows per warp instruction)
-            const bool drains = g < 2;  // groups 0, 1 drain / write O columns [64 g, 64 g + 64)
-            const bool staged = PAIR && N > 0 && !to_acc && drains;  // TMA-stored bf16 (the box also serves as scratch)
-            const uint32_t stg = sbase + L::OFF_STG + static_cast<uint32_t>(g) * (BM * 128);
-            if (staged && threadIdx.x == static_cast<unsigned>(g * BM)) bulk_wait_read0();  // previous store read the box
             if (N > 0) {
-                // final m = m(last); combine the groups' row sums relative to it
-                const int last = gn0 + N - 1;
-                float2* lsh = reinterpret_cast<float2*>(smem + L::OFF_L) + (n_units_done & 1) * NG * BM;
-                float* mlast = reinterpret_cast<float*>(smem + L::OFF_ML) + (n_units_done & 1) * BM;
-                lsh[g * BM + r] = make_float2(m_used, lacc.x + lacc.y);
-                if (last % NG == g) mlast[r] = m;
-                named_bar_sync(1, NG * BM);  // every group's (m_used, l) and the final m visible
-                m = mlast[r];
-#pragma unroll
-                for (int gg = 0; gg < NG; ++gg) {
-                    const float2 ml = lsh[gg * BM + r];
-                    if (ml.y > 0.f) l += ml.y * ex2(ml.x - m);
-                }
+                const int pu = n_units_done & 1, use = n_units_done >> 1;
+                float2* lsh = reinterpret_cast<float2*>(smem + L::OFF_L) + pu * NG * BM;
                 gn0 += N;
                 ++n_units_done;
-                if (!drains) continue;  // (group 2: l only)
-                // drain O to registers and hand TMEM back to the next unit's PV
-                mbar_wait(bar(L::B_OF), (n_units_done - 1) & 1);
-                tc_fence_after();
+                if (g != E) {
+                    if (use >= 1) mbar_wait(bar(L::B_LE + pu), (use - 1) & 1);  // slot read by the unit 2 back
+                    lsh[g * BM + r] = make_float2(m_used, lacc.x + lacc.y);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar(L::B_LF + pu));
+                    continue;
+                }
+                mbar_wait(bar(L::B_LF + pu), use & 1);
+                if (m != -INFINITY) {  // (m = -inf: no visible key; the FMA-pipe exp2 floors at 2^-126)
+                    l = lacc.x + lacc.y;  // relative to m: this group made the last m (m_used == m)
 #pragma unroll
-                for (int c = 0; c < HD / 64; ++c) tmem_ld32p(tO + (HD / 2) * g + 32 * c, o + 32 * c);
-                tc_wait_ld();
-                reg_tie32(o);
-                if constexpr (HD == 128) reg_tie32(o + 32);
-                tc_fence_before();
+                    for (int gg = 0; gg < NG; ++gg) {
+                        if (gg == g) continue;
+                        const float2 ml = lsh[gg * BM + r];
+                        if (ml.y > 0.f) l += ml.y * ex2(ml.x - m);
+                    }
+                }
                 __syncwarp();
-                if (lane == 0) arrive_leader(L::B_OE);
-            } else {
-                if (!drains) continue;
-#pragma unroll
-                for (int q = 0; q < HD / 2; ++q) o[q] = 0u;
+                if (lane == 0) mbar_arrive(bar(L::B_LE + pu));
+            } else if (g != E) {
+                continue;
             }
             const float inv_l = l > 0.f ? 1.0f / l : 0.f;
             const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
             float wa = 0.f, wb = 1.f, lse_out = lse_b;
             if (merge) merge_weights(lse_a, lse_b, wa, wb, lse_out);
             const float sbw = wb * inv_l;
-            if (PAIR && N > 0 && (CDSP_EPI_COALESCED || !to_acc)) {
-                // this warp's 32 rows: its 4 KB slice of the group's staging box (scratch for the
-                // coalesced fp32 accumulator I/O; for bf16 results also the rows of the TMA box)
-                const uint32_t wtile = stg + static_cast<uint32_t>(quad) * (32 * 128);
-                const int64_t wrow0 = row0 + 32 * quad;
-                const int nvalid = static_cast<int>(nq - wrow0 < 32 ? (nq - wrow0 > 0 ? nq - wrow0 : 0) : 32);
-                float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + (HD / 2) * g;
-                const size_t rstride = static_cast<size_t>(p.Hq) * HD;
-#pragma unroll
-                for (int c = 0; c < HD / 64; ++c) {
-                    float a[32];
-                    if (merge) warp_rows_load(a, acc_w + 32 * c, rstride, nvalid, wtile, lane);
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) {
-                        float v = __uint_as_float(o[32 * c + q]) * sbw;
-                        if (merge) v = fmaf(wa, a[q], v);
-                        o[32 * c + q] = __float_as_uint(v);
+            // PAIR: bf16 rows go through two 128B-swizzled boxes (64 columns each) and TMA stores;
+            // fp32 accumulator rows through each warp's 4 KB slices of the same boxes (coalesced)
+            const bool boxed = PAIR && N > 0 && (CDSP_EPI_COALESCED || !to_acc);
+            const uint32_t stg0 = sbase + L::OFF_STG;
+            const int64_t wrow0 = row0 + 32 * quad;
+            const int nvalid = static_cast<int>(nq - wrow0 < 32 ? (nq - wrow0 > 0 ? nq - wrow0 : 0) : 32);
+            const size_t rstride = static_cast<size_t>(p.Hq) * HD;
+#pragma unroll 1
+            for (int hh = 0; hh < HD / 64; ++hh) {  // O columns [64 hh, 64 hh + 64)
+                uint32_t o[64];
+                if (N > 0) {
+                    if (hh == 0) {
+                        mbar_wait(bar(L::B_OF), (n_units_done - 1) & 1);
+                        tc_fence_after();
                     }
-                }
-                if (to_acc) {
-#pragma unroll
-                    for (int c = 0; c < HD / 64; ++c) warp_rows_store(o + 32 * c, acc_w + 32 * c, rstride, nvalid, wtile, lane);
-                    if (row_ok && g == 0) p.lse_acc[static_cast<size_t>(head) * nq + row] = lse_out;
+                    tmem_ld32p(tO + 64 * hh, o);
+                    tmem_ld32p(tO + 64 * hh + 32, o + 32);
+                    tc_wait_ld();
+                    reg_tie32(o);
+                    reg_tie32(o + 32);
+                    if (hh == HD / 64 - 1) {  // O drained: TMEM back to the next unit's PV
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) arrive_leader(L::B_OE);
+                    }
                 } else {
-                    const uint32_t rsw = static_cast<uint32_t>(r & 7), rowa = stg + static_cast<uint32_t>(r) * 128;
 #pragma unroll
-                    for (int q = 0; q < HD / 16; ++q) {  // 16-byte chunk q of the 128-byte row
-                        const uint32_t* w = o + 8 * q;
-                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rowa + ((static_cast<uint32_t>(q) ^ rsw) << 4)),
-                                     "r"(pack_bf16(__uint_as_float(w[0]), __uint_as_float(w[1]))),
-                                     "r"(pack_bf16(__uint_as_float(w[2]), __uint_as_float(w[3]))),
-                                     "r"(pack_bf16(__uint_as_float(w[4]), __uint_as_float(w[5]))),
-                                     "r"(pack_bf16(__uint_as_float(w[6]), __uint_as_float(w[7])))
-                                     : "memory");
-                    }
-                    fence_proxy_async_smem();
-                    named_bar_sync(8 + g, BM);  // this group's 128 rows are in the box
-                    if (threadIdx.x == static_cast<unsigned>(g * BM)) {
-                        tma_store_3d(&tm_out, stg, (HD / 2) * g, head, static_cast<int>(row0));  // rows >= nq clipped
-                        bulk_commit();
-                    }
-                    if (row_ok && g == 0 && p.lse) p.lse[static_cast<size_t>(head) * nq + row] = lse_out;
+                    for (int q = 0; q < 64; ++q) o[q] = 0u;
                 }
-            } else if (row_ok) {
-                const size_t orow = (static_cast<size_t>(row) * p.Hq + head) * HD + (HD / 2) * g;
+                if (boxed) {
+                    const uint32_t box = stg0 + static_cast<uint32_t>(hh) * (BM * 128);
+                    const uint32_t wtile = box + static_cast<uint32_t>(quad) * (32 * 128);
+                    float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
 #pragma unroll
-                for (int c = 0; c < HD / 64; ++c) {
-                    float v[32];
+                    for (int c = 0; c < 2; ++c) {
+                        float a[32];
+                        if (merge) warp_rows_load(a, acc_w + 32 * c, rstride, nvalid, wtile, lane);
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(o[32 * c + q]) * sbw;
-                    if (merge) {
-                        const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float4 av = a4[q];
-                            v[4 * q + 0] = fmaf(wa, av.x, v[4 * q + 0]);
-                            v[4 * q + 1] = fmaf(wa, av.y, v[4 * q + 1]);
-                            v[4 * q + 2] = fmaf(wa, av.z, v[4 * q + 2]);
-                            v[4 * q + 3] = fmaf(wa, av.w, v[4 * q + 3]);
+                        for (int q = 0; q < 32; ++q) {
+                            float v = __uint_as_float(o[32 * c + q]) * sbw;
+                            if (merge) v = fmaf(wa, a[q], v);
+                            o[32 * c + q] = __float_as_uint(v);
                         }
                     }
                     if (to_acc) {
-                        float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow + 32 * c);
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                        for (int c = 0; c < 2; ++c) warp_rows_store(o + 32 * c, acc_w + 32 * c, rstride, nvalid, wtile, lane);
                     } else {
-                        uint4* d4 = reinterpret_cast<uint4*>(p.out + orow + 32 * c);
+                        const uint32_t rsw = static_cast<uint32_t>(r & 7), rowa = box + static_cast<uint32_t>(r) * 128;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            d4[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                                               pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+                        for (int q = 0; q < 8; ++q) {  // 16-byte chunk q of the 128-byte row
+                            const uint32_t* w = o + 8 * q;
+                            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rowa + ((static_cast<uint32_t>(q) ^ rsw) << 4)),
+                                         "r"(pack_bf16(__uint_as_float(w[0]), __uint_as_float(w[1]))),
+                                         "r"(pack_bf16(__uint_as_float(w[2]), __uint_as_float(w[3]))),
+                                         "r"(pack_bf16(__uint_as_float(w[4]), __uint_as_float(w[5]))),
+                                         "r"(pack_bf16(__uint_as_float(w[6]), __uint_as_float(w[7])))
+                                         : "memory");
+                        }
                     }
-                }
-                if (g == 0) {
-                    const size_t li = static_cast<size_t>(head) * nq + row;
-                    if (to_acc) {
-                        p.lse_acc[li] = lse_out;
-                    } else if (p.lse) {
-                        p.lse[li] = lse_out;
+                } else if (row_ok) {
+                    const size_t orow = (static_cast<size_t>(row) * p.Hq + head) * HD + 64 * hh;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        float v[32];
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(o[32 * c + q]) * sbw;
+                        if (merge) {
+                            const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 av = a4[q];
+                                v[4 * q + 0] = fmaf(wa, av.x, v[4 * q + 0]);
+                                v[4 * q + 1] = fmaf(wa, av.y, v[4 * q + 1]);
+                                v[4 * q + 2] = fmaf(wa, av.z, v[4 * q + 2]);
+                                v[4 * q + 3] = fmaf(wa, av.w, v[4 * q + 3]);
+                            }
+                        }
+                        if (to_acc) {
+                            float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow + 32 * c);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                        } else {
+                            uint4* d4 = reinterpret_cast<uint4*>(p.out + orow + 32 * c);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                d4[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                                   pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+                        }
                     }
                 }
             }
+            if (boxed && !to_acc) {
+                fence_proxy_async_smem();
+                named_bar_sync(8 + g, BM);  // this group's 128 rows are in the boxes
+                if (threadIdx.x == static_cast<unsigned>(g * BM)) {
+                    for (int hh = 0; hh < HD / 64; ++hh)
+                        tma_store_3d(&tm_out, stg0 + static_cast<uint32_t>(hh) * (BM * 128), 64 * hh, head,
+                                     static_cast<int>(row0));  // rows >= nq clipped
+                    bulk_commit();
+                    bulk_wait_read0();  // the boxes are free again (the next unit may finish in another group)
+                }
+            }
+            if (row_ok) {
+                const size_t li = static_cast<size_t>(head) * nq + row;
+                if (to_acc) {
+                    p.lse_acc[li] = lse_out;
+                } else if (p.lse) {
+                    p.lse[li] = lse_out;
+                }
+            }
 #ifdef CDSP_KTRACE
-            if (r == 0 && g == 0) {
+            if (r == 0) {
                 const unsigned long long t = gtime_ns();
                 unsigned smid;
                 asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -1094,7 +1117,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
     }
 
     // ---- teardown
-    if (PAIR && (threadIdx.x == 0 || threadIdx.x == BM)) bulk_wait_all0();  // staged output stores done
+    if (PAIR && warp < 4 * NG && (threadIdx.x % BM) == 0) bulk_wait_all0();  // staged output stores done
     tc_fence_before();
     if constexpr (PAIR) cluster_sync_all();  // no remote arrive / DSMEM access into a CTA that exits
     else __syncthreads();

@@ -79,6 +79,28 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         }
     }
 }
+// Producer-side wait: the waiting warp backs off with nanosleep between tries, so a warp that
+// runs stages ahead does not spend issue slots of the sub-partition it shares with softmax warps.
+#ifndef CDSP_PRODUCER_BACKOFF_NS
+#define CDSP_PRODUCER_BACKOFF_NS 0
+#endif
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity) {
+#if CDSP_PRODUCER_BACKOFF_NS > 0
+    if (mbar_try_wait(bar, parity)) return;
+    uint64_t t0 = 0;
+    uint32_t n = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        __nanosleep(CDSP_PRODUCER_BACKOFF_NS);
+        if ((++n & 255u) == 0) {
+            const uint64_t t = globaltimer();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 4000000000ull) __trap();
+        }
+    }
+#else
+    mbar_wait(bar, parity);
+#endif
+}
 // Same, without the suspend hint: lowest wake-up latency, for a latency-critical waiter
 // (the MMA issuer) whose spinning costs one warp's issue slots.
 __device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
