@@ -150,29 +150,44 @@ __global__ void zigzag_map_kernel(int64_t L, int s, int64_t m, int32_t* tok_rank
 // One warp per (token, K|V) row: the token's position and physical block are resolved once;
 // the row [Hkv, D] splits into tp contiguous slices (one per decode TP rank), each copied to a
 // contiguous slot [blk][p % B][Hkv/tp][D] of that rank's cache in 16-byte vectors.
-__global__ void __launch_bounds__(256) paged_scatter_kernel(const PagedArgs a) {
-    const int warps = blockDim.x >> 5;
-    const int64_t w = static_cast<int64_t>(blockIdx.x) * warps + (threadIdx.x >> 5);
+// Grid-stride over (token, K|V) rows, one warp per row; each lane keeps 4 16-byte vectors in
+// flight.
+__global__ void __launch_bounds__(512) paged_scatter_kernel(const PagedArgs a) {
+    const int wpb = blockDim.x >> 5;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * wpb;
     const int lane = threadIdx.x & 31;
-    if (w >= 2 * a.n_tok) return;
-    const int which = w >= a.n_tok;  // 0: K, 1: V
-    const int64_t tok = which ? w - a.n_tok : w;
-    const int64_t pos = tok < a.len0 ? a.pos0 + tok * a.pos_stride : a.pos1 + (tok - a.len0) * a.pos_stride;
-    const int64_t lb = pos / a.block_size;
-    const int32_t blk = lb < a.n_table ? __ldg(a.block_table + lb) : -1;
-    if (blk < 0 || blk >= a.num_blocks) {
-        if (lane == 0 && which == 0) atomicAdd(a.bad_count, 1ull);
-        return;
-    }
     const int seg_vec = a.seg_vec;                  // 16-byte vectors per TP slice (Hkv/tp heads)
     const int row_vec = seg_vec * a.tp;             // per token row
-    const int64_t slot = static_cast<int64_t>(blk) * a.block_size + pos % a.block_size;
-    const uint4* src = static_cast<const uint4*>(which ? a.v : a.k) + tok * row_vec;
-    for (int c = lane; c < row_vec; c += 32) {
-        const int t = a.seg_shift >= 0 ? (c >> a.seg_shift) : c / seg_vec;
-        const int cl = c - t * seg_vec;
-        uint4* dst = static_cast<uint4*>(which ? a.v_cache[t] : a.k_cache[t]) + slot * seg_vec + cl;
-        *dst = __ldg(src + c);
+    for (int64_t w = static_cast<int64_t>(blockIdx.x) * wpb + (threadIdx.x >> 5); w < 2 * a.n_tok; w += nw) {
+        const int which = w >= a.n_tok;  // 0: K, 1: V
+        const int64_t tok = which ? w - a.n_tok : w;
+        const int64_t pos = tok < a.len0 ? a.pos0 + tok * a.pos_stride : a.pos1 + (tok - a.len0) * a.pos_stride;
+        const int64_t lb = pos / a.block_size;
+        const int32_t blk = lb < a.n_table ? __ldg(a.block_table + lb) : -1;
+        if (blk < 0 || blk >= a.num_blocks) {
+            if (lane == 0 && which == 0) atomicAdd(a.bad_count, 1ull);
+            continue;
+        }
+        const int64_t slot = static_cast<int64_t>(blk) * a.block_size + pos % a.block_size;
+        const uint4* src = static_cast<const uint4*>(which ? a.v : a.k) + tok * row_vec;
+        for (int c0 = 0; c0 < row_vec; c0 += 128) {
+            uint4 x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = c0 + 32 * u + lane;
+                if (c < row_vec) x[u] = __ldg(src + c);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = c0 + 32 * u + lane;
+                if (c < row_vec) {
+                    const int t = a.seg_shift >= 0 ? (c >> a.seg_shift) : c / seg_vec;
+                    const int cl = c - t * seg_vec;
+                    uint4* dst = static_cast<uint4*>(which ? a.v_cache[t] : a.k_cache[t]) + slot * seg_vec + cl;
+                    *dst = x[u];
+                }
+            }
+        }
     }
 }
 
@@ -287,9 +302,17 @@ cdsp_status launch_paged_scatter(const PagedArgs& a_in, cudaStream_t st) {
         if ((1 << sh) == a.seg_vec) a.seg_shift = sh;
     const int64_t rows = 2 * a.n_tok;  // one warp per (token, K|V)
     if (rows == 0) return CDSP_OK;
-    const int64_t blocks = (rows + 7) / 8;
-    CDSP_REQUIRE(blocks < (1ll << 31), CDSP_ERR_SHAPE, "transfer too large");
-    paged_scatter_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(a);
+    // CTAs of 16 warps, one warp per row.  CDSP_SCATTER_CTAS caps the grid (measurement control):
+    // confining the scatter to 8-32 SMs beside the attention lengthened the bench step (the
+    // scatter then outlasts the attention: 6.5 -> 6.8-7.9 ms), so the default is uncapped.
+    static const int64_t cap = [] {
+        const char* e = getenv("CDSP_SCATTER_CTAS");
+        const long v = e ? strtol(e, nullptr, 10) : 0;
+        return static_cast<int64_t>(v > 0 ? v : (1ll << 30));
+    }();
+    int64_t blocks = (rows + 15) / 16;
+    if (blocks > cap) blocks = cap;
+    paged_scatter_kernel<<<static_cast<unsigned>(blocks), 512, 0, st>>>(a);
     CDSP_CUDA(cudaGetLastError());
     return CDSP_OK;
 }
