@@ -254,6 +254,8 @@ def main():
     # HBM-bound scatter beside a tensor-bound kernel); the step ends when both are done
     xfer = torch.cuda.Stream(dev)
     ev_kv = torch.cuda.Event()
+    xfer_first = os.environ.get("CDSP_BENCH_XFER_FIRST") == "1"
+    no_xfer = os.environ.get("CDSP_BENCH_NO_XFER") == "1"  # measurement control: attention alone
 
     def step(qq=None, kk=None, vv=None, oo=None):
         qq, kk, vv, oo = (qq if qq is not None else q), (kk if kk is not None else k), \
@@ -263,19 +265,26 @@ def main():
         if s == 1:
             # one rank: the zigzag partition (S_0 then S_1) is the identity, so the shard IS the
             # chunk and a2 moves no data; the output is written in place
+            # the attention is enqueued first: its persistent grid takes every SM, and the
+            # transfer (same dependencies, own stream) fills SMs as the attention's tail frees
+            # them -- enqueued first, the scatter's CTAs would hold SMs the attention needs
             ev_kv.record(stream)
-            xfer.wait_event(ev_kv)
-            api.kv_transfer_to_decode(kk, vv, group, dst, xfer)
+            if xfer_first and not no_xfer:  # measurement control: the scatter enqueued first
+                xfer.wait_event(ev_kv)
+                api.kv_transfer_to_decode(kk, vv, group, dst, xfer)
             api.prefill_chunk(qq, kk, vv, comm.kvstore(), group, 0.0, oo, lse_s, stream)
+            if not xfer_first and not no_xfer:
+                xfer.wait_event(ev_kv)
+                api.kv_transfer_to_decode(kk, vv, group, dst, xfer)
             stream.wait_stream(xfer)
             return
         api.zigzag_gather(qq, s, rank, qs, stream)
         api.zigzag_gather(kk, s, rank, ks, stream)
         api.zigzag_gather(vv, s, rank, vs, stream)
         ev_kv.record(stream)
+        api.prefill_chunk(qs, ks, vs, comm.kvstore(), group, 0.0, out_s, lse_s, stream)
         xfer.wait_event(ev_kv)
         api.kv_transfer_to_decode(ks, vs, group, dst, xfer)
-        api.prefill_chunk(qs, ks, vs, comm.kvstore(), group, 0.0, out_s, lse_s, stream)
         api.zigzag_scatter(out_s, s, rank, oo, stream)
         stream.wait_stream(xfer)  # ks/vs are rewritten by the next step's gathers
 
