@@ -372,6 +372,9 @@ typedef enum {
 /* One block-attention launch: q [nq, Hq, D]; k, v [nkv, Hkv, D]; o_acc fp32 [nq, Hq, D] and
  * lse_acc fp32 [Hq, nq] (FIRST/MID/LAST); out [nq, Hq, D] dtype of q and lse fp32 [Hq, nq]
  * (ONLY/LAST; lse may be NULL).  bf16 runs the tcgen05/TMEM/TMA kernel, f32 the FFMA kernel.
+ * MID / LAST (bf16) launch as programmatic dependents of the preceding kernel in the stream: they
+ * may start while a preceding block-attention launch finishes its last units and touch o_acc /
+ * lse_acc / out / lse only after it completed, so q / k / v must not be written by that launch.
  * Errors: CDSP_ERR_INVALID/SHAPE/DTYPE (host validation); CDSP_ERR_CAPACITY when a bf16 block has
  * more than 4096 KV tiles of 128 keys (512K keys per launch; split longer blocks with FIRST /
  * MID / LAST); CDSP_ERR_CUDA. */

@@ -537,6 +537,9 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 if (lane == 0) {
                     uinfo[ub].x = -1;
                     mbar_arrive(bar(L::B_UF + ub));
+                    // no more units here: a programmatically dependent launch (the next ring step)
+                    // may start on the SMs this grid frees from now on
+                    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
                 }
                 break;
             }
@@ -796,8 +799,6 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             const bool row_ok = row < nq;
             const uint16_t* list = reinterpret_cast<const uint16_t*>(smem + L::OFF_SCHED) + ub * L::LISTMAX;
             const int64_t* qp = reinterpret_cast<const int64_t*>(smem + L::OFF_QP) + ub * BM;
-            float lse_a = -INFINITY;  // issued early: only needed in the epilogue
-            if (merge && row_ok) lse_a = p.lse_acc[static_cast<size_t>(head) * nq + row];
 
             float m = -INFINITY;       // m(n) of the last tile this thread has seen
             float m_used = -INFINITY;  // max that this group's l is relative to
@@ -985,6 +986,10 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             } else if (g != E) {
                 continue;
             }
+            // the accumulator / output belong to the previous launch until it completes (a no-op
+            // unless this grid was launched as its programmatic dependent)
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            const float lse_a = merge && row_ok ? p.lse_acc[static_cast<size_t>(head) * nq + row] : -INFINITY;
             const float inv_l = l > 0.f ? 1.0f / l : 0.f;
             const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
             float wa = 0.f, wb = 1.f, lse_out = lse_b;
@@ -1256,7 +1261,7 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     // persistent: one CTA per SM (TMEM and shared memory admit one), units claimed dynamically
     const int groups = static_cast<int>(units < max_groups ? units : max_groups);
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = PAIR ? 2 : 1;
     at[0].val.clusterDim.y = 1;
@@ -1265,8 +1270,19 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = Lt::SMEM;
     cfg.stream = st;
+    // MID / LAST steps depend on the previous launch only through the accumulator, read and
+    // written after griddepcontrol.wait, so they are launched as programmatic dependents and
+    // start under its tail (CDSP_PDL=0: plain stream order, measurement control)
+    static const bool pdl = !(getenv("CDSP_PDL") != nullptr && getenv("CDSP_PDL")[0] == '0');
+    int na = 0;
+    if (PAIR) at[na++] = at[0];
+    if (pdl && (a.mode == CDSP_ATTN_MID || a.mode == CDSP_ATTN_LAST)) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = PAIR ? 1 : 0;
+    cfg.numAttrs = na;
     CDSP_CUDA(cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, p));
 #ifdef CDSP_KTRACE
     if (const char* path = getenv("CDSP_TRACE")) {  // debug builds only: synchronous dump
