@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--zigzag-only", action="store_true")
+    ap.add_argument("--one-stream", action="store_true",
+                    help="all ranks on one stream: the sum of the ranks' ring times (no time-sharing noise)")
     args = ap.parse_args()
     L, H, D = args.seq, args.heads, 128
     dev = torch.device("cuda:0")
@@ -38,7 +40,8 @@ def main():
             comms = make_loopback_comms(plan, H, D, torch.bfloat16)
             shards = prepare_shards(q, k, v, plan)
             outs = alloc_out_shards(plan, H, D, torch.bfloat16, dev, want_lse=False)
-            streams = [torch.cuda.Stream(dev) for _ in range(s)]
+            one = torch.cuda.Stream(dev)
+            streams = [one] * s if args.one_stream else [torch.cuda.Stream(dev) for _ in range(s)]
             times = []
             for it in range(args.iters + 2):
                 torch.cuda.synchronize()
