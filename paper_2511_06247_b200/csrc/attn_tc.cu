@@ -7,42 +7,42 @@
 // tensors"), extended to historical tokens as Tetris does (§6: "we extend Flash
 // Attention [7] to support zigzag ring attention for historical tokens").
 //
-// B200 design (not the paper's A100 FlashAttention-2), from measurements on the box:
-//  * tcgen05.mma M=128 reaches the full 8192 FLOP/clk/SM only for N >= 128 (N=64: ~48 clk
-//    per K=16 step instead of 32; tools/mma_rate.cu), so S = Q K^T uses 128-key tiles.
-//    The issuing thread is paced by the tensor pipe (a group of 8 MMAs is accepted about
-//    when the previous group drains), so the MMA order below is the execution order.
-//  * MUFU.EX2 issues 16 lanes/clk/SM (tools/exp_rate.cu): the 16384 exponentials of a
-//    128x128 tile take 1024 clk, exactly the two MMAs of that tile, and TMEM reads run at
-//    ~64 B/clk per SM sub-partition (64 KB of S: ~256 clk).  The softmax of one tile is
-//    therefore longer than its MMAs; it must not sit on the tensor pipe's critical path.
-//  * one CTA = one 128-row query tile of one head, 11 warps:
-//      warps 0-3   softmax group 0: KV tiles 0, 2, 4, ... of the schedule
-//      warps 4-7   softmax group 1: KV tiles 1, 3, 5, ...
-//                  (warp w owns TMEM lanes 32*(w%4).., one thread = one query row holding
-//                  all 128 scores of the tile in registers)
-//      warp 8      TMA producer: Q once, then K tiles (3 stages)
-//      warp 9      TMA producer: V tiles (2 stages)
-//      warp 10     TMEM allocator + tcgen05.mma issuer (warp-uniform loop, one lane issues)
-//  * TMEM (512 cols): O [0,128), S/P triple buffer [128,256) [256,384) [384,512).  P (bf16)
-//    is written over its own S columns and is the A operand of PV straight from TMEM.  The
-//    MMA order is S(0) S(1) S(2) | PV(0) S(3) | PV(1) S(4) | ...: S(n+3) reuses the buffer
-//    of P(n) right after PV(n) (same in-order pipe), so scores are always two tiles ahead
-//    and the two softmax groups overlap each other's exponentials.
-//  * the only serial link between consecutive tiles is the running row max m (online
-//    softmax): a group takes the row max of its own tile first, then m(n-1) from the other
-//    group through shared memory, publishes m(n) and only then runs the exponentials.
-//    Each group keeps its own row sum l (rescaled whenever m moves); the two are added in
-//    the epilogue.  Lazy rescaling: m only moves when it grows by > 8 (log2 units); O is
-//    then rescaled in TMEM after PV(n-1) completed and before m(n) is published.
-//  * 1/8 of the exponentials run as a cubic on the FMA pipe (rel. error 7.5e-5, far below
-//    bf16's 2^-9), packed fp32x2 FFMA2/FADD2.  Under sustained load the B200 sits at its
-//    ~1000 W cap (SM clock ~1.5 GHz, tools/clock_probe.py), so energy per tile matters as much
-//    as clocks per tile: 1/8 measured best sustained (1/4: -3.5%, 3/8: -3%, none: -1%).
-//  * one score tile is 128 fp32 registers; holding it whole spilled loop state whose reloads
-//    queue behind MUFU traffic, so a thread keeps 64 scores: columns 64-127 are read for the
-//    row max, 0-63 for max + exponentials, and 64-127 again for theirs.
-//  * masks from segment descriptors: empty tiles are skipped, full tiles run mask-free,
+// B200 design (not the paper's A100 FlashAttention-2), from measurements on the box (DESIGN.md
+// 6.1 has the numbers and the tools):
+//  * tcgen05.mma M=128 reaches the full 8192 FLOP/clk/SM only for N >= 128, so S = Q K^T uses
+//    128-key tiles; a KV tile costs the tensor pipe 1024 clk (S and PV, 512 each).
+//  * Supply, not math, bounds a 1-SM kernel: 64 KB of K+V per tile per SM from L2 capped the
+//    MMA pipe at ~1373 clk/tile.  HD = 128 therefore runs as CTA PAIRS (cluster of 2,
+//    tcgen05 cta_group::2, M = 256): each CTA holds its own 128 query rows (Q, S/P, O in its
+//    TMEM) and half of every K tile (64 keys) and V tile (64 of 128 d columns); the even CTA
+//    issues the MMAs, completions are multicast commits, both CTAs' TMA bytes and softmax
+//    arrivals land on the even CTA's barriers.  HD = 64 (and CDSP_ATTN_1SM=1) run the same
+//    code on one SM per unit (PAIR = false).
+//  * Persistent: one CTA per SM, work units (a pair of 128-row blocks x one head) claimed from
+//    an atomic counter, head-major and heaviest first; the producer warp publishes each unit's
+//    compacted list of used KV tiles one unit ahead (double-buffered u_full / u_empty).
+//  * 11 warps: 0-3 and 4-7 two softmax groups (one thread = one query row = one TMEM lane)
+//    taking alternate KV tiles; 8 unit scheduler + TMA producer of Q (2 buffers in PAIR) and K
+//    (3 stages); 9 TMA producer of V (3 stages in PAIR); 10 TMEM allocator + MMA issuer.
+//  * TMEM (512 cols): O [0,128), S/P triple buffer [128,256) [256,384) [384,512); P (bf16) is
+//    written over its own S columns and is PV's A operand straight from TMEM.  MMA order
+//    S(0) S(1) S(2) | PV(0) S(3) | PV(1) S(4) | ...: scores run two tiles ahead.
+//  * The only serial link between consecutive tiles is the running row max m (online
+//    softmax): a group reads its tile (all 128 scores in registers), takes m(n-1) from the
+//    other group over a named barrier, publishes m(n) before its exponentials.  Lazy
+//    rescaling: m moves only when it grows by > 8 (log2 units); O is then rescaled in TMEM
+//    after PV(n-1) completed and before m(n) is published.  Each group keeps its own row sum.
+//  * The softmax is bound by its instruction stream (~1340 clk/tile vs 1037 for the MMA pipe
+//    alone): FMNMX3 row max, 1/8 of the exponentials as a cubic on the FMA pipe (rel. error
+//    7.5e-5, far below bf16's 2^-9; same-box sweep 0 / 1/8 / 1/4 = 1313 / 1340 / 1267 TF/s).
+//  * The group that computed a unit's last tile finishes the unit (the other hands over its
+//    row sum and starts the next unit): O drained from TMEM in two 64-column halves, bf16
+//    results TMA-stored from 128B-swizzled boxes, fp32 accumulators merged (R3) through
+//    per-warp swizzled transposes (coalesced 512-byte warp transactions).
+//  * MID / LAST launches are programmatic dependents of the previous launch (the next ring
+//    step's main loop runs under this one's tail; the accumulator is touched after
+//    griddepcontrol.wait).
+//  * Masks from segment descriptors: empty tiles are skipped, full tiles run mask-free,
 //    diagonal / ragged tiles build per-row 32-bit column masks from the three visible
 //    intervals (history, segment 0, segment 1).
 #include <cuda.h>
@@ -526,7 +526,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             if constexpr (PAIR) {
                 if (!leader && i >= 1) {  // unit id from the even CTA (message i)
                     const int s = (i - 1) & 1, use = (i - 1) >> 1;
-                    mbar_wait(bar(L::B_CF + s), use & 1);
+                    mbar_wait_acq_cluster(bar(L::B_CF + s), use & 1);  // pairs with the even CTA's release.cluster
                     x = *reinterpret_cast<volatile int*>(claim_slot + s);
                     __syncwarp();
                     if (lane == 0) mbar_arrive_remote(mapa_shared(bar(L::B_CE + s), 0));
