@@ -192,8 +192,10 @@ def main():
     L = args.seq * (s if args.weak else 1)
     Hq, Hkv, D = args.heads, args.kv_heads, 128
     cfg = {"L": L, "Hq": Hq, "Hkv": Hkv, "D": D, "scaling": "weak" if args.weak else "strong",
-           "config": {"workload": "7B-shaped MHA 32K prompt, single chunk (BASELINE configs[1])"
-                      if not args.weak else f"weak: {args.seq} tokens per GPU, single chunk",
+           "config": {"workload": (f"weak: {args.seq} tokens per GPU, single chunk" if args.weak else
+                                   "7B-shaped MHA 32K prompt, single chunk (BASELINE configs[1])"
+                                   if (L, Hq, Hkv) == (32768, 32, 32) else
+                                   f"{L // 1024}K prompt, {Hq}/{Hkv} q/kv heads, d=128, single chunk"),
                       "prompt_tokens": L, "chunks": 1, "sp": s, "q_heads": Hq, "kv_heads": Hkv, "head_dim": D,
                       "plan": f"[({L}, ranks 0..{s - 1})]", "l2": "inputs larger than L2 (no flush needed)",
                       "decode_target": "paged K/V, block 16, tp=min(8,Hkv), seeded block table"}}
