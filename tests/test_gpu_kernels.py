@@ -275,3 +275,28 @@ def test_kv_block_capacity_error():
         api.attention_fwd(q, k, k, api.causal_segments(128, nkv, q_pos0=nkv - 128), 0.0, api.ATTN_ONLY,
                           out=torch.empty_like(q))
     assert ei.value.status == 5
+
+
+def test_back_to_back_merge_chain_programmatic_launch():
+    """FIRST, 6 x MID, LAST over 8 KV blocks of one 16K causal prompt, launched back to back on
+    one stream: each MID / LAST grid is a programmatic dependent of the previous one (it starts
+    its main loop under the predecessor's tail and touches the accumulator after
+    griddepcontrol.wait).  Sampled rows vs the oracle; GQA 32/8 so units are many and long."""
+    N, Hq, Hkv, D = 16384, 16, 4, 128
+    q, k, v = (t.cuda() for t in qkv(N, Hq, Hkv, D, torch.bfloat16, seed=31))
+    scale = 1.0 / math.sqrt(D)
+    o_acc = torch.empty((N, Hq, D), dtype=torch.float32, device="cuda")
+    l_acc = torch.empty((Hq, N), dtype=torch.float32, device="cuda")
+    out = torch.empty_like(q)
+    lse = torch.empty((Hq, N), dtype=torch.float32, device="cuda")
+    cuts = [i * N // 8 for i in range(9)]
+    blocks = [(k[a:b].contiguous(), v[a:b].contiguous()) for a, b in zip(cuts[:-1], cuts[1:])]
+    torch.cuda.synchronize()
+    for i, ((a, b), (kb, vb)) in enumerate(zip(zip(cuts[:-1], cuts[1:]), blocks)):
+        mode = api.ATTN_FIRST if i == 0 else api.ATTN_LAST if i == 7 else api.ATTN_MID
+        seg = api.segments(N, N, 0, 0, b - a, 0, b - a, a, 0)
+        api.attention_fwd(q, kb, vb, seg, scale, mode, o_acc, l_acc, out, lse)
+    torch.cuda.synchronize()
+    rows = sample_rows(N, 256, seed=5, edges=[0, 127, 128, 2047, 2048, N - 1])
+    o_ref, l_ref = oracle.causal_rows(_np(q), _np(k), _np(v), scale, rows=rows.numpy())
+    _check(out[rows], lse[:, rows], o_ref, l_ref, torch.bfloat16, "back-to-back chain")
