@@ -300,3 +300,20 @@ def test_back_to_back_merge_chain_programmatic_launch():
     rows = sample_rows(N, 256, seed=5, edges=[0, 127, 128, 2047, 2048, N - 1])
     o_ref, l_ref = oracle.causal_rows(_np(q), _np(k), _np(v), scale, rows=rows.numpy())
     _check(out[rows], lse[:, rows], o_ref, l_ref, torch.bfloat16, "back-to-back chain")
+
+
+def test_kv_block_at_capacity_512k_keys():
+    """One launch over exactly 4096 KV tiles (512K keys, the per-unit tile list at full length):
+    the last 200 query rows of a 512K causal prompt, sampled vs the oracle."""
+    nkv, nq, Hq, Hkv, D = 4096 * 128, 200, 2, 1, 128
+    q, k, v = (t.cuda() for t in qkv(nkv, Hq, Hkv, D, torch.bfloat16, seed=41))
+    qs = q[nkv - nq:].contiguous()
+    out = torch.empty_like(qs)
+    lse = torch.empty((Hq, nq), dtype=torch.float32, device="cuda")
+    scale = 1.0 / math.sqrt(D)
+    api.attention_fwd(qs, k, v, api.causal_segments(nq, nkv, q_pos0=nkv - nq), scale, api.ATTN_ONLY,
+                      out=out, lse=lse)
+    torch.cuda.synchronize()
+    rows = sample_rows(nq, 24, seed=3, edges=[0, 127, 128, nq - 1])
+    o_ref, l_ref = oracle.causal_rows(_np(q), _np(k), _np(v), scale, rows=(rows + nkv - nq).numpy())
+    _check(out[rows], lse[:, rows], o_ref, l_ref, torch.bfloat16, "512K keys")
