@@ -80,6 +80,10 @@
 #define CDSP_FULL_ROW 1
 #endif
 
+#ifndef CDSP_EPI_WIDE  // FIRST / MID epilogue: 64 accumulator columns per L2 round trip
+#define CDSP_EPI_WIDE 1
+#endif
+
 #ifndef CDSP_EPI_COALESCED  // fp32 accumulator epilogue through the warp-transpose tiles (PAIR)
 #define CDSP_EPI_COALESCED 1
 #endif
@@ -424,6 +428,55 @@ __device__ __forceinline__ void warp_rows_store(const uint32_t* v, float* base, 
                      : "r"(tile + rr * 128 + ((ch ^ (rr & 7)) << 4))
                      : "memory");
         if (rr < nvalid) *reinterpret_cast<float4*>(base + rr * rstride + ch * 4) = x;
+    }
+    __syncwarp();
+}
+
+// 64 columns (two 32-column chunks, tiles t0 / t1) per round trip: all 16 loads of the warp's
+// rows are in flight before the first use.
+__device__ __forceinline__ void warp_rows_load64(float (&a)[64], const float* base, size_t rstride, int nvalid,
+                                                 uint32_t t0, uint32_t t1, int lane) {
+    float4 x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int c = k >> 3, rr = 4 * (k & 7) + (lane >> 3), ch = lane & 7;
+        x[k] = rr < nvalid ? *reinterpret_cast<const float4*>(base + rr * rstride + 32 * c + ch * 4)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int c = k >> 3, rr = 4 * (k & 7) + (lane >> 3), ch = lane & 7;
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"((c ? t1 : t0) + rr * 128 + ((ch ^ (rr & 7)) << 4)),
+                     "f"(x[k].x), "f"(x[k].y), "f"(x[k].z), "f"(x[k].w)
+                     : "memory");
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(a[4 * j]), "=f"(a[4 * j + 1]), "=f"(a[4 * j + 2]), "=f"(a[4 * j + 3])
+                     : "r"(((j >> 3) ? t1 : t0) + lane * 128 + (((j & 7) ^ (lane & 7)) << 4))
+                     : "memory");
+    __syncwarp();
+}
+__device__ __forceinline__ void warp_rows_store64(const uint32_t* v, float* base, size_t rstride, int nvalid,
+                                                  uint32_t t0, uint32_t t1, int lane) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(((j >> 3) ? t1 : t0) + lane * 128 +
+                                                                     (((j & 7) ^ (lane & 7)) << 4)),
+                     "r"(v[4 * j]), "r"(v[4 * j + 1]), "r"(v[4 * j + 2]), "r"(v[4 * j + 3])
+                     : "memory");
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int c = k >> 3, rr = 4 * (k & 7) + (lane >> 3), ch = lane & 7;
+        float4 x;
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                     : "r"((c ? t1 : t0) + rr * 128 + ((ch ^ (rr & 7)) << 4))
+                     : "memory");
+        if (rr < nvalid) *reinterpret_cast<float4*>(base + rr * rstride + 32 * c + ch * 4) = x;
     }
     __syncwarp();
 }
@@ -1024,7 +1077,24 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
 #pragma unroll
                     for (int q = 0; q < 64; ++q) o[q] = 0u;
                 }
-                if (boxed) {
+                if (boxed && to_acc && CDSP_EPI_WIDE) {
+                    // fp32 accumulator, FIRST / MID: the finishing group alone uses the 32 KB of
+                    // boxes, so this warp's 8 KB (its rows of both boxes) carry a 64-column half
+                    // per round trip
+                    const uint32_t t0 = stg0 + static_cast<uint32_t>(quad) * (32 * 128);
+                    const uint32_t t1 = t0 + BM * 128;
+                    float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
+                    if (merge) {
+                        float a[64];
+                        warp_rows_load64(a, acc_w, rstride, nvalid, t0, t1, lane);
+#pragma unroll
+                        for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(fmaf(wa, a[q], __uint_as_float(o[q]) * sbw));
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * sbw);
+                    }
+                    warp_rows_store64(o, acc_w, rstride, nvalid, t0, t1, lane);
+                } else if (boxed) {
                     const uint32_t box = stg0 + static_cast<uint32_t>(hh) * (BM * 128);
                     const uint32_t wtile = box + static_cast<uint32_t>(quad) * (32 * 128);
                     float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
