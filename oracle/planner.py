@@ -145,7 +145,7 @@ def chunk_plan_solve(L: int, A: list, s_cur: int, s_next: int, pool, node_size, 
     t_next = max(pool[i] for i in nxt)                                 # line 10
     budget = t_next - t_cur                                            # line 11
     l_chunk = min(L, solve_chunk_len(models[s_cur], C, budget))        # line 13
-    l_chunk = int(math.floor(l_chunk / granule)) * granule             # R25: whole granules
+    l_chunk = int(l_chunk // granule) * granule                        # R25: whole granules (exact floor)
     return l_chunk, cur
 
 

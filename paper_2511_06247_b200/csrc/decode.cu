@@ -11,7 +11,10 @@
 //
 // B200 design.  One query row per head makes this a pure HBM stream: per token 2 Hkv_t D
 // elements are read once and every byte feeds G = Hq_t/Hkv_t dot products, ~4 FLOP/B, far
-// below any tensor-core ridge, so it runs on the FMA pipe and is sized for bandwidth:
+// below any tensor-core ridge, so it is sized for bandwidth.  The bf16 path
+// (decode_mma_kernel, below) streams K/V with cp.async and computes S and PV with the legacy
+// warp MMA (mma.sync m16n8k16: one query row per head leaves no M for a tcgen05 tile); the
+// f32 path (decode_attn_kernel, described here) runs on the FMA pipe:
 //  * grid = (n_split, Hkv_t), 256 threads; n_split x Hkv_t = one wave of resident CTAs
 //    (occupancy x 148) so that every SM streams; each CTA owns a contiguous token range, its
 //    8 warps interleave 8-vector steps.

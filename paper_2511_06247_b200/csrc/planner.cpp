@@ -181,6 +181,18 @@ double solve_len(const cdsp_latency_model& m, double C, double budget) {
     return (-B + std::sqrt(B * B + 4.0 * m.d * (budget - m.a))) / (2.0 * m.d);
 }
 
+// R25: the largest multiple of g not above x, by an exact floor of x / g: the rounded quotient
+// x / g can land on the next integer when x sits just below a multiple of g, so the integer
+// candidate is corrected against exact products (k g < 2^53 is exact in a double).
+int64_t whole_granules(double x, int64_t g) {
+    if (!(x > 0.0)) return 0;
+    const double gd = static_cast<double>(g);
+    int64_t k = static_cast<int64_t>(x / gd);
+    while (k > 0 && static_cast<double>(k) * gd > x) --k;
+    while (static_cast<double>(k + 1) * gd <= x) ++k;
+    return k * g;
+}
+
 // Algorithm 3
 bool chunk_plan(int64_t L, const Alloc& A, int s_cur, int s_next, const Pool& pool, const Ctx& cx, int64_t& l_chunk,
                 Group& cur) {
@@ -191,7 +203,7 @@ bool chunk_plan(int64_t L, const Alloc& A, int s_cur, int s_next, const Pool& po
     if (!get_group(pool, cx.node_size, cur, s_next, nxt)) return false;
     const double budget = max_queue(pool, nxt) - max_queue(pool, cur);
     const double x = std::min(static_cast<double>(L), solve_len(cx.model(s_cur), C, budget));
-    l_chunk = static_cast<int64_t>(std::floor(x / static_cast<double>(cx.granule))) * cx.granule;
+    l_chunk = whole_granules(x, cx.granule);
     return true;
 }
 

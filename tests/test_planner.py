@@ -139,7 +139,7 @@ def test_cpp_planner_matches_oracle_plan_for_plan():
         ref, ref_ttft = P.cdsp_schedule(L, [], S, queue, node, models, rate, granule)
         plan, ttft = api.schedule_prefill(L, [queue[i] for i in range(len(queue))], node, models, rate, granule)
         assert plan == [(c[0], list(c[1])) for c in ref]
-        assert ttft == ref_ttft
+        assert abs(ttft - ref_ttft) <= 1e-12 * abs(ref_ttft)  # plans exact; TTFT to rounding order
         n_multi += len(plan) > 1
         api.plan_partition(api.Plan(plan), len(plan) - 1)  # the library accepts its own plans
     assert n_multi >= 5
