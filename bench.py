@@ -4,13 +4,15 @@
 Workload (BASELINE.json configs[1]): 7B-shaped MHA (32 Q / 32 KV heads, d=128), a 32K-token
 prompt as ONE chunk, bf16, synthetic seeded inputs (cdsp_inputs.py).  On N GPUs the chunk
 runs at SP=N (one process per GPU, torchrun): at N=8 this is configs[1] exactly; total work
-is fixed, so scaling is "strong".  ``--weak`` instead holds 32K tokens per GPU (L = 32K*N).
+is fixed, so scaling is "strong".  ``--weak`` is BASELINE configs[4] / SURVEY M5: LLaMA3-8B-shaped
+GQA (32 Q / 8 KV heads), 64K tokens per GPU (L = 64K * N: the 512K prompt at N = 8).
 
 One step = one pass of the whole hot path over the chunk:
   a1 plan -> partition (host, cdsp_plan_partition)
   a2 zigzag gather of this rank's q/k/v shard from the full tensors (cdsp_zigzag_gather)
-  a4-a6 cdsp_prefill_chunk: store append, ring KV exchange (s>1), block attention with the
-        LSE merge fused into its epilogue
+  a4-a6 cdsp_prefill_chunk: store append, ring KV exchange (s>1: every pull issued up front
+        on the comm stream), ONE attention launch walking the rank's whole ring with O resident
+        in tensor memory (the LSE merge of R3 is the online softmax across blocks)
   a2 zigzag scatter of the output shard (cdsp_zigzag_scatter)
   a7 KV transfer into decode paged caches (cdsp_kv_transfer_to_decode), on a side stream
      concurrent with a4-a6 (the chunk's KV is final before its attention starts)
@@ -18,6 +20,8 @@ One step = one pass of the whole hot path over the chunk:
 
 value = algorithmic attention FLOPs of the chunk, 4*d*Hq*L(L+1)/2, over the
 step time (max over ranks, CUDA events).  Inputs (0.8 GB+) exceed the 126 MB L2.
+At s > 1 the same steps are timed again with CDSP_RING_CONTROL (peer blocks pre-staged in the
+receive slots, no pulls: SURVEY §8(d)'s control run); ring.hidden_ms = ring - control latency.
 """
 from __future__ import annotations
 
@@ -124,7 +128,18 @@ def oracle_sample(q, k, v, scale, n_rows, seed=11):
     return dt, flops, oracle.num_threads(), rows
 
 
-def cpu_baseline(q, k, v, scale, target_s=12.0):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(q, k, v, scale, total_flops, target_s=12.0):
     import oracle
     oracle.build()
     dt0, f0, _, _ = oracle_sample(q, k, v, scale, 16, seed=5)
@@ -132,10 +147,15 @@ def cpu_baseline(q, k, v, scale, target_s=12.0):
     per_row = f0 / 16
     n = int(max(16, min(4096, target_s * rate / per_row)))
     dt, fl, thr, rows = oracle_sample(q, k, v, scale, n)
-    return {"value": fl / dt / 1e12, "unit": UNIT, "cores": thr, "kind": "oracle",
+    value = fl / dt / 1e12
+    return {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle", "cpu_model": cpu_model(),
+            "nproc": os.cpu_count(),
             "sample": f"{len(rows)} seeded query rows x all {q.shape[1]} heads of the {q.shape[0]}-token "
                       f"workload (f64 C oracle, OpenMP), {dt:.1f} s; value = sample attention FLOPs / time",
-            "seconds": dt}
+            "seconds": dt,
+            "full_oracle_s_extrapolated": total_flops / (value * 1e12),
+            "full_oracle_note": "extrapolated: the whole chunk's algorithmic FLOPs at the sampled rate "
+                                "(the full oracle is not run)"}
 
 
 # ------------------------------------------------------------------------------ reference arm
@@ -174,10 +194,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--weak", action="store_true", help="hold 32K tokens per GPU (L = 32K * N)")
-    ap.add_argument("--seq", type=int, default=32768, help="prompt tokens (per GPU with --weak)")
+    ap.add_argument("--weak", action="store_true",
+                    help="configs[4] / M5: GQA 32/8, 64K tokens per GPU (L = 64K * N; 512K at N = 8)")
+    ap.add_argument("--seq", type=int, default=None, help="prompt tokens (per GPU with --weak)")
     ap.add_argument("--heads", type=int, default=32)
-    ap.add_argument("--kv-heads", type=int, default=32)
+    ap.add_argument("--kv-heads", type=int, default=None)
+    ap.add_argument("--no-control", action="store_true", help="skip the s > 1 control run (no pulls)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=48)
@@ -189,10 +211,13 @@ def main():
     if world != args.gpus:
         world = max(world, 1)
     s = world
-    L = args.seq * (s if args.weak else 1)
-    Hq, Hkv, D = args.heads, args.kv_heads, 128
+    seq = args.seq if args.seq is not None else (65536 if args.weak else 32768)
+    L = seq * (s if args.weak else 1)
+    Hq, D = args.heads, 128
+    Hkv = args.kv_heads if args.kv_heads is not None else (8 if args.weak else 32)
     cfg = {"L": L, "Hq": Hq, "Hkv": Hkv, "D": D, "scaling": "weak" if args.weak else "strong",
-           "config": {"workload": (f"weak: {args.seq} tokens per GPU, single chunk" if args.weak else
+           "config": {"workload": (f"weak (BASELINE configs[4] / M5 at N=8): {seq} tokens per GPU, "
+                                   f"{Hq}/{Hkv} q/kv heads, single chunk" if args.weak else
                                    "7B-shaped MHA 32K prompt, single chunk (BASELINE configs[1])"
                                    if (L, Hq, Hkv) == (32768, 32, 32) else
                                    f"{L // 1024}K prompt, {Hq}/{Hkv} q/kv heads, d=128, single chunk"),
@@ -247,9 +272,9 @@ def main():
     dst = api.DecodeTarget(kc, vc, B, bt)
     group = api.SpGroup(comm, plan, 0)
     # our kernels per step: s == 1: position fill + attention + paged scatter (k/v reach the
-    # store by copy engine); s > 1: 3 gathers, 2 peer barriers, store append, s attention
-    # steps, output scatter, paged scatter
-    launches_per_step = 3 if s == 1 else 3 + 2 + 1 + s + 1 + 1
+    # store by copy engine); s > 1: 3 gathers, 2 peer barriers, store append, the attention
+    # launch(es) (one for a fused ring), output scatter, paged scatter
+    launches_fixed = 2 if s == 1 else 3 + 2 + 1 + 1 + 1
 
     # a7 runs on its own stream: the chunk's KV is final once its shard exists, so the transfer
     # to the decode caches streams out while the attention computes ("dedicated ... streams";
@@ -262,7 +287,7 @@ def main():
     def step(qq=None, kk=None, vv=None, oo=None):
         qq, kk, vv, oo = (qq if qq is not None else q), (kk if kk is not None else k), \
             (vv if vv is not None else v), (oo if oo is not None else out_full)
-        api.plan_partition(plan, 0) if L <= 65536 else None  # a1 (host)
+        api.plan_partition(plan, 0)  # a1 (host)
         comm.reset(stream)
         if s == 1:
             # one rank: the zigzag partition (S_0 then S_1) is the identity, so the shard IS the
@@ -314,12 +339,33 @@ def main():
     attn_ms, attn_n = comm.profile_read()
     comm.profile(False)
     comm.check()
+    # control run (s > 1): the same steps with the peer blocks pre-staged (the receive slots
+    # hold what the timed steps pulled; identical inputs), no pulls
+    ctrl_ms = None
+    if s > 1 and not args.no_control:
+        comm.set_ring_options(api.RING_CONTROL)
+        step()
+        torch.cuda.synchronize()
+        barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for _ in range(args.steps):
+            step()
+        c1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ctrl_ms = c0.elapsed_time(c1)
+        comm.set_ring_options(0)
+        comm.check()
     if dist is not None:
-        ms, attn_avg, ring_ex, ring_cp = dist_utils.max_over_ranks(
-            [ms, attn_ms / max(attn_n, 1), ring_ex, ring_cp], device=None if shared is not None else dev)
+        ms, attn_avg, ring_ex, ring_cp, ctrl_ms = dist_utils.max_over_ranks(
+            [ms, attn_ms / max(attn_n, 1), ring_ex, ring_cp, ctrl_ms if ctrl_ms is not None else -1.0],
+            device=None if shared is not None else dev)
+        ctrl_ms = None if ctrl_ms < 0 else ctrl_ms
     else:
         attn_avg = attn_ms / max(attn_n, 1)
     ms_step = ms / args.steps
+    launches_per_step = launches_fixed + attn_n / args.steps
     flops = attn_flops(L, 0, Hq, D)
     value = flops / (ms_step * 1e-3) / 1e12
 
@@ -391,14 +437,15 @@ def main():
                "d2h_bytes_per_step": d2h, "ms_per_step": ems}
 
     peaks = load_peaks()
-    # dominant kernel: the block-attention launch(es) inside cdsp_prefill_chunk
-    per_launch_flops = flops / s / s if s > 1 else flops
+    # dominant kernel: the block-attention launch(es) inside cdsp_prefill_chunk; each rank's
+    # launches together cover its 1/s of the chunk's visible pairs (zigzag: equal work)
+    per_launch_flops = flops / s / max(attn_n / args.steps, 1.0)
     achieved = per_launch_flops / (attn_avg * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_attn_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(f"L{L}_H{Hq}_s{s}")
+            traffic = json.load(open(prof)).get(f"L{L}_H{Hq}_KV{Hkv}_s{s}")
         except Exception:
             traffic = None
     # Peak: the timed kernel launches add up to attn_ms (this rank).  A run whose kernel time
@@ -410,7 +457,9 @@ def main():
     peak = peaks["bf16_sustained"] if sustained else peaks["bf16_burst"]
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": UNIT,
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "attn_tc_kernel<128> (tcgen05/TMEM/TMA)", "avg_launch_ms": attn_avg,
+                "kernel": "attn_tc_kernel<128,PAIR> (tcgen05 cta_group::2 / TMEM / TMA)"
+                          + (" walking the rank's whole ring in one launch" if s > 1 else ""),
+                "avg_launch_ms": attn_avg,
                 "launches_timed": attn_n, "kernel_ms_timed": attn_ms,
                 "peak_note": f"{'bf16_tflops_sustained' if sustained else 'bf16_tflops (burst)'} of "
                              f"MEASURED_PEAKS.json ({peaks['source']}): the timed launches total "
@@ -422,17 +471,21 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": cfg["scaling"],
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": cfg["config"],
-            "roofline": roofline, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "roofline": roofline, "e2e": e2e, "gpu_launches": int(round(launches_per_step * args.steps)),
             "clocks": clk.summary(), "chunk_latency_ms": ms_step,
             "ring": None if s == 1 else {
                 "pulls_per_step": ring_n / args.steps, "bytes_per_step": ring_bytes / args.steps,
                 "pull_ms_per_step": ring_cp / args.steps, "exposed_ms_per_step": ring_ex / args.steps,
                 "pull_gbs": ring_bytes / max(ring_cp, 1e-9) / 1e6,
-                "note": "owner-pull copy-engine reads of peer stores over NVLink (CUDA IPC); exposed = "
-                        "compute-stream wait for pulls, max over ranks (0 = ring fully hidden)"},
+                "control_ms_per_step": None if ctrl_ms is None else ctrl_ms / args.steps,
+                "hidden_ms": None if ctrl_ms is None else ms_step - ctrl_ms / args.steps,
+                "note": "owner-pull copy-engine reads of peer stores over NVLink (CUDA IPC), all issued up "
+                        "front; exposed = compute-stream wait for pulls (event-gated launches), max over "
+                        "ranks; hidden_ms = step latency - control latency (control: peer blocks "
+                        "pre-staged, no pulls), max over ranks each; ~0 = ring fully hidden"},
             "tflops_per_gpu": value / world}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(q, k, v, 1.0 / math.sqrt(D))
+        line["cpu_baseline"] = cpu_baseline(q, k, v, 1.0 / math.sqrt(D), flops)
     if rank == 0:
         print(json.dumps(line), flush=True)
     comm.close()

@@ -45,7 +45,7 @@ extern "C" {
 #define CDSP_API
 #endif
 
-#define CDSP_ABI_VERSION 2
+#define CDSP_ABI_VERSION 3
 #define CDSP_IPC_HANDLE_BYTES 64   /* one cudaIpcMemHandle_t */
 #define CDSP_MAX_SP 8
 
@@ -102,17 +102,19 @@ typedef struct {
 
 /* ---------------------------------------------------------------------------------
  * Communicator: one per process per GPU ("instance").  It owns the instance's KV store
- * (history of the current request, in memory its peers can read over NVLink), the ring
- * receive double buffers, fp32 merge work buffers, an internal comm stream, events and
- * the peer barrier flags.
+ * (history of the current request, in memory its peers can read over NVLink), one ring
+ * receive slot per ring step, the optional fp32 merge accumulators (cdsp_comm_reserve), an
+ * internal comm stream, events, arrival flags and the peer barrier flags.
  * ------------------------------------------------------------------------------- */
 typedef struct cdsp_comm_s* cdsp_comm;
 
 /* Create the communicator of instance `rank` of `world` on CUDA device `device`.
  * store_cap_tokens: capacity (tokens) of this instance's KV store and of each ring
- * receive buffer; must cover the largest (history + shard) any chunk of any plan will
+ * receive slot; must cover the largest (history + shard) any chunk of any plan will
  * hold on one rank.  Hkv, D, dtype: KV geometry of every request served.  Allocates
- * 3 * store_cap_tokens * Hkv * D * sizeof(dtype) (+ small) bytes of device memory.
+ * 2 * world * store_cap_tokens * Hkv * D * sizeof(dtype) (+ small) bytes of device memory:
+ * the K and V store, plus one K and V receive slot per ring step (world - 1 of them; none
+ * when world == 1).  The fp32 merge accumulators are NOT allocated here (cdsp_comm_reserve).
  * Errors: CDSP_ERR_INVALID, CDSP_ERR_SHAPE (D not in {64,128}), CDSP_ERR_CUDA. */
 CDSP_API cdsp_status cdsp_comm_create(cdsp_comm* out, int32_t rank, int32_t world, int32_t device,
                                       int64_t store_cap_tokens, int32_t Hkv, int32_t D, int32_t dtype);
@@ -120,17 +122,46 @@ CDSP_API cdsp_status cdsp_comm_create(cdsp_comm* out, int32_t rank, int32_t worl
 /* Same with n_layers per-layer KV stores (one per transformer layer; positions shared): the
  * layer-wise prefill (cdsp_prefill_chunk_layer) overlaps each layer's cache balancing with
  * the previous layer ("Cache-Balancing Latency Overlap", Fig. 6-b).  Allocates
- * (2 n_layers + 4) * store_cap_tokens * Hkv * D * sizeof(dtype) (+ small) bytes. */
+ * (2 n_layers + 2 (world - 1)) * store_cap_tokens * Hkv * D * sizeof(dtype) (+ small) bytes. */
 CDSP_API cdsp_status cdsp_comm_create_layers(cdsp_comm* out, int32_t rank, int32_t world, int32_t device,
                                              int64_t store_cap_tokens, int32_t n_layers, int32_t Hkv, int32_t D,
                                              int32_t dtype);
+
+/* Reserve the fp32 merge accumulators (max_q_rows * max_hq * D + max_q_rows * max_hq floats)
+ * for rings that run as SEVERAL launches merged through them: f32 rings (one launch per
+ * block), bf16 rings whose blocks exceed one launch's KV tile list (4096 tiles of 128 keys at
+ * D = 128), and CDSP_RING_STEPWISE.  A bf16 ring that fits one launch needs none (its output
+ * stays in tensor memory across the whole ring).  Synchronises the device; grows only;
+ * never called by cdsp_prefill_chunk, which fails with CDSP_ERR_CAPACITY instead.
+ * Errors: CDSP_ERR_INVALID, CDSP_ERR_CUDA. */
+CDSP_API cdsp_status cdsp_comm_reserve(cdsp_comm c, int64_t max_q_rows, int32_t max_hq);
+
+/* Ring options (bits, default 0), for measurement and tests:
+ *  CDSP_RING_STEPWISE    one attention launch per ring step, merged through the reserved fp32
+ *                        accumulators (the round-1 design; control for the fused ring);
+ *  CDSP_RING_CONTROL     no pulls: the receive slots keep the blocks an earlier call with the
+ *                        same inputs pulled ("peer blocks pre-staged", SURVEY §8(d)'s control run:
+ *                        ring latency minus control latency = the exposed ring time);
+ *  CDSP_RING_GATE_FLAGS  gate the fused ring on arrival flags even when a peer shares this GPU
+ *                        (default: flags only when every peer is another GPU, else events;
+ *                        loopback groups then run their rings one at a time);
+ *  CDSP_RING_GATE_EVENTS always wait for a launch's pulls with events. */
+#define CDSP_RING_STEPWISE 1
+#define CDSP_RING_CONTROL 2
+#define CDSP_RING_GATE_FLAGS 4
+#define CDSP_RING_GATE_EVENTS 8
+CDSP_API cdsp_status cdsp_comm_set_ring_options(cdsp_comm c, int32_t options);
 
 /* Export this instance's shared region as CDSP_IPC_HANDLE_BYTES bytes (host buffer). */
 CDSP_API cdsp_status cdsp_comm_ipc_handle(cdsp_comm c, void* handle_out);
 
 /* Multi-process: open every other instance's region.  handles = world * CDSP_IPC_HANDLE_BYTES
  * host bytes, handle i from instance i (entry `rank` is ignored).  All instances must use
- * the same store_cap_tokens / Hkv / D / dtype.  Errors: CDSP_ERR_COMM, CDSP_ERR_CUDA. */
+ * the same world / store_cap_tokens / n_layers / Hkv / D / dtype: each region carries a
+ * geometry header, and a peer whose header differs is refused with CDSP_ERR_COMM (nothing
+ * is mapped into the peer's store at a wrong offset).  Peers on another GPU (by UUID) are
+ * marked remote: the fused ring then gates on arrival flags instead of events.
+ * Errors: CDSP_ERR_COMM, CDSP_ERR_CUDA. */
 CDSP_API cdsp_status cdsp_comm_connect(cdsp_comm c, const void* handles);
 
 /* Loopback: `world` communicators created in THIS process on ONE device (comms[i] has
@@ -368,13 +399,16 @@ typedef enum {
     CDSP_ATTN_MID = 2,    /* o_acc/lse_acc := merge(acc, this block)                     */
     CDSP_ATTN_LAST = 3    /* out/lse := merge(acc, this block)                           */
 } cdsp_attn_mode;
+/* OR-ed into the mode of a bf16 MID / LAST launch: launch it as a programmatic dependent of the
+ * preceding kernel in the stream.  It may then start while that kernel finishes its last work
+ * and touches o_acc / lse_acc / out / lse only after it completed, so the preceding kernel must
+ * not write q / k / v (use it to chain FIRST / MID / LAST launches; off by default). */
+#define CDSP_ATTN_PDL 0x100
 
 /* One block-attention launch: q [nq, Hq, D]; k, v [nkv, Hkv, D]; o_acc fp32 [nq, Hq, D] and
  * lse_acc fp32 [Hq, nq] (FIRST/MID/LAST); out [nq, Hq, D] dtype of q and lse fp32 [Hq, nq]
  * (ONLY/LAST; lse may be NULL).  bf16 runs the tcgen05/TMEM/TMA kernel, f32 the FFMA kernel.
- * MID / LAST (bf16) launch as programmatic dependents of the preceding kernel in the stream: they
- * may start while a preceding block-attention launch finishes its last units and touch o_acc /
- * lse_acc / out / lse only after it completed, so q / k / v must not be written by that launch.
+ * mode may carry CDSP_ATTN_PDL (see there).
  * Errors: CDSP_ERR_INVALID/SHAPE/DTYPE (host validation); CDSP_ERR_CAPACITY when a bf16 block has
  * more than 4096 KV tiles of 128 keys (512K keys per launch; split longer blocks with FIRST /
  * MID / LAST); CDSP_ERR_CUDA. */
@@ -382,6 +416,20 @@ CDSP_API cdsp_status cdsp_attention_fwd(const cdsp_tensor* q, const cdsp_tensor*
                                         const cdsp_segments* seg, float softmax_scale, int32_t mode,
                                         float* o_acc, float* lse_acc, cdsp_tensor* out, float* lse,
                                         void* cuda_stream);
+
+/* The same over nblk <= 8 KV blocks in ONE launch: the queries attend to the union of the blocks
+ * (block b: k[b], v[b] [nkv_b, Hkv, D], described by seg[b]; the query fields q_len0, q_pos0,
+ * q_pos1 and pos_stride of every seg[b] must equal seg[0]'s), walked in order with one online
+ * softmax per query row — the result is the R3 merge of the per-block attentions without any
+ * intermediate partial (a rank's local queries against every block of the ring; P:304
+ * "zigzag ring attention for historical tokens").  This is the kernel of a fused ring step
+ * sequence.  bf16 only for nblk > 1 (else CDSP_ERR_UNSUPPORTED); all blocks together <= 4096 KV
+ * tiles of 128 keys at D = 128 (else CDSP_ERR_CAPACITY).  Other arguments and errors as
+ * cdsp_attention_fwd. */
+CDSP_API cdsp_status cdsp_attention_fwd_blocks(const cdsp_tensor* q, int32_t nblk, const cdsp_tensor* const* k,
+                                               const cdsp_tensor* const* v, const cdsp_segments* seg,
+                                               float softmax_scale, int32_t mode, float* o_acc, float* lse_acc,
+                                               cdsp_tensor* out, float* lse, void* cuda_stream);
 
 /* Zigzag gather / scatter: full [L, H, D] <-> ring rank r's shard [2m, H, D]
  * (rows S_r then S_{2s-1-r}).  Bit-exact.  Errors: CDSP_ERR_SHAPE, CDSP_ERR_DTYPE. */

@@ -23,6 +23,8 @@ STATUS_NAMES = {0: "CDSP_OK", 1: "CDSP_ERR_INVALID", 2: "CDSP_ERR_SHAPE", 3: "CD
                 8: "CDSP_ERR_UNSUPPORTED"}
 CDSP_F32, CDSP_BF16 = 0, 1
 ATTN_ONLY, ATTN_FIRST, ATTN_MID, ATTN_LAST = 0, 1, 2, 3
+ATTN_PDL = 0x100
+RING_STEPWISE, RING_CONTROL, RING_GATE_FLAGS, RING_GATE_EVENTS = 1, 2, 4, 8
 IPC_HANDLE_BYTES = 64
 
 EXPORTED_SYMBOLS = (
@@ -34,6 +36,7 @@ EXPORTED_SYMBOLS = (
     "cdsp_comm_profile_read", "cdsp_decode_workspace_bytes", "cdsp_decode_attention", "cdsp_comm_profile_ring",
     "cdsp_comm_create_layers", "cdsp_kvstore_get_layer", "cdsp_prefill_chunk_layer",
     "cdsp_striped_gather", "cdsp_striped_scatter", "cdsp_fit_latency_model", "cdsp_schedule_prefill",
+    "cdsp_comm_reserve", "cdsp_comm_set_ring_options", "cdsp_attention_fwd_blocks",
 )
 
 
@@ -114,6 +117,11 @@ def lib():
             "cdsp_prefill_chunk_layer": [ctypes.POINTER(Tensor)] * 3 + [ctypes.POINTER(KvStoreC),
                                                                         ctypes.POINTER(SpGroupC), i32, f32,
                                                                         ctypes.POINTER(Tensor), P, P],
+            "cdsp_comm_reserve": [P, i64, i32],
+            "cdsp_comm_set_ring_options": [P, i32],
+            "cdsp_attention_fwd_blocks": [ctypes.POINTER(Tensor), i32, ctypes.POINTER(ctypes.POINTER(Tensor)),
+                                          ctypes.POINTER(ctypes.POINTER(Tensor)), ctypes.POINTER(Segments), f32, i32,
+                                          P, P, ctypes.POINTER(Tensor), P, P],
             "cdsp_comm_ipc_handle": [P, P],
             "cdsp_comm_connect": [P, P],
             "cdsp_comm_connect_local": [ctypes.POINTER(P), i32],
@@ -281,7 +289,8 @@ class KvStore:
 
 class Comm:
     def __init__(self, rank: int, world: int, device: int, store_cap_tokens: int, Hkv: int, D: int,
-                 dtype: torch.dtype = torch.bfloat16, n_layers: int = 1):
+                 dtype: torch.dtype = torch.bfloat16, n_layers: int = 1, max_q_rows: int = 0, max_hq: int = 0):
+        """cdsp_comm_create_layers (+ cdsp_comm_reserve(max_q_rows, max_hq) when both are given)."""
         self.rank, self.world, self.device = rank, world, device
         self.Hkv, self.D, self.dtype, self.n_layers = Hkv, D, dtype, n_layers
         h = ctypes.c_void_p()
@@ -290,6 +299,16 @@ class Comm:
         self.h = h
         self.cap = int(store_cap_tokens)
         self._stores = {}
+        if max_q_rows and max_hq:
+            self.reserve(max_q_rows, max_hq)
+
+    def reserve(self, max_q_rows: int, max_hq: int):
+        """cdsp_comm_reserve: fp32 merge accumulators for multi-launch rings."""
+        _check(lib().cdsp_comm_reserve(self.h, int(max_q_rows), int(max_hq)))
+
+    def set_ring_options(self, options: int):
+        """cdsp_comm_set_ring_options (RING_* bits)."""
+        _check(lib().cdsp_comm_set_ring_options(self.h, int(options)))
 
     def ipc_handle(self) -> bytes:
         buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
@@ -481,6 +500,23 @@ def attention_fwd(q, k, v, seg: Segments, softmax_scale: float = 0.0, mode: int 
     _check(lib().cdsp_attention_fwd(ctypes.byref(tq), ctypes.byref(tk), ctypes.byref(tv), ctypes.byref(seg),
                                     float(softmax_scale), mode, _ptr(o_acc), _ptr(lse_acc),
                                     ctypes.byref(to) if to is not None else None, _ptr(lse), _stream(stream)))
+    return out
+
+
+def attention_fwd_blocks(q, ks, vs, segs, softmax_scale: float = 0.0, mode: int = ATTN_ONLY,
+                         o_acc=None, lse_acc=None, out=None, lse=None, stream=None):
+    """cdsp_attention_fwd_blocks: q against the union of KV blocks (ks[b], vs[b], segs[b]) in one launch."""
+    n = len(ks)
+    tq = as_tensor(q)
+    tk = [as_tensor(x) for x in ks]
+    tv = [as_tensor(x) for x in vs]
+    pk = (ctypes.POINTER(Tensor) * n)(*[ctypes.pointer(t) for t in tk])
+    pv = (ctypes.POINTER(Tensor) * n)(*[ctypes.pointer(t) for t in tv])
+    sg = (Segments * n)(*segs)
+    to = as_tensor(out) if out is not None else None
+    _check(lib().cdsp_attention_fwd_blocks(ctypes.byref(tq), n, pk, pv, sg, float(softmax_scale), mode,
+                                           _ptr(o_acc), _ptr(lse_acc), ctypes.byref(to) if to is not None else None,
+                                           _ptr(lse), _stream(stream)))
     return out
 
 

@@ -160,13 +160,14 @@ template <int HD>
 cdsp_status launch_simt(const AttnArgs& a, cudaStream_t st) {
     SimtParams p;
     p.q = static_cast<const float*>(a.q);
-    p.k = static_cast<const float*>(a.k);
-    p.v = static_cast<const float*>(a.v);
-    p.seg = a.seg;
+    CDSP_REQUIRE(a.nblk == 1, CDSP_ERR_UNSUPPORTED, "the fp32 kernel takes one KV block per launch");
+    p.k = static_cast<const float*>(a.k[0]);
+    p.v = static_cast<const float*>(a.v[0]);
+    p.seg = a.seg[0];
     p.Hq = a.Hq;
     p.Hkv = a.Hkv;
     p.g = a.Hq / a.Hkv;
-    p.n_rb = static_cast<int>((a.seg.nq + SB_M - 1) / SB_M);
+    p.n_rb = static_cast<int>((a.seg[0].nq + SB_M - 1) / SB_M);
     p.scale_log2 = a.scale * 1.4426950408889634f;
     p.mode = a.mode;
     p.o_acc = a.o_acc;

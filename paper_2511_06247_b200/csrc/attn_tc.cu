@@ -51,6 +51,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "attn_common.cuh"
 #include "common.cuh"
@@ -106,6 +107,7 @@ constexpr int BN = 128;                 // KV rows per tile
 constexpr int NSB = 3;                  // S/P buffers in TMEM
 constexpr int kBox = 128 * 128;         // TMA box: 128 rows x 64 bf16 (128-byte swizzle rows)
 constexpr int kSchedMax = 8192;         // KV tiles per launch (1M keys)
+constexpr int kMaxBlk = CDSP_MAX_SP;    // KV blocks one launch walks (a rank's whole ring)
 constexpr int W_K = 4 * NG, W_V = 4 * NG + 1, W_MMA = 4 * NG + 2;
 
 // PAIR: 2-SM variant (HD = 128).  A CTA pair (cluster of 2) runs M = 256 MMAs (cta_group::2):
@@ -154,14 +156,33 @@ struct Layout {
     // [2][LISTMAX] used KV tiles of the unit in order: tile index | 0x8000 if partial
     static constexpr int LISTMAX = HD == 64 ? kSchedMax : kSchedMax / 2;
     static constexpr int OFF_SCHED = OFF_UNIT + 2 * 16;
-    static constexpr int SMEM = OFF_SCHED + 2 * LISTMAX * 2 + 1024;  // + alignment slack
+    // KV blocks of the launch: segment descriptors [kMaxBlk] and first-tile offsets [kMaxBlk + 1]
+    static constexpr int OFF_SEG = OFF_SCHED + 2 * LISTMAX * 2;
+    static constexpr int OFF_TOFF = OFF_SEG + kMaxBlk * static_cast<int>(sizeof(cdsp_segments));
+    static constexpr int SMEM = OFF_TOFF + (kMaxBlk + 1) * 4 + 1024;  // + alignment slack
 };
 
 constexpr uint32_t COL_O = 0;
 __host__ __device__ constexpr uint32_t col_s(int b) { return 128u + 128u * b; }
 
+// A launch walks nblk KV blocks (a ring rank's own store and its peers' stores: P:59 each
+// instance "interact[s] local query tensors with full key-value tensors"): every unit's tile
+// list runs through block 0, 1, ... in order, with O and the row statistics resident in TMEM /
+// registers across blocks, so one launch covers the rank's whole ring.  seg[b] describes
+// block b (its query fields are the same in every block); the unit lists use launch-global
+// tile ids, block b's tiles being [tile_off[b], tile_off[b + 1]).
 struct TcParams {
-    cdsp_segments seg;
+    cdsp_segments seg[kMaxBlk];
+    int tile_off[kMaxBlk + 1];
+    int nblk;
+    // Arrival gating (ring pulls landing while the launch runs): the first K / V tile of block
+    // b (bit b of gate_mask) for KV head kvh is loaded only once
+    // gate[b * gate_ng + kvh / gate_hpg] has reached gate_target (written by the stream that
+    // pulls the block, behind the pull); a wait longer than ~3 s sets *gate_err and proceeds.
+    const uint32_t* gate;
+    uint32_t gate_target, gate_mask;
+    int gate_ng, gate_hpg;
+    int* gate_err;
     int Hq, Hkv, g, n_rb, n_units;
     float scale_log2;
     int mode;
@@ -321,6 +342,15 @@ __device__ __forceinline__ void mask_cols(uint32_t* s, const cdsp_segments& sg, 
     }
 }
 
+// mask_cols for launch-global tile id gt (block b: tiles [toff[b], toff[b + 1]))
+template <int NW>
+__device__ __forceinline__ void mask_tile(uint32_t* s, const cdsp_segments* segs, const int* toff, int gt, int64_t qpos,
+                                          int col0) {
+    int b = 0;
+    while (gt >= toff[b + 1]) ++b;
+    mask_cols<NW>(s, segs[b], gt - toff[b], qpos, col0);
+}
+
 __device__ __forceinline__ float fmax3(float a, float b, float c) {  // FMNMX3 (sm_100)
     float r;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -340,8 +370,23 @@ __device__ __forceinline__ float max64(const uint32_t* s) {
     return fmax3(fmax3(a[0], a[1], a[2]), fmax3(a[3], a[4], a[5]), fmaxf(a[6], a[7]));
 }
 
+// lacc += the two bf16 halves of pk, widened exactly (FHADD.BF16: one instruction per half).
+__device__ __forceinline__ void add_bf16x2(float2& lacc, uint32_t pk) {
+    asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+        "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %1, hi, %1;\n\t}"
+        : "+f"(lacc.x), "+f"(lacc.y)
+        : "r"(pk));
+}
+
 // p = 2^(s*sl2 - m) for 32 scores -> 16 bf16 pairs stored to TMEM columns tP .. tP+15 (two
 // tcgen05.st x8); row sum accumulated in lacc.  Pairs selected by CDSP_EMU_MASK run on the FMA pipe.
+// CDSP_SUM_ROUNDED=1 (measured, not the default): the row sum adds the bf16-ROUNDED p the PV
+// MMA consumes (FHADD.BF16), so numerator and denominator share their rounding.  Same box:
+// 3-7% slower, sharp-q max-abs out 0.021 -> 0.011, but the LSE then carries the bf16 rounding
+// of the p (1.3e-3 > the 1e-3 bound); the fp32 sum is kept.
+#ifndef CDSP_SUM_ROUNDED
+#define CDSP_SUM_ROUNDED 0
+#endif
 __device__ __forceinline__ void exp32_store(const uint32_t* s, float2 sc, float2 nm, float2& lacc, uint32_t tP) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -361,8 +406,12 @@ __device__ __forceinline__ void exp32_store(const uint32_t* s, float2 sc, float2
                 pp.y = ex2(x.y);
 #endif
             }
-            lacc = fadd2(lacc, pp);
             pk[ii] = pack_bf16(pp.x, pp.y);
+#if CDSP_SUM_ROUNDED
+            add_bf16x2(lacc, pk[ii]);
+#else
+            lacc = fadd2(lacc, pp);
+#endif
         }
 #if defined(CDSP_DBG_SOFTMAX) && CDSP_DBG_SOFTMAX == 2
         lacc.x += __uint_as_float(pk[0] ^ pk[1] ^ pk[2] ^ pk[3] ^ pk[4] ^ pk[5] ^ pk[6] ^ pk[7]);
@@ -481,11 +530,34 @@ __device__ __forceinline__ void warp_rows_store64(const uint32_t* v, float* base
     __syncwarp();
 }
 
+// TMA descriptors: queries, bf16 output, and K / V of every block (kernel-parameter space)
+struct TcMaps {
+    CUtensorMap q, out;
+    CUtensorMap k[kMaxBlk], v[kMaxBlk];
+};
+
+// Block b of the unit's KV walk has arrived: spin (acquire, system scope: the block is written
+// by copy engines, possibly of a peer GPU) until the gate word reaches the target, then order
+// the async proxy (TMA) after it.
+__device__ __forceinline__ void gate_wait(const TcParams& p, int b, int kvh) {
+    const uint32_t* f = p.gate + b * p.gate_ng + kvh / p.gate_hpg;
+    const uint64_t t0 = globaltimer();
+    for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (static_cast<int32_t>(v - p.gate_target) >= 0) break;
+        if (globaltimer() - t0 > 3000000000ull) {  // before the 4 s mbarrier watchdogs of the other warps
+            atomicExch(p.gate_err, 3);
+            break;
+        }
+        __nanosleep(128);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 template <int HD, bool PAIR>
 __global__ void __maxnreg__(CDSP_MAXNREG)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_out,
-                   const TcParams p) {
+    attn_tc_kernel(const __grid_constant__ TcMaps tm, const __grid_constant__ TcParams p) {
     using L = Layout<HD, PAIR>;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
@@ -499,8 +571,9 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
     UnitInfo* uinfo = reinterpret_cast<UnitInfo*>(smem + L::OFF_UNIT);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const cdsp_segments& sg = p.seg;
-    const int n_kv_tiles = static_cast<int>((sg.nkv + BN - 1) / BN);
+    const cdsp_segments* segs = reinterpret_cast<const cdsp_segments*>(smem + L::OFF_SEG);
+    const int* toff = reinterpret_cast<const int*>(smem + L::OFF_TOFF);
+    const cdsp_segments& sg = segs[0];  // query fields (the same in every block)
     constexpr int CL = PAIR ? 2 : 1;
     const int crank = PAIR ? static_cast<int>(cluster_ctarank()) : 0;
     const bool leader = crank == 0;
@@ -542,11 +615,19 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 mbar_init(bar(L::B_LE + i), 4);
             }
             fence_barrier_init();
-            tma_prefetch_desc(&tm_q);
-            tma_prefetch_desc(&tm_k);
-            tma_prefetch_desc(&tm_v);
-            if (PAIR) tma_prefetch_desc(&tm_out);
+            tma_prefetch_desc(&tm.q);
+            for (int b = 0; b < p.nblk; ++b) {
+                tma_prefetch_desc(&tm.k[b]);
+                tma_prefetch_desc(&tm.v[b]);
+            }
+            if (PAIR) tma_prefetch_desc(&tm.out);
         }
+        // block table into shared memory (read by the producers and on partial tiles)
+        const int64_t* src = reinterpret_cast<const int64_t*>(p.seg);
+        int64_t* dst = reinterpret_cast<int64_t*>(smem + L::OFF_SEG);
+        constexpr int nw = kMaxBlk * static_cast<int>(sizeof(cdsp_segments)) / 8;
+        for (int i = lane; i < nw; i += 32) dst[i] = src[i];
+        for (int i = lane; i <= kMaxBlk; i += 32) reinterpret_cast<int*>(smem + L::OFF_TOFF)[i] = p.tile_off[i];
     } else if (warp == W_MMA) {
         if constexpr (PAIR) {
             tmem_alloc2(smem_u32(tmem_slot), 512);
@@ -611,20 +692,24 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 seg_qrange(sg, prow0, prow0 + BM, plo, phi, pany);
             }
             int cnt = 0;
-            for (int j0 = 0; j0 < n_kv_tiles; j0 += 32) {  // 32 tiles per step, compacted in order
-                const int j = j0 + lane;
-                int k = TILE_EMPTY;
-                if (j < n_kv_tiles) {
-                    k = seg_tile_kind(sg, qany, qlo, qhi, static_cast<int64_t>(j) * BN, BN);
-                    if (PAIR && k == TILE_EMPTY &&
-                        seg_tile_kind(sg, pany, plo, phi, static_cast<int64_t>(j) * BN, BN) != TILE_EMPTY)
-                        k = TILE_PARTIAL;  // needed by the peer only: fully masked here
+            for (int b = 0; b < p.nblk; ++b) {  // blocks in walk order, each block's tiles in order
+                const cdsp_segments& sb = segs[b];
+                const int t0 = toff[b], nt = toff[b + 1] - t0;
+                for (int j0 = 0; j0 < nt; j0 += 32) {  // 32 tiles per step, compacted in order
+                    const int j = j0 + lane;
+                    int k = TILE_EMPTY;
+                    if (j < nt) {
+                        k = seg_tile_kind(sb, qany, qlo, qhi, static_cast<int64_t>(j) * BN, BN);
+                        if (PAIR && k == TILE_EMPTY &&
+                            seg_tile_kind(sb, pany, plo, phi, static_cast<int64_t>(j) * BN, BN) != TILE_EMPTY)
+                            k = TILE_PARTIAL;  // needed by the peer only: fully masked here
+                    }
+                    const uint32_t used = __ballot_sync(0xFFFFFFFFu, k != TILE_EMPTY);
+                    if (k != TILE_EMPTY)
+                        list[cnt + __popc(used & ((1u << lane) - 1u))] =
+                            static_cast<uint16_t>((t0 + j) | (k == TILE_PARTIAL ? kPartialBit : 0));
+                    cnt += __popc(used);
                 }
-                const uint32_t used = __ballot_sync(0xFFFFFFFFu, k != TILE_EMPTY);
-                if (k != TILE_EMPTY)
-                    list[cnt + __popc(used & ((1u << lane) - 1u))] =
-                        static_cast<uint16_t>(j | (k == TILE_PARTIAL ? kPartialBit : 0));
-                cnt += __popc(used);
             }
             // query positions (only read on partial tiles)
             int64_t* qp = reinterpret_cast<int64_t*>(smem + L::OFF_QP) + ub * BM;
@@ -646,10 +731,10 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                     const uint32_t dst = sQ + qb * L::TILE;
                     for (int b = 0; b < L::NBOX; ++b) {
                         if constexpr (PAIR)
-                            tma_load_3d_2sm(dst + b * kBox, &tm_q, lbar(L::B_QF + qb), b * 64, head, static_cast<int>(row0),
+                            tma_load_3d_2sm(dst + b * kBox, &tm.q, lbar(L::B_QF + qb), b * 64, head, static_cast<int>(row0),
                                             pol_q);
                         else
-                            tma_load_3d(dst + b * kBox, &tm_q, bar(L::B_QF + qb), b * 64, head, static_cast<int>(row0));
+                            tma_load_3d(dst + b * kBox, &tm.q, bar(L::B_QF + qb), b * 64, head, static_cast<int>(row0));
                     }
                 }
                 // merge modes: pull this unit's accumulator rows into L2 for the epilogue
@@ -665,8 +750,17 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 ++n_ne;
             }
             __syncwarp();
+            int blk = 0;  // block of the current list entry (the list runs through blocks in order)
+            uint32_t gated = 0;  // gated blocks already seen arrived (this unit)
             for (int n = 0; n < cnt; ++n) {
-                const int j = list[n] & ~kPartialBit;
+                const int gt = list[n] & ~kPartialBit;
+                while (gt >= toff[blk + 1]) ++blk;
+                const int j = gt - toff[blk];
+                if (((p.gate_mask & ~gated) >> blk) & 1u) {
+                    if (lane == 0) gate_wait(p, blk, kvh);
+                    __syncwarp();
+                    gated |= 1u << blk;
+                }
                 const int st = it % L::KST;
                 // stage st last held tile it - 3: free once S(it - 3) is done (in both CTAs)
                 if (it >= L::KST) mbar_wait_backoff(bar(L::B_SF + st), ((it - L::KST) / L::KST) & 1);
@@ -676,13 +770,13 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                         // this CTA's 64 keys of the tile, both d halves
                         if (leader) mbar_expect_tx(bar(L::B_KF + st), 2 * L::KTILE);
                         for (int b = 0; b < L::NBOX; ++b)
-                            tma_load_3d_2sm(sK + st * L::KTILE + b * (kBox / 2), &tm_k, lbar(L::B_KF + st), b * 64, kvh,
-                                            j * BN + crank * (BN / 2), pol_kv);
+                            tma_load_3d_2sm(sK + st * L::KTILE + b * (kBox / 2), &tm.k[blk], lbar(L::B_KF + st), b * 64,
+                                            kvh, j * BN + crank * (BN / 2), pol_kv);
                     } else {
                         mbar_expect_tx(bar(L::B_KF + st), L::KTILE);
                         for (int b = 0; b < L::NBOX; ++b)
-                            tma_load_3d_hint(sK + st * L::KTILE + b * kBox, &tm_k, bar(L::B_KF + st), b * 64, kvh, j * BN,
-                                             pol_kv);
+                            tma_load_3d_hint(sK + st * L::KTILE + b * kBox, &tm.k[blk], bar(L::B_KF + st), b * 64, kvh,
+                                             j * BN, pol_kv);
                     }
                 }
                 __syncwarp();
@@ -711,20 +805,30 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             if (u.x < 0) break;
             const int kvh = (u.x / p.n_pb) / p.g;
             const uint16_t* list = reinterpret_cast<const uint16_t*>(smem + L::OFF_SCHED) + ub * L::LISTMAX;
+            int blk = 0;
+            uint32_t gated = 0;
             for (int n = 0; n < u.n_used; ++n) {
-                const int j = list[n] & ~kPartialBit;
+                const int gt = list[n] & ~kPartialBit;
+                while (gt >= toff[blk + 1]) ++blk;
+                const int j = gt - toff[blk];
+                if (((p.gate_mask & ~gated) >> blk) & 1u) {
+                    if (lane == 0) gate_wait(p, blk, kvh);
+                    __syncwarp();
+                    gated |= 1u << blk;
+                }
                 const int st = it % L::VST;
                 if (it >= L::VST) mbar_wait_backoff(bar(L::B_VE + st), ((it - L::VST) / L::VST) & 1);
                 if (lane == 0) KTRACE(14, it);
                 if (elect_one()) {
                     if constexpr (PAIR) {  // all 128 keys, this CTA's 64 d columns
                         if (leader) mbar_expect_tx(bar(L::B_VF + st), 2 * L::VTILE);
-                        tma_load_3d_2sm(sV + st * L::VTILE, &tm_v, lbar(L::B_VF + st), crank * 64, kvh, j * BN, pol_kv);
+                        tma_load_3d_2sm(sV + st * L::VTILE, &tm.v[blk], lbar(L::B_VF + st), crank * 64, kvh, j * BN,
+                                        pol_kv);
                     } else {
                         mbar_expect_tx(bar(L::B_VF + st), L::VTILE);
                         for (int b = 0; b < L::NBOX; ++b)
-                            tma_load_3d_hint(sV + st * L::VTILE + b * kBox, &tm_v, bar(L::B_VF + st), b * 64, kvh, j * BN,
-                                             pol_kv);
+                            tma_load_3d_hint(sV + st * L::VTILE + b * kBox, &tm.v[blk], bar(L::B_VF + st), b * 64, kvh,
+                                             j * BN, pol_kv);
                     }
                 }
                 __syncwarp();
@@ -861,7 +965,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             for (int n = n_first; n < N; n += NG) {
                 const int gn = gn0 + n;
                 const uint32_t e = list[n];
-                const int j = static_cast<int>(e & ~kPartialBit);
+                const int j = static_cast<int>(e & ~kPartialBit);  // launch-global tile id
                 const bool partial = (e & kPartialBit) != 0;
                 const int b = gn % NSB;
                 const uint32_t tS = tmem + lane_off + col_s(b);
@@ -893,7 +997,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 reg_tie32(s + 32);
                 reg_tie32(s + 64);
                 reg_tie32(s + 96);
-                if (partial) mask_cols<4>(s, sg, j, qp[r], 0);
+                if (partial) mask_tile<4>(s, segs, toff, j, qp[r], 0);
                 const float mx = fmaxf(max64(s), max64(s + 64)) * sl2;
 #else
                 uint32_t s[64];
@@ -902,14 +1006,14 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 tc_wait_ld();
                 reg_tie32(s);
                 reg_tie32(s + 32);
-                if (partial) mask_cols<2>(s, sg, j, qp[r], 64);
+                if (partial) mask_tile<2>(s, segs, toff, j, qp[r], 64);
                 const float mx_hi = max64(s);
                 tmem_ld32p(tS, s);
                 tmem_ld32p(tS + 32, s + 32);
                 tc_wait_ld();
                 reg_tie32(s);
                 reg_tie32(s + 32);
-                if (partial) mask_cols<2>(s, sg, j, qp[r], 0);
+                if (partial) mask_tile<2>(s, segs, toff, j, qp[r], 0);
                 const float mx = fmaxf(mx_hi, max64(s)) * sl2;
 #endif
 #ifdef CDSP_KTRACE
@@ -985,11 +1089,11 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 tc_wait_ld();
                 reg_tie32(s);
                 tmem_ld32p(tS + 96, s + 32);
-                if (partial) mask_cols<1>(s, sg, j, qp[r], 64);
+                if (partial) mask_tile<1>(s, segs, toff, j, qp[r], 64);
                 exp32_store(s, sc, nm, lacc, tS + 32);
                 tc_wait_ld();
                 reg_tie32(s + 32);
-                if (partial) mask_cols<1>(s + 32, sg, j, qp[r], 96);
+                if (partial) mask_tile<1>(s + 32, segs, toff, j, qp[r], 96);
                 exp32_store(s + 32, sc, nm, lacc, tS + 48);
 #endif
                 if (lane == 0 && quad == 0) KTRACE(4 * g + 2, gn);
@@ -1162,7 +1266,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 named_bar_sync(8 + g, BM);  // this group's 128 rows are in the boxes
                 if (threadIdx.x == static_cast<unsigned>(g * BM)) {
                     for (int hh = 0; hh < HD / 64; ++hh)
-                        tma_store_3d(&tm_out, stg0 + static_cast<uint32_t>(hh) * (BM * 128), 64 * hh, head,
+                        tma_store_3d(&tm.out, stg0 + static_cast<uint32_t>(hh) * (BM * 128), 64 * hh, head,
                                      static_cast<int>(row0));  // rows >= nq clipped
                     bulk_commit();
                     bulk_wait_read0();  // the boxes are free again (the next unit may finish in another group)
@@ -1298,14 +1402,30 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
             max_groups = sm_count();
         }
     }
-    CDSP_REQUIRE((a.seg.nkv + BN - 1) / BN <= Lt::LISTMAX, CDSP_ERR_CAPACITY, "KV block of %lld rows exceeds %d",
-                 static_cast<long long>(a.seg.nkv), Lt::LISTMAX * BN);
+    CDSP_REQUIRE(a.nblk >= 1 && a.nblk <= kMaxBlk, CDSP_ERR_INVALID, "%d KV blocks (1..%d)", a.nblk, kMaxBlk);
+    const cdsp_segments& s0 = a.seg[0];
     TcParams p;
-    p.seg = a.seg;
+    std::memset(&p, 0, sizeof(p));
+    p.nblk = a.nblk;
+    int64_t tiles = 0;
+    for (int b = 0; b < a.nblk; ++b) {
+        p.seg[b] = a.seg[b];
+        p.tile_off[b] = static_cast<int>(tiles);
+        tiles += (a.seg[b].nkv + BN - 1) / BN;
+        CDSP_REQUIRE(tiles <= Lt::LISTMAX, CDSP_ERR_CAPACITY, "KV blocks of %lld tiles exceed %d per launch",
+                     static_cast<long long>(tiles), Lt::LISTMAX);
+    }
+    for (int b = a.nblk; b <= kMaxBlk; ++b) p.tile_off[b] = static_cast<int>(tiles);
+    p.gate = a.gate;
+    p.gate_target = a.gate_target;
+    p.gate_mask = a.gate ? a.gate_mask : 0u;
+    p.gate_ng = a.gate_ng > 0 ? a.gate_ng : 1;
+    p.gate_hpg = a.gate_hpg > 0 ? a.gate_hpg : 1;
+    p.gate_err = a.gate_err;
     p.Hq = a.Hq;
     p.Hkv = a.Hkv;
     p.g = a.Hq / a.Hkv;
-    p.n_rb = static_cast<int>((a.seg.nq + BM - 1) / BM);
+    p.n_rb = static_cast<int>((s0.nq + BM - 1) / BM);
     p.n_pb = PAIR ? (p.n_rb + 1) / 2 : p.n_rb;
     const int64_t units = static_cast<int64_t>(p.n_pb) * a.Hq;
     if (units == 0) return CDSP_OK;
@@ -1318,18 +1438,25 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     p.out = static_cast<__nv_bfloat16*>(a.out);
     p.lse = a.lse;
     CDSP_CHECK_STATUS(claim_slot(&p.claim));
-    CUtensorMap mq, mk, mv;
-    CDSP_CHECK_STATUS(make_map(&mq, a.q, a.seg.nq, a.Hq, HD));
-    const void* kb = a.seg.nkv > 0 ? a.k : a.q;  // nkv == 0: map never dereferenced
-    const void* vb = a.seg.nkv > 0 ? a.v : a.q;
-    // PAIR: each CTA loads 64 of a K tile's 128 keys (and 64 of V's 128 d columns)
-    CDSP_CHECK_STATUS(make_map(&mk, kb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD, PAIR ? BN / 2 : BN));
-    CDSP_CHECK_STATUS(make_map(&mv, vb, a.seg.nkv, a.seg.nkv > 0 ? a.Hkv : a.Hq, HD));
-    CUtensorMap mo = mq;  // bf16 output (staged epilogue); never dereferenced in fp32-result modes
+    TcMaps tm;
+    std::memset(&tm, 0, sizeof(tm));
+    CDSP_CHECK_STATUS(make_map(&tm.q, a.q, s0.nq, a.Hq, HD));
+    for (int b = 0; b < a.nblk; ++b) {
+        const bool has = a.seg[b].nkv > 0;
+        const void* kb = has ? a.k[b] : a.q;  // nkv == 0: map never dereferenced
+        const void* vb = has ? a.v[b] : a.q;
+        // PAIR: each CTA loads 64 of a K tile's 128 keys (and 64 of V's 128 d columns)
+        CDSP_CHECK_STATUS(make_map(&tm.k[b], kb, a.seg[b].nkv, has ? a.Hkv : a.Hq, HD, PAIR ? BN / 2 : BN));
+        CDSP_CHECK_STATUS(make_map(&tm.v[b], vb, a.seg[b].nkv, has ? a.Hkv : a.Hq, HD));
+    }
+    tm.out = tm.q;  // bf16 output (staged epilogue); never dereferenced in fp32-result modes
     if (PAIR && (a.mode == CDSP_ATTN_ONLY || a.mode == CDSP_ATTN_LAST))
-        CDSP_CHECK_STATUS(make_map(&mo, a.out, a.seg.nq, a.Hq, HD));
-    // persistent: one CTA per SM (TMEM and shared memory admit one), units claimed dynamically
-    const int groups = static_cast<int>(units < max_groups ? units : max_groups);
+        CDSP_CHECK_STATUS(make_map(&tm.out, a.out, s0.nq, a.Hq, HD));
+    // persistent: one CTA per SM (TMEM and shared memory admit one), units claimed dynamically;
+    // spare_sms leaves SMs to kernels this launch waits on (gated blocks copied by SM kernels)
+    int cap_groups = max_groups - (a.spare_sms + (PAIR ? 1 : 0)) / (PAIR ? 2 : 1);
+    if (cap_groups < 1) cap_groups = 1;
+    const int groups = static_cast<int>(units < cap_groups ? units : cap_groups);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1340,20 +1467,21 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = Lt::SMEM;
     cfg.stream = st;
-    // MID / LAST steps depend on the previous launch only through the accumulator, read and
-    // written after griddepcontrol.wait, so they are launched as programmatic dependents and
-    // start under its tail (CDSP_PDL=0: plain stream order, measurement control)
-    static const bool pdl = !(getenv("CDSP_PDL") != nullptr && getenv("CDSP_PDL")[0] == '0');
+    // MID / LAST steps of an internal ring chain depend on the previous launch only through the
+    // accumulator, read and written after griddepcontrol.wait, so they may be launched as
+    // programmatic dependents and start under its tail (CDSP_PDL=0: plain stream order,
+    // measurement control)
+    static const bool pdl_env = !(getenv("CDSP_PDL") != nullptr && getenv("CDSP_PDL")[0] == '0');
     int na = 0;
     if (PAIR) at[na++] = at[0];
-    if (pdl && (a.mode == CDSP_ATTN_MID || a.mode == CDSP_ATTN_LAST)) {
+    if (a.pdl && pdl_env && (a.mode == CDSP_ATTN_MID || a.mode == CDSP_ATTN_LAST)) {
         at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
     }
     cfg.attrs = at;
     cfg.numAttrs = na;
-    CDSP_CUDA(cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mo, p));
+    CDSP_CUDA(cudaLaunchKernelEx(&cfg, kern, tm, p));
 #ifdef CDSP_KTRACE
     if (const char* path = getenv("CDSP_TRACE")) {  // debug builds only: synchronous dump
         static unsigned long long c[65536 * 8], it[4 * 512 * 16];
@@ -1371,6 +1499,17 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
+
+int attention_tc_max_tiles(int D) {
+    static const bool no_pair = getenv("CDSP_ATTN_1SM") != nullptr;
+    int n = D == 128 ? (no_pair ? Layout<128, false>::LISTMAX : Layout<128, true>::LISTMAX) : Layout<64, false>::LISTMAX;
+    // test knob: a smaller per-launch tile budget makes small rings take the multi-launch path
+    if (const char* e = getenv("CDSP_MAX_TILES")) {
+        const int m = atoi(e);
+        if (m >= 1 && m < n) n = m;
+    }
+    return n;
+}
 
 cdsp_status launch_attention_tc(const AttnArgs& a, cudaStream_t st) {
 #ifndef CDSP_NO_PAIR

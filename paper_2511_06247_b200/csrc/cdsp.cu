@@ -15,6 +15,7 @@
 //       hop, so the logical ring needs no store-and-forward), overlapped with step k-1's
 //       attention; each step's attention LSE-merges into fp32 accumulators in its epilogue
 //       and the last step writes the output.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -46,6 +47,19 @@ using namespace cdsp;
 
 namespace {
 constexpr int kMaxWorld = 8;
+constexpr int kMaxHG = 8;  // head groups a gated pull is split into
+
+// Geometry header every communicator writes into its exported region (after the flag
+// counters), so cdsp_comm_connect can refuse a peer whose store offsets differ.
+struct RegionHeader {
+    uint64_t magic;
+    int32_t abi, n_layers, Hkv, D, dtype, world;
+    int64_t cap;
+    uint64_t region_bytes, off_v, off_pos, off_flags;
+    unsigned char uuid[16];  // the GPU holding the region
+};
+constexpr uint64_t kRegionMagic = 0x43445350'52454731ull;  // "CDSPREG1"
+constexpr size_t kHeaderOff = 2 * kMaxWorld * sizeof(unsigned long long);  // within the flag page
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -93,19 +107,27 @@ struct cdsp_comm_s {
     void* ipc_base[kMaxWorld] = {nullptr};
     bool connected = false;
     // local buffers
-    void* recv = nullptr;  // 2 x (K, V) receive buffers, cap rows each
-    char* recv_k[2] = {nullptr, nullptr};
-    char* recv_v[2] = {nullptr, nullptr};
-    float* o_acc = nullptr;
+    void* recv = nullptr;  // (world - 1) x (K, V) receive slots, cap rows each: slot k-1 takes ring step k's block
+    char* recv_k[kMaxWorld] = {};
+    char* recv_v[kMaxWorld] = {};
+    int n_slots = 0;
+    float* o_acc = nullptr;  // fp32 merge accumulators (cdsp_comm_reserve); only multi-launch rings use them
     float* lse_acc = nullptr;
-    size_t acc_elems = 0, lse_elems = 0;
+    int64_t acc_rows = 0;
+    int32_t acc_hq = 0;
+    // ring arrival gating (fused ring over cross-device pulls): gate[k * kMaxHG + hg]
+    uint32_t* gate = nullptr;
+    uint32_t gate_seq = 0;
+    bool peer_remote[kMaxWorld] = {};  // peer j lives on another GPU (copy-engine pulls over NVLink)
+    int32_t ring_opts = 0;             // CDSP_RING_* option bits (cdsp_comm_set_ring_options)
+    cudaEvent_t ev_pull[kMaxWorld] = {};
+    cudaEvent_t ev_ring0 = nullptr;    // timing event at the ring start (profiling)
     unsigned long long sent[kMaxWorld] = {0};
     int* err_host = nullptr;
     int* err_dev = nullptr;
     unsigned long long* bad_count = nullptr;
     cudaStream_t comm_stream = nullptr;
-    cudaEvent_t ev_ready = nullptr, ev_done = nullptr, ev_copy[2] = {nullptr, nullptr},
-                ev_comp[2] = {nullptr, nullptr};
+    cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
     // layers (cdsp_comm_create_layers): one K/V store per layer, positions shared
     int n_layers = 1;
     size_t kv_bytes = 0;                 // bytes of one layer's K (or V) store
@@ -121,8 +143,8 @@ struct cdsp_comm_s {
     // ring profile (cdsp_comm_profile_ring): per pull, events at copy start / copy end (comm
     // stream) and the index of the attention launch the pull must beat (its end event)
     struct RingRec {
-        int ev;         // ring_ev[2 ev], ring_ev[2 ev + 1]
-        int prev_attn;  // prof_ev index of the previous step's attention end, -1 if none
+        int ev;              // ring_ev[2 ev], ring_ev[2 ev + 1]: pull start / end (comm stream)
+        cudaEvent_t from;    // the compute stream waited for this pull from this event on; NULL: no wait
         int64_t bytes;
     };
     std::vector<cudaEvent_t> ring_ev;
@@ -163,53 +185,35 @@ cdsp_status barrier(cdsp_comm c, const ChunkInfo& ci, cudaStream_t st) {
     return launch_peer_barrier(a, st);
 }
 
-cdsp_status ensure_acc(cdsp_comm c, size_t acc_elems, size_t lse_elems, cudaStream_t st) {
-    if (acc_elems > c->acc_elems) {
-        if (c->o_acc) CDSP_CUDA(cudaFreeAsync(c->o_acc, st));
-        CDSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c->o_acc), acc_elems * sizeof(float), st));
-        c->acc_elems = acc_elems;
-    }
-    if (lse_elems > c->lse_elems) {
-        if (c->lse_acc) CDSP_CUDA(cudaFreeAsync(c->lse_acc, st));
-        CDSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c->lse_acc), lse_elems * sizeof(float), st));
-        c->lse_elems = lse_elems;
-    }
-    return CDSP_OK;
+// One block-attention launch over a.nblk KV blocks (bf16: tcgen05 kernel, f32: FFMA kernel),
+// bracketed by a CUDA event pair when the communicator is profiling.
+cdsp_status run_attention(const AttnArgs& a, cudaStream_t st) {
+    return a.dtype == CDSP_BF16 ? launch_attention_tc(a, st) : launch_attention_simt(a, st);
 }
-
-cdsp_status run_attention(const void* q, const void* k, const void* v, int32_t dtype, int Hq, int Hkv, int D,
-                          const cdsp_segments& seg, float scale, int mode, float* o_acc, float* lse_acc, void* out,
-                          float* lse, cudaStream_t st) {
-    AttnArgs a;
-    a.q = q;
-    a.k = k;
-    a.v = v;
-    a.dtype = dtype;
-    a.Hq = Hq;
-    a.Hkv = Hkv;
-    a.D = D;
-    a.seg = seg;
-    a.scale = scale;
-    a.mode = mode;
-    a.o_acc = o_acc;
-    a.lse_acc = lse_acc;
-    a.out = out;
-    a.lse = lse;
-    return dtype == CDSP_BF16 ? launch_attention_tc(a, st) : launch_attention_simt(a, st);
-}
-
-// run_attention bracketed by a CUDA event pair when the communicator is profiling.
-cdsp_status run_attention_timed(cdsp_comm c, const void* q, const void* k, const void* v, int32_t dtype, int Hq,
-                                int Hkv, int D, const cdsp_segments& seg, float scale, int mode, float* o_acc,
-                                float* lse_acc, void* out, float* lse, cudaStream_t st) {
+cdsp_status run_attention_timed(cdsp_comm c, const AttnArgs& a, cudaStream_t st) {
     const bool rec = c->profiling && c->prof_n * 2 + 1 < static_cast<int>(c->prof_ev.size());
     if (rec) CDSP_CUDA(cudaEventRecord(c->prof_ev[2 * c->prof_n], st));
-    CDSP_CHECK_STATUS(run_attention(q, k, v, dtype, Hq, Hkv, D, seg, scale, mode, o_acc, lse_acc, out, lse, st));
+    CDSP_CHECK_STATUS(run_attention(a, st));
     if (rec) {
         CDSP_CUDA(cudaEventRecord(c->prof_ev[2 * c->prof_n + 1], st));
         ++c->prof_n;
     }
     return CDSP_OK;
+}
+AttnArgs attn_args(cdsp_comm c, const void* q, int Hq, float scale, int mode, void* out, float* lse) {
+    AttnArgs a;
+    a.q = q;
+    a.dtype = c->dtype;
+    a.Hq = Hq;
+    a.Hkv = c->Hkv;
+    a.D = c->D;
+    a.scale = scale;
+    a.mode = mode;
+    a.o_acc = c->o_acc;
+    a.lse_acc = c->lse_acc;
+    a.out = out;
+    a.lse = lse;
+    return a;
 }
 
 // Segments of ring rank r's query shard against src's block (history + src's shard).
@@ -330,54 +334,161 @@ inline bool prebalanced(cdsp_comm c, const ChunkInfo& ci, int layer, const cdsp_
     return c->prebal[layer] == ci.c && c->prebal_plan == plan;
 }
 
-// The ring (R10, R11): step k attends to src = (r - k) mod s's whole store; steps >= 1
-// read it through a copy-engine pull on the comm stream into receive buffer k & 1, overlapped
-// with step k-1.  g != NULL (loopback): each pull waits for src's append event.
+// cuStreamWriteValue32 through the runtime's driver entry point (no link-time libcuda): the
+// stream front end writes the word after the preceding copies, no SM involved.
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value_fn() {
+    static WriteValue32Fn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<WriteValue32Fn>(p);
+    }
+    return fn;
+}
+
+// How ring rank r runs chunk ci's ring: blocks k = 0 .. s-1 (k = 0: its own store; k >= 1: the
+// store of src = (r - k) mod s, pulled into receive slot k - 1), walked by launches of
+// consecutive blocks.  bf16: one launch walks every block with O resident in TMEM (the fused
+// ring), unless the blocks exceed the kernel's tile list (then several launches, merged
+// through the fp32 accumulators) or CDSP_RING_STEPWISE is set; f32: one launch per block.
+struct RingLaunches {
+    int n = 0;
+    int first[kMaxWorld + 1] = {};  // launch i covers blocks [first[i], first[i + 1])
+    bool fused = false;
+};
+cdsp_status ring_launches(cdsp_comm c, const ChunkInfo& ci, int r, RingLaunches* out) {
+    const bool fused = c->dtype == CDSP_BF16 && !(c->ring_opts & CDSP_RING_STEPWISE);
+    const int max_t = c->dtype == CDSP_BF16 ? attention_tc_max_tiles(c->D) : 0;
+    out->n = 0;
+    out->fused = fused;
+    int64_t acc = 0;
+    for (int k = 0; k < ci.s; ++k) {
+        const int src = (r - k + ci.s) % ci.s;
+        const int64_t t = (ci.hist[src] + 2 * ci.m + 127) / 128;
+        CDSP_REQUIRE(c->dtype != CDSP_BF16 || t <= max_t, CDSP_ERR_CAPACITY,
+                     "ring block of %lld tiles exceeds the %d KV tiles of one launch", static_cast<long long>(t),
+                     max_t);
+        if (k == 0 || !fused || acc + t > max_t) {
+            out->first[out->n++] = k;
+            acc = 0;
+        }
+        acc += t;
+    }
+    out->first[out->n] = ci.s;
+    return CDSP_OK;
+}
+
+// The ring (R10, R11): ring step k's block is src = (r - k) mod s's whole store
+// (history + shard).  Every pull is issued up front on the comm stream (copy engines; over
+// NVLink when the peer is another GPU) into its own receive slot, so the transfers run
+// back to back under the attention.  The attention walks the blocks in ring order:
+//  * events: a launch starts once the pulls of its blocks landed (same-device peers, where a
+//    device-to-device copy may itself need SMs, and multi-launch rings);
+//  * arrival flags (fused ring, every peer on another GPU): the launch starts at once on its
+//    own block and each producer warp waits for block k's flag (written by the comm stream
+//    behind block k's pull, per head group, so the first units' heads arrive first) right
+//    before that block's first tile.
+// g != NULL (loopback): each pull waits for src's append event.
 cdsp_status phase_ring(cdsp_comm c, const ChunkInfo& ci, int r, int layer, const void* q, int Hq, void* out,
                        float* lse, float scale, cudaStream_t st, LocalGroup* g) {
     const int64_t m2 = 2 * ci.m;
-    const int prof_base = c->prof_n;  // profiling: index of this call's step-0 attention launch
-    CDSP_CUDA(cudaEventRecord(c->ev_ready, st));  // recv buffers are free after st's earlier work
+    const int s = ci.s;
+    RingLaunches rl;
+    CDSP_CHECK_STATUS(ring_launches(c, ci, r, &rl));
+    const bool control = (c->ring_opts & CDSP_RING_CONTROL) != 0;
+    bool remote_all = true;
+    for (int k = 1; k < s; ++k)
+        if (!c->peer_remote[ci.ranks[(r - k + s) % s]]) remote_all = false;
+    const bool want_flags = (c->ring_opts & CDSP_RING_GATE_FLAGS) ||
+                            (remote_all && !(c->ring_opts & CDSP_RING_GATE_EVENTS));
+    const bool gating = rl.fused && rl.n == 1 && s > 1 && !control && want_flags && c->gate && write_value_fn();
+    // head groups of a gated pull: >= 2 KB per row piece (copy-engine friendly), <= kMaxHG
+    int ng = 1;
+    if (gating) {
+        static const int ng_env = getenv("CDSP_RING_NG") ? atoi(getenv("CDSP_RING_NG")) : 0;
+        ng = ng_env > 0 ? ng_env : static_cast<int>(c->row_bytes / 2048);
+        if (ng > kMaxHG) ng = kMaxHG;
+        if (ng < 1) ng = 1;
+        while (c->Hkv % ng != 0) --ng;
+    }
+    const uint32_t seq = ++c->gate_seq;
+    CDSP_CUDA(cudaEventRecord(c->ev_ready, st));  // receive slots are free after st's earlier work
     CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-    auto issue_copy = [&](int step) -> cdsp_status {
-        const int src = (r - step + ci.s) % ci.s;
-        const int b = step & 1;
-        if (step >= 3) CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_comp[b], 0));
-        if (g) CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, g->comms[ci.ranks[src]]->ev_app, 0));
-        const size_t bytes = static_cast<size_t>(ci.hist[src] + m2) * c->row_bytes;
-        const PeerView& pv = c->peers[ci.ranks[src]];
-        // profiling: the pull of step k must beat the end of step k-1's attention, the
-        // launch recorded right before this step's (prof_n counts launches issued so far)
-        const bool rec = c->profiling && c->ring_n < static_cast<int>(c->ring_rec.size());
-        if (rec) CDSP_CUDA(cudaEventRecord(c->ring_ev[2 * c->ring_n], c->comm_stream));
-        CDSP_CUDA(cudaMemcpyAsync(c->recv_k[b], layer_k(c, pv, layer), bytes, cudaMemcpyDeviceToDevice,
-                                  c->comm_stream));
-        CDSP_CUDA(cudaMemcpyAsync(c->recv_v[b], layer_v(c, pv, layer), bytes, cudaMemcpyDeviceToDevice,
-                                  c->comm_stream));
-        if (rec) {
-            CDSP_CUDA(cudaEventRecord(c->ring_ev[2 * c->ring_n + 1], c->comm_stream));
-            c->ring_rec[c->ring_n] = {c->ring_n, prof_base + step - 1, 2 * static_cast<int64_t>(bytes)};
-            ++c->ring_n;
+    const bool prof = c->profiling && c->ev_ring0 != nullptr;
+    if (prof) CDSP_CUDA(cudaEventRecord(c->ev_ring0, st));
+    int rec_last[kMaxWorld];  // ring profile record of step k's last pull piece
+    for (int k = 0; k < kMaxWorld; ++k) rec_last[k] = -1;
+    if (!control) {
+        for (int hg = 0; hg < ng; ++hg) {
+            for (int k = 1; k < s; ++k) {
+                const int src = (r - k + s) % s;
+                if (g && hg == 0) CDSP_CUDA(cudaStreamWaitEvent(c->comm_stream, g->comms[ci.ranks[src]]->ev_app, 0));
+                const PeerView& pv = c->peers[ci.ranks[src]];
+                const int64_t rows = ci.hist[src] + m2;
+                const bool rec = prof && c->ring_n < static_cast<int>(c->ring_rec.size());
+                if (rec) CDSP_CUDA(cudaEventRecord(c->ring_ev[2 * c->ring_n], c->comm_stream));
+                if (ng == 1) {
+                    const size_t bytes = static_cast<size_t>(rows) * c->row_bytes;
+                    CDSP_CUDA(cudaMemcpyAsync(c->recv_k[k - 1], layer_k(c, pv, layer), bytes, cudaMemcpyDeviceToDevice,
+                                              c->comm_stream));
+                    CDSP_CUDA(cudaMemcpyAsync(c->recv_v[k - 1], layer_v(c, pv, layer), bytes, cudaMemcpyDeviceToDevice,
+                                              c->comm_stream));
+                } else {  // head group hg: a 2D copy of its slice of every row
+                    const size_t w = c->row_bytes / ng, off = hg * w;
+                    CDSP_CUDA(cudaMemcpy2DAsync(c->recv_k[k - 1] + off, c->row_bytes, layer_k(c, pv, layer) + off,
+                                                c->row_bytes, w, rows, cudaMemcpyDeviceToDevice, c->comm_stream));
+                    CDSP_CUDA(cudaMemcpy2DAsync(c->recv_v[k - 1] + off, c->row_bytes, layer_v(c, pv, layer) + off,
+                                                c->row_bytes, w, rows, cudaMemcpyDeviceToDevice, c->comm_stream));
+                }
+                if (rec) {
+                    CDSP_CUDA(cudaEventRecord(c->ring_ev[2 * c->ring_n + 1], c->comm_stream));
+                    c->ring_rec[c->ring_n] = {c->ring_n, nullptr,
+                                              2 * static_cast<int64_t>(rows) * static_cast<int64_t>(c->row_bytes / ng)};
+                    rec_last[k] = c->ring_n++;
+                }
+                if (gating) {
+                    const CUresult e = write_value_fn()(reinterpret_cast<CUstream>(c->comm_stream),
+                                                        reinterpret_cast<CUdeviceptr>(c->gate + k * kMaxHG + hg), seq, 0);
+                    CDSP_REQUIRE(e == CUDA_SUCCESS, CDSP_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", static_cast<int>(e));
+                }
+                if (hg == ng - 1) CDSP_CUDA(cudaEventRecord(c->ev_pull[k], c->comm_stream));
+            }
         }
-        CDSP_CUDA(cudaEventRecord(c->ev_copy[b], c->comm_stream));
-        return CDSP_OK;
-    };
-    CDSP_CHECK_STATUS(issue_copy(1));
-    for (int step = 0; step < ci.s; ++step) {
-        if (step + 1 >= 2 && step + 1 < ci.s) CDSP_CHECK_STATUS(issue_copy(step + 1));
-        const int src = (r - step + ci.s) % ci.s;
-        const int b = step & 1;
-        const char* kb = layer_k(c, c->self, layer);
-        const char* vb = layer_v(c, c->self, layer);
-        if (step > 0) {
-            CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_copy[b], 0));
-            kb = c->recv_k[b];
-            vb = c->recv_v[b];
+    }
+    for (int i = 0; i < rl.n; ++i) {
+        const int k0 = rl.first[i], k1 = rl.first[i + 1];
+        if (!control && !gating && k1 - 1 >= 1) {  // the launch's blocks have landed (the comm stream is in order)
+            CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_pull[k1 - 1], 0));
+            const int rc = rec_last[k1 - 1];
+            if (rc >= 0)  // exposed: from the previous launch's end (or the ring start) to this pull's end
+                c->ring_rec[rc].from = i == 0 || c->prof_n == 0 ? c->ev_ring0 : c->prof_ev[2 * (c->prof_n - 1) + 1];
         }
-        const int mode = step == 0 ? CDSP_ATTN_FIRST : (step == ci.s - 1 ? CDSP_ATTN_LAST : CDSP_ATTN_MID);
-        CDSP_CHECK_STATUS(run_attention_timed(c, q, kb, vb, c->dtype, Hq, c->Hkv, c->D, segments_for(ci, r, src),
-                                              scale, mode, c->o_acc, c->lse_acc, out, lse, st));
-        if (step > 0) CDSP_CUDA(cudaEventRecord(c->ev_comp[b], st));
+        const int mode = rl.n == 1 ? CDSP_ATTN_ONLY
+                                   : (i == 0 ? CDSP_ATTN_FIRST : (i == rl.n - 1 ? CDSP_ATTN_LAST : CDSP_ATTN_MID));
+        AttnArgs a = attn_args(c, q, Hq, scale, mode, out, lse);
+        a.nblk = k1 - k0;
+        a.pdl = i > 0;  // the accumulator is this chain's own
+        for (int k = k0; k < k1; ++k) {
+            const int b = k - k0;
+            a.k[b] = k == 0 ? layer_k(c, c->self, layer) : c->recv_k[k - 1];
+            a.v[b] = k == 0 ? layer_v(c, c->self, layer) : c->recv_v[k - 1];
+            a.seg[b] = segments_for(ci, r, (r - k + s) % s);
+        }
+        if (gating) {
+            a.gate = c->gate;
+            a.gate_target = seq;
+            a.gate_mask = ((1u << a.nblk) - 1u) & ~1u;  // block 0 is the own store
+            a.gate_ng = kMaxHG;
+            a.gate_hpg = c->Hkv / ng;
+            a.gate_err = c->err_dev;
+            if (!remote_all) a.spare_sms = 8;  // forced flags over same-device copies: leave SMs to them
+        }
+        CDSP_CHECK_STATUS(run_attention_timed(c, a, st));
     }
     CDSP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
     CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
@@ -412,10 +523,19 @@ cdsp_status run_group_local(LocalGroup* g, const ChunkInfo& ci, int layer) {
         CDSP_CUDA(cudaEventRecord(comm_of(r)->ev_app, pc.st));
         pc.prev_kv->n = comm_of(r)->n_l[layer];
     }
+    // forced arrival flags on one device (a test of the gating path): the rings run one after
+    // another once every append is done, so a spinning persistent grid never starves the
+    // append kernels or the same-device copies it waits for (they get the SMs it leaves free)
+    const bool serial = (comm_of(0)->ring_opts & CDSP_RING_GATE_FLAGS) != 0;
     for (int r = 0; r < ci.s; ++r) {
         PendingCall& pc = g->calls[r];
+        if (serial) {
+            for (int j = 0; j < ci.s; ++j) CDSP_CUDA(cudaStreamWaitEvent(pc.st, comm_of(j)->ev_app, 0));
+            if (r > 0) CDSP_CUDA(cudaStreamWaitEvent(pc.st, comm_of(r - 1)->ev_fin, 0));
+        }
         CDSP_CHECK_STATUS(phase_ring(comm_of(r), ci, r, layer, pc.q.ptr, static_cast<int>(pc.q.H), pc.out.ptr,
                                      pc.lse, pc.scale, pc.st, g));
+        if (serial) CDSP_CUDA(cudaEventRecord(comm_of(r)->ev_fin, pc.st));
     }
     for (int r = 0; r < ci.s; ++r) {
         CDSP_CUDA(cudaEventRecord(comm_of(r)->ev_fin, g->calls[r].st));
@@ -468,8 +588,9 @@ cdsp_status cdsp_comm_create_layers(cdsp_comm* out, int32_t rank, int32_t world,
     c->off_v = static_cast<size_t>(n_layers) * kv_bytes;
     c->off_pos = 2 * static_cast<size_t>(n_layers) * kv_bytes;
     c->off_flags = c->off_pos + align_up(static_cast<size_t>(store_cap_tokens) * 4, 256);
-    // flags: [0, 8) peer-barrier counters, [8, 16) balancing-ack counters (per peer)
-    c->region_bytes = c->off_flags + align_up(2 * kMaxWorld * sizeof(unsigned long long), 256);
+    // flag page: [0, 8) peer-barrier counters, [8, 16) balancing-ack counters (per peer), then
+    // the geometry header peers check on connect
+    c->region_bytes = c->off_flags + align_up(kHeaderOff + sizeof(RegionHeader), 256);
     auto fail = [&](cudaError_t e, const char* what) {
         set_error("%s failed: %s", what, cudaGetErrorString(e));
         cdsp_comm_destroy(c);
@@ -485,11 +606,41 @@ cdsp_status cdsp_comm_create_layers(cdsp_comm* out, int32_t rank, int32_t world,
     c->self.pos = reinterpret_cast<int32_t*>(base + c->off_pos);
     c->self.flags = reinterpret_cast<unsigned long long*>(base + c->off_flags);
     c->peers[rank] = c->self;
-    e = cudaMalloc(&c->recv, 4 * kv_bytes);
-    if (e != cudaSuccess) return fail(e, "cudaMalloc(recv)");
-    for (int b = 0; b < 2; ++b) {
-        c->recv_k[b] = static_cast<char*>(c->recv) + (2 * b) * kv_bytes;
-        c->recv_v[b] = static_cast<char*>(c->recv) + (2 * b + 1) * kv_bytes;
+    {
+        RegionHeader h;
+        std::memset(&h, 0, sizeof(h));
+        h.magic = kRegionMagic;
+        h.abi = CDSP_ABI_VERSION;
+        h.n_layers = n_layers;
+        h.Hkv = Hkv;
+        h.D = D;
+        h.dtype = dtype;
+        h.world = world;
+        h.cap = store_cap_tokens;
+        h.region_bytes = c->region_bytes;
+        h.off_v = c->off_v;
+        h.off_pos = c->off_pos;
+        h.off_flags = c->off_flags;
+        cudaDeviceProp prop;
+        e = cudaGetDeviceProperties(&prop, device);
+        if (e != cudaSuccess) return fail(e, "cudaGetDeviceProperties");
+        std::memcpy(h.uuid, &prop.uuid, sizeof(h.uuid));
+        e = cudaMemcpy(base + c->off_flags + kHeaderOff, &h, sizeof(h), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return fail(e, "cudaMemcpy(header)");
+    }
+    // one receive slot (K and V, cap rows each) per ring step k = 1 .. world-1
+    c->n_slots = world - 1;
+    if (c->n_slots > 0) {
+        e = cudaMalloc(&c->recv, 2 * static_cast<size_t>(c->n_slots) * kv_bytes);
+        if (e != cudaSuccess) return fail(e, "cudaMalloc(recv)");
+        for (int b = 0; b < c->n_slots; ++b) {
+            c->recv_k[b] = static_cast<char*>(c->recv) + (2 * b) * kv_bytes;
+            c->recv_v[b] = static_cast<char*>(c->recv) + (2 * b + 1) * kv_bytes;
+        }
+        e = cudaMalloc(reinterpret_cast<void**>(&c->gate), kMaxWorld * kMaxHG * sizeof(uint32_t));
+        if (e != cudaSuccess) return fail(e, "cudaMalloc(gate)");
+        e = cudaMemset(c->gate, 0, kMaxWorld * kMaxHG * sizeof(uint32_t));
+        if (e != cudaSuccess) return fail(e, "cudaMemset(gate)");
     }
     e = cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int), cudaHostAllocMapped);
     if (e != cudaSuccess) return fail(e, "cudaHostAlloc");
@@ -502,10 +653,13 @@ cdsp_status cdsp_comm_create_layers(cdsp_comm* out, int32_t rank, int32_t world,
     if (e != cudaSuccess) return fail(e, "cudaMemset");
     e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return fail(e, "cudaStreamCreate");
-    cudaEvent_t* evs[9] = {&c->ev_ready,   &c->ev_done,   &c->ev_copy[0], &c->ev_copy[1], &c->ev_comp[0],
-                           &c->ev_comp[1], &c->ev_bal,    &c->ev_app,     &c->ev_fin};
+    cudaEvent_t* evs[5] = {&c->ev_ready, &c->ev_done, &c->ev_bal, &c->ev_app, &c->ev_fin};
     for (auto* ev : evs) {
         e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return fail(e, "cudaEventCreate");
+    }
+    for (auto& ev : c->ev_pull) {
+        e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
         if (e != cudaSuccess) return fail(e, "cudaEventCreate");
     }
     for (auto& ev : c->ev_bal_l) {
@@ -515,6 +669,37 @@ cdsp_status cdsp_comm_create_layers(cdsp_comm* out, int32_t rank, int32_t world,
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return fail(e, "cudaDeviceSynchronize");
     *out = c;
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_comm_reserve(cdsp_comm c, int64_t max_q_rows, int32_t max_hq) {
+    CDSP_REQUIRE(c != nullptr, CDSP_ERR_INVALID, "NULL comm");
+    CDSP_REQUIRE(max_q_rows >= 0 && max_hq >= 0, CDSP_ERR_INVALID, "negative reservation");
+    if (max_q_rows <= c->acc_rows && max_hq <= c->acc_hq) return CDSP_OK;
+    const int64_t rows = max_q_rows > c->acc_rows ? max_q_rows : c->acc_rows;
+    const int32_t hq = max_hq > c->acc_hq ? max_hq : c->acc_hq;
+    CDSP_CUDA(cudaSetDevice(c->device));
+    CDSP_CUDA(cudaDeviceSynchronize());  // no launch may still use the old buffers
+    if (c->o_acc) CDSP_CUDA(cudaFree(c->o_acc));
+    if (c->lse_acc) CDSP_CUDA(cudaFree(c->lse_acc));
+    c->o_acc = nullptr;
+    c->lse_acc = nullptr;
+    c->acc_rows = 0;
+    c->acc_hq = 0;
+    CDSP_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->o_acc), static_cast<size_t>(rows) * hq * c->D * sizeof(float)));
+    CDSP_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->lse_acc), static_cast<size_t>(rows) * hq * sizeof(float)));
+    c->acc_rows = rows;
+    c->acc_hq = hq;
+    return CDSP_OK;
+}
+
+cdsp_status cdsp_comm_set_ring_options(cdsp_comm c, int32_t options) {
+    CDSP_REQUIRE(c != nullptr, CDSP_ERR_INVALID, "NULL comm");
+    CDSP_REQUIRE((options & ~(CDSP_RING_STEPWISE | CDSP_RING_CONTROL | CDSP_RING_GATE_FLAGS | CDSP_RING_GATE_EVENTS)) == 0,
+                 CDSP_ERR_INVALID, "unknown ring option bits 0x%x", options);
+    CDSP_REQUIRE(!((options & CDSP_RING_GATE_FLAGS) && (options & CDSP_RING_GATE_EVENTS)), CDSP_ERR_INVALID,
+                 "CDSP_RING_GATE_FLAGS and CDSP_RING_GATE_EVENTS exclude each other");
+    c->ring_opts = options;
     return CDSP_OK;
 }
 
@@ -530,6 +715,10 @@ cdsp_status cdsp_comm_ipc_handle(cdsp_comm c, void* handle_out) {
 cdsp_status cdsp_comm_connect(cdsp_comm c, const void* handles) {
     CDSP_REQUIRE(c && handles, CDSP_ERR_INVALID, "NULL argument");
     CDSP_REQUIRE(!c->connected, CDSP_ERR_INVALID, "communicator already connected");
+    CDSP_CUDA(cudaSetDevice(c->device));
+    RegionHeader mine;
+    CDSP_CUDA(cudaMemcpy(&mine, static_cast<char*>(c->region) + c->off_flags + kHeaderOff, sizeof(mine),
+                         cudaMemcpyDeviceToHost));
     const char* hb = static_cast<const char*>(handles);
     for (int j = 0; j < c->world; ++j) {
         if (j == c->rank) continue;
@@ -540,6 +729,20 @@ cdsp_status cdsp_comm_connect(cdsp_comm c, const void* handles) {
         CDSP_REQUIRE(e == cudaSuccess, CDSP_ERR_COMM, "cudaIpcOpenMemHandle(peer %d): %s", j, cudaGetErrorString(e));
         c->ipc_base[j] = base;
         char* b = static_cast<char*>(base);
+        // the peer's geometry must match this one's: every peer offset below is computed locally
+        RegionHeader ph;
+        e = cudaMemcpy(&ph, b + c->off_flags + kHeaderOff, sizeof(ph), cudaMemcpyDeviceToHost);
+        CDSP_REQUIRE(e == cudaSuccess, CDSP_ERR_COMM, "reading peer %d's header: %s", j, cudaGetErrorString(e));
+        CDSP_REQUIRE(ph.magic == kRegionMagic && ph.abi == mine.abi && ph.n_layers == mine.n_layers &&
+                         ph.Hkv == mine.Hkv && ph.D == mine.D && ph.dtype == mine.dtype && ph.world == mine.world &&
+                         ph.cap == mine.cap && ph.region_bytes == mine.region_bytes && ph.off_v == mine.off_v &&
+                         ph.off_pos == mine.off_pos && ph.off_flags == mine.off_flags,
+                     CDSP_ERR_COMM,
+                     "peer %d's communicator geometry differs (cap %lld/%lld, layers %d/%d, Hkv %d/%d, D %d/%d, "
+                     "dtype %d/%d, world %d/%d)",
+                     j, static_cast<long long>(ph.cap), static_cast<long long>(mine.cap), ph.n_layers, mine.n_layers,
+                     ph.Hkv, mine.Hkv, ph.D, mine.D, ph.dtype, mine.dtype, ph.world, mine.world);
+        c->peer_remote[j] = std::memcmp(ph.uuid, mine.uuid, sizeof(mine.uuid)) != 0;
         c->peers[j].k = b;
         c->peers[j].v = b + c->off_v;
         c->peers[j].pos = reinterpret_cast<int32_t*>(b + c->off_pos);
@@ -590,6 +793,7 @@ cdsp_status cdsp_comm_profile(cdsp_comm c, int32_t enable) {
         c->ring_ev.resize(2 * 4096, nullptr);
         for (auto& ev : c->ring_ev) CDSP_CUDA(cudaEventCreate(&ev));
         c->ring_rec.resize(4096);
+        CDSP_CUDA(cudaEventCreate(&c->ev_ring0));
     }
     c->profiling = enable != 0;
     c->prof_n = 0;
@@ -603,19 +807,18 @@ cdsp_status cdsp_comm_profile_ring(cdsp_comm c, double* copy_ms, double* exposed
     double cp = 0.0, ex = 0.0;
     int64_t by = 0;
     if (c->ring_n > 0) CDSP_CUDA(cudaEventSynchronize(c->ring_ev[2 * c->ring_n - 1]));
-    const int n_attn = static_cast<int>(c->prof_ev.size() / 2);
     for (int i = 0; i < c->ring_n; ++i) {
         const auto& r = c->ring_rec[i];
         float ms = 0.f;
         CDSP_CUDA(cudaEventElapsedTime(&ms, c->ring_ev[2 * r.ev], c->ring_ev[2 * r.ev + 1]));
         cp += ms;
         by += r.bytes;
-        if (r.prev_attn >= 0 && r.prev_attn < n_attn) {
-            // the compute stream idles from the end of the previous step's attention until
-            // this pull lands (the next attention waits on it)
-            CDSP_CUDA(cudaEventSynchronize(c->prof_ev[2 * r.prev_attn + 1]));
+        if (r.from != nullptr) {
+            // the compute stream idles from `from` (the previous launch's end, or the ring's
+            // start) until this pull lands: its next launch waits on it
+            CDSP_CUDA(cudaEventSynchronize(r.from));
             float gap = 0.f;
-            CDSP_CUDA(cudaEventElapsedTime(&gap, c->prof_ev[2 * r.prev_attn + 1], c->ring_ev[2 * r.ev + 1]));
+            CDSP_CUDA(cudaEventElapsedTime(&gap, r.from, c->ring_ev[2 * r.ev + 1]));
             if (gap > 0.f) ex += gap;
         }
     }
@@ -656,12 +859,15 @@ cdsp_status cdsp_comm_destroy(cdsp_comm c) {
     if (c->o_acc) cudaFree(c->o_acc);
     if (c->lse_acc) cudaFree(c->lse_acc);
     if (c->recv) cudaFree(c->recv);
+    if (c->gate) cudaFree(c->gate);
+    if (c->ev_ring0) cudaEventDestroy(c->ev_ring0);
+    for (auto ev : c->ev_pull)
+        if (ev) cudaEventDestroy(ev);
     if (c->region) cudaFree(c->region);
     if (c->bad_count) cudaFree(c->bad_count);
     if (c->err_host) cudaFreeHost(c->err_host);
     if (c->lg && --c->lg->refs == 0) delete c->lg;
-    cudaEvent_t evs[9] = {c->ev_ready,   c->ev_done, c->ev_copy[0], c->ev_copy[1], c->ev_comp[0],
-                          c->ev_comp[1], c->ev_bal,  c->ev_app,     c->ev_fin};
+    cudaEvent_t evs[5] = {c->ev_ready, c->ev_done, c->ev_bal, c->ev_app, c->ev_fin};
     for (auto ev : evs)
         if (ev) cudaEventDestroy(ev);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
@@ -785,7 +991,16 @@ cdsp_status cdsp_prefill_chunk_layer(const cdsp_tensor* q, const cdsp_tensor* k,
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf(static_cast<float>(c->D));
     const int Hq = static_cast<int>(q->H);
-    if (ci.s > 1) CDSP_CHECK_STATUS(ensure_acc(c, static_cast<size_t>(m2) * Hq * c->D, static_cast<size_t>(Hq) * m2, st));
+    if (ci.s > 1) {  // the ring's launch structure; several launches merge through the reserved accumulators
+        RingLaunches rl;
+        CDSP_CHECK_STATUS(ring_launches(c, ci, r, &rl));
+        CDSP_REQUIRE(rl.n == 1 || (c->acc_rows >= m2 && c->acc_hq >= Hq), CDSP_ERR_CAPACITY,
+                     "this ring runs as %d launches merged in fp32 accumulators: reserve %lld rows x %d heads with "
+                     "cdsp_comm_reserve (reserved %lld x %d)",
+                     rl.n, static_cast<long long>(m2), Hq, static_cast<long long>(c->acc_rows), c->acc_hq);
+        CDSP_REQUIRE(ci.s - 1 <= c->n_slots, CDSP_ERR_INVALID, "ring of %d needs %d receive slots, comm has %d", ci.s,
+                     ci.s - 1, c->n_slots);
+    }
 
     if (ci.s > 1 && c->lg != nullptr) {
         // loopback: a deferred collective (like an NCCL group) — record this rank's call; the
@@ -832,9 +1047,11 @@ cdsp_status cdsp_prefill_chunk_layer(const cdsp_tensor* q, const cdsp_tensor* k,
                                                 shard_stride(ci), c->comm_stream));
         n = m2;
         prev_kv->n = n;
-        CDSP_CHECK_STATUS(run_attention_timed(c, q->ptr, k->ptr, v->ptr, c->dtype, Hq, c->Hkv, c->D,
-                                              segments_for(ci, r, 0), scale, CDSP_ATTN_ONLY, nullptr, nullptr,
-                                              out->ptr, lse, st));
+        AttnArgs a = attn_args(c, q->ptr, Hq, scale, CDSP_ATTN_ONLY, out->ptr, lse);
+        a.k[0] = k->ptr;
+        a.v[0] = v->ptr;
+        a.seg[0] = segments_for(ci, r, 0);
+        CDSP_CHECK_STATUS(run_attention_timed(c, a, st));
         CDSP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
         CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_done, 0));
         return CDSP_OK;
@@ -842,9 +1059,11 @@ cdsp_status cdsp_prefill_chunk_layer(const cdsp_tensor* q, const cdsp_tensor* k,
     CDSP_CHECK_STATUS(phase_append(c, ci, r, layer, k, v, st));
     prev_kv->n = n;
     if (ci.s == 1) {
-        return run_attention_timed(c, q->ptr, layer_k(c, c->self, layer), layer_v(c, c->self, layer), c->dtype, Hq,
-                                   c->Hkv, c->D, segments_for(ci, r, 0), scale, CDSP_ATTN_ONLY, nullptr, nullptr,
-                                   out->ptr, lse, st);
+        AttnArgs a = attn_args(c, q->ptr, Hq, scale, CDSP_ATTN_ONLY, out->ptr, lse);
+        a.k[0] = layer_k(c, c->self, layer);
+        a.v[0] = layer_v(c, c->self, layer);
+        a.seg[0] = segments_for(ci, r, 0);
+        return run_attention_timed(c, a, st);
     }
     CDSP_CHECK_STATUS(barrier(c, ci, st));  // B3
     CDSP_CHECK_STATUS(phase_ring(c, ci, r, layer, q->ptr, Hq, out->ptr, lse, scale, st, nullptr));
@@ -934,27 +1153,50 @@ cdsp_status cdsp_kv_transfer_errors(cdsp_comm c, void* cuda_stream, int64_t* n_b
 }
 
 // ------------------------------------------------------------------------------- blocks
-cdsp_status cdsp_attention_fwd(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
-                               const cdsp_segments* seg, float softmax_scale, int32_t mode, float* o_acc,
-                               float* lse_acc, cdsp_tensor* out, float* lse, void* cuda_stream) {
-    CDSP_REQUIRE(seg != nullptr, CDSP_ERR_INVALID, "NULL segments");
-    CDSP_REQUIRE(seg->pos_stride >= 0 && seg->pos_stride <= 8, CDSP_ERR_SHAPE, "pos_stride %lld not in [0,8]",
-                 static_cast<long long>(seg->pos_stride));
-    cdsp_segments sg = *seg;
-    if (sg.pos_stride == 0) sg.pos_stride = 1;  // 0 = contiguous (ABI 1 callers)
-    CDSP_CHECK_STATUS(check_tensor(q, "q"));
-    CDSP_CHECK_STATUS(check_tensor(k, "k"));
-    CDSP_CHECK_STATUS(check_tensor(v, "v"));
+cdsp_status cdsp_attention_fwd_blocks(const cdsp_tensor* q, int32_t nblk, const cdsp_tensor* const* k,
+                                      const cdsp_tensor* const* v, const cdsp_segments* seg, float softmax_scale,
+                                      int32_t mode, float* o_acc, float* lse_acc, cdsp_tensor* out, float* lse,
+                                      void* cuda_stream) {
+    CDSP_REQUIRE(nblk >= 1 && nblk <= CDSP_MAX_SP, CDSP_ERR_INVALID, "nblk %d not in [1,%d]", nblk, CDSP_MAX_SP);
+    CDSP_REQUIRE(k != nullptr && v != nullptr && seg != nullptr, CDSP_ERR_INVALID, "NULL k/v/segments");
+    const bool pdl = (mode & CDSP_ATTN_PDL) != 0;
+    mode &= ~CDSP_ATTN_PDL;
     CDSP_REQUIRE(mode >= CDSP_ATTN_ONLY && mode <= CDSP_ATTN_LAST, CDSP_ERR_INVALID, "bad mode %d", mode);
-    CDSP_REQUIRE(q->dtype == k->dtype && k->dtype == v->dtype, CDSP_ERR_DTYPE, "q/k/v dtypes differ");
-    CDSP_REQUIRE(q->D == k->D && k->D == v->D && (q->D == 64 || q->D == 128), CDSP_ERR_SHAPE,
-                 "head dim must match and be 64 or 128");
-    CDSP_REQUIRE(k->H == v->H && q->H % k->H == 0, CDSP_ERR_SHAPE, "Hq %% Hkv != 0");
-    CDSP_REQUIRE(seg->nq == q->T && seg->nkv <= k->T && seg->nkv <= v->T && seg->nkv >= 0, CDSP_ERR_SHAPE,
-                 "segments do not match tensor rows");
-    CDSP_REQUIRE(seg->q_len0 >= 0 && seg->q_len0 <= seg->nq && seg->kv_hist >= 0 && seg->kv_len0 >= 0 &&
-                     seg->kv_hist + seg->kv_len0 <= seg->nkv,
-                 CDSP_ERR_SHAPE, "inconsistent segments");
+    CDSP_CHECK_STATUS(check_tensor(q, "q"));
+    CDSP_REQUIRE(q->D == 64 || q->D == 128, CDSP_ERR_SHAPE, "head dim must be 64 or 128");
+    CDSP_REQUIRE(q->dtype == CDSP_BF16 || nblk == 1, CDSP_ERR_UNSUPPORTED, "fp32 attention takes one KV block per launch");
+    AttnArgs a;
+    a.nblk = nblk;
+    int64_t tiles = 0;
+    for (int b = 0; b < nblk; ++b) {
+        CDSP_REQUIRE(k[b] != nullptr && v[b] != nullptr, CDSP_ERR_INVALID, "NULL k/v of block %d", b);
+        CDSP_CHECK_STATUS(check_tensor(k[b], "k"));
+        CDSP_CHECK_STATUS(check_tensor(v[b], "v"));
+        const cdsp_segments& sb = seg[b];
+        CDSP_REQUIRE(sb.pos_stride >= 0 && sb.pos_stride <= 8, CDSP_ERR_SHAPE, "pos_stride %lld not in [0,8]",
+                     static_cast<long long>(sb.pos_stride));
+        CDSP_REQUIRE(q->dtype == k[b]->dtype && k[b]->dtype == v[b]->dtype, CDSP_ERR_DTYPE, "q/k/v dtypes differ");
+        CDSP_REQUIRE(q->D == k[b]->D && k[b]->D == v[b]->D, CDSP_ERR_SHAPE, "head dims differ");
+        CDSP_REQUIRE(k[b]->H == v[b]->H && k[b]->H == k[0]->H && q->H % k[b]->H == 0, CDSP_ERR_SHAPE,
+                     "Hq %% Hkv != 0 or KV heads differ between blocks");
+        CDSP_REQUIRE(sb.nq == q->T && sb.nkv <= k[b]->T && sb.nkv <= v[b]->T && sb.nkv >= 0, CDSP_ERR_SHAPE,
+                     "segments of block %d do not match tensor rows", b);
+        CDSP_REQUIRE(sb.q_len0 >= 0 && sb.q_len0 <= sb.nq && sb.kv_hist >= 0 && sb.kv_len0 >= 0 &&
+                         sb.kv_hist + sb.kv_len0 <= sb.nkv,
+                     CDSP_ERR_SHAPE, "inconsistent segments (block %d)", b);
+        CDSP_REQUIRE(sb.q_len0 == seg[0].q_len0 && sb.q_pos0 == seg[0].q_pos0 && sb.q_pos1 == seg[0].q_pos1 &&
+                         (sb.pos_stride ? sb.pos_stride : 1) == (seg[0].pos_stride ? seg[0].pos_stride : 1),
+                     CDSP_ERR_SHAPE, "block %d's query segments differ from block 0's", b);
+        a.k[b] = k[b]->ptr;
+        a.v[b] = v[b]->ptr;
+        a.seg[b] = sb;
+        if (a.seg[b].pos_stride == 0) a.seg[b].pos_stride = 1;  // 0 = contiguous (ABI 1 callers)
+        tiles += (sb.nkv + 127) / 128;
+    }
+    if (q->dtype == CDSP_BF16)
+        CDSP_REQUIRE(tiles <= attention_tc_max_tiles(static_cast<int>(q->D)), CDSP_ERR_CAPACITY,
+                     "%lld KV tiles exceed the %d of one launch (split the blocks with FIRST / MID / LAST)",
+                     static_cast<long long>(tiles), attention_tc_max_tiles(static_cast<int>(q->D)));
     const bool final_out = mode == CDSP_ATTN_ONLY || mode == CDSP_ATTN_LAST;
     if (final_out) {
         CDSP_CHECK_STATUS(check_tensor(out, "out"));
@@ -963,10 +1205,25 @@ cdsp_status cdsp_attention_fwd(const cdsp_tensor* q, const cdsp_tensor* k, const
     }
     CDSP_REQUIRE(mode == CDSP_ATTN_ONLY || (o_acc && lse_acc) || q->T == 0, CDSP_ERR_INVALID,
                  "accumulator buffers required for mode %d", mode);
-    const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf(static_cast<float>(q->D));
-    return run_attention(q->ptr, k->ptr, v->ptr, q->dtype, static_cast<int>(q->H), static_cast<int>(k->H),
-                         static_cast<int>(q->D), sg, scale, mode, o_acc, lse_acc, final_out ? out->ptr : nullptr,
-                         lse, static_cast<cudaStream_t>(cuda_stream));
+    a.q = q->ptr;
+    a.dtype = q->dtype;
+    a.Hq = static_cast<int>(q->H);
+    a.Hkv = static_cast<int>(k[0]->H);
+    a.D = static_cast<int>(q->D);
+    a.scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf(static_cast<float>(q->D));
+    a.mode = mode;
+    a.o_acc = o_acc;
+    a.lse_acc = lse_acc;
+    a.out = final_out ? out->ptr : nullptr;
+    a.lse = lse;
+    a.pdl = pdl;
+    return run_attention(a, static_cast<cudaStream_t>(cuda_stream));
+}
+
+cdsp_status cdsp_attention_fwd(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
+                               const cdsp_segments* seg, float softmax_scale, int32_t mode, float* o_acc,
+                               float* lse_acc, cdsp_tensor* out, float* lse, void* cuda_stream) {
+    return cdsp_attention_fwd_blocks(q, 1, &k, &v, seg, softmax_scale, mode, o_acc, lse_acc, out, lse, cuda_stream);
 }
 
 static cdsp_status zigzag_copy(const cdsp_tensor* full, int32_t s, int32_t r, cdsp_tensor* shard, bool gather,

@@ -8,21 +8,37 @@
 
 namespace cdsp {
 
-// One block-attention launch (see cdsp_attention_fwd in cdsp.h).
+// One block-attention launch (see cdsp_attention_fwd / cdsp_attention_fwd_blocks in cdsp.h):
+// the queries against nblk KV blocks (k[b], v[b], seg[b]; the query fields of every seg[b]
+// are equal), walked in order with one softmax state per query row.
 struct AttnArgs {
-    const void* q;
-    const void* k;
-    const void* v;
-    int32_t dtype;
-    int Hq, Hkv, D;
-    cdsp_segments seg;
-    float scale;   // softmax scale sigma
-    int mode;      // cdsp_attn_mode
-    float* o_acc;
-    float* lse_acc;
-    void* out;
-    float* lse;
+    const void* q = nullptr;
+    int nblk = 1;
+    const void* k[CDSP_MAX_SP] = {};
+    const void* v[CDSP_MAX_SP] = {};
+    cdsp_segments seg[CDSP_MAX_SP] = {};
+    int32_t dtype = CDSP_BF16;
+    int Hq = 0, Hkv = 0, D = 0;
+    float scale = 0.f;   // softmax scale sigma
+    int mode = CDSP_ATTN_ONLY;  // cdsp_attn_mode
+    float* o_acc = nullptr;
+    float* lse_acc = nullptr;
+    void* out = nullptr;
+    float* lse = nullptr;
+    // launch as a programmatic dependent of the previous kernel in the stream (MID / LAST only:
+    // the accumulator is touched after griddepcontrol.wait); internal ring chains and explicit
+    // opt-in (CDSP_ATTN_PDL) only
+    bool pdl = false;
+    // arrival gating of blocks (bf16 kernel; see TcParams in attn_tc.cu); gate == NULL: none
+    const uint32_t* gate = nullptr;
+    uint32_t gate_target = 0, gate_mask = 0;
+    int gate_ng = 1, gate_hpg = 1;
+    int* gate_err = nullptr;
+    int spare_sms = 0;  // leave at least this many SMs to other kernels (persistent bf16 grid)
 };
+
+// KV tiles (128 keys) the bf16 kernel can list per launch (all blocks together).
+int attention_tc_max_tiles(int D);
 
 cdsp_status launch_attention_tc(const AttnArgs& a, cudaStream_t st);    // bf16, tcgen05/TMEM/TMA
 cdsp_status launch_attention_simt(const AttnArgs& a, cudaStream_t st);  // fp32, FFMA

@@ -31,63 +31,111 @@ struct MergeParams {
     float* lse;
 };
 
-template <int D>
+// Loads that bypass L1 (every byte is read once) and streaming stores.
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float2 ld_stream2(const float* p) {
+    float2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+}
+
+// Warp per (token, head) row: lane owns PER = D/32 contiguous elements of the row in every part.
+// All of a row's loads — the n LSEs and the n partial slices — are issued before any is used
+// (one memory round trip per row), and each warp walks RPI rows per iteration (grid-stride) so
+// enough bytes are in flight at small n.  A part whose lse is -inf contributes nothing and its
+// O is never multiplied in (R16: it may be unwritten).
+template <int D, int NP, int RPI>
 __global__ void __launch_bounds__(256) lse_merge_kernel(const MergeParams p) {
     constexpr int PER = D / 32;  // elements per lane (2 or 4)
-    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t rows = p.T * p.H;
-    if (gw >= rows) return;
-    const int64_t t = gw / p.H;
-    const int h = static_cast<int>(gw % p.H);
-    const size_t li = static_cast<size_t>(h) * p.T + t;
-    float M = -INFINITY;
-    float a[kMaxMerge];
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t g0 = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * RPI; g0 < rows;
+         g0 += nwarps * RPI) {
+        float a[RPI][NP];
+        float x[RPI][NP][PER];
 #pragma unroll
-    for (int i = 0; i < kMaxMerge; ++i) {
-        if (i < p.n) {
-            a[i] = p.lses[i][li];
-            M = fmaxf(M, a[i]);
-        }
-    }
-    float acc[PER];
+        for (int rr = 0; rr < RPI; ++rr) {
+            const int64_t gw = g0 + rr;
+            const bool ok = gw < rows;
+            const int64_t t = ok ? gw / p.H : 0;
+            const int h = ok ? static_cast<int>(gw % p.H) : 0;
+            const size_t li = static_cast<size_t>(h) * p.T + t;
+            const size_t base = static_cast<size_t>(ok ? gw : 0) * D + lane * PER;
 #pragma unroll
-    for (int e = 0; e < PER; ++e) acc[e] = 0.f;
-    float den = 0.f;
-    if (M != -INFINITY) {
-        const size_t base = static_cast<size_t>(gw) * D + lane * PER;
-#pragma unroll
-        for (int i = 0; i < kMaxMerge; ++i) {
-            if (i < p.n && a[i] != -INFINITY) {
-                const float w = expf(a[i] - M);
-                den += w;
-                if constexpr (PER == 4) {
-                    const float4 x = *reinterpret_cast<const float4*>(p.parts[i] + base);
-                    acc[0] = fmaf(w, x.x, acc[0]);
-                    acc[1] = fmaf(w, x.y, acc[1]);
-                    acc[2] = fmaf(w, x.z, acc[2]);
-                    acc[3] = fmaf(w, x.w, acc[3]);
-                } else {
-                    const float2 x = *reinterpret_cast<const float2*>(p.parts[i] + base);
-                    acc[0] = fmaf(w, x.x, acc[0]);
-                    acc[1] = fmaf(w, x.y, acc[1]);
+            for (int i = 0; i < NP; ++i) {
+                a[rr][i] = -INFINITY;
+                if (ok && i < p.n) {
+                    a[rr][i] = p.lses[i][li];
+                    if constexpr (PER == 4) {
+                        const float4 v = ld_stream4(p.parts[i] + base);
+                        x[rr][i][0] = v.x;
+                        x[rr][i][1] = v.y;
+                        x[rr][i][2] = v.z;
+                        x[rr][i][3] = v.w;
+                    } else {
+                        const float2 v = ld_stream2(p.parts[i] + base);
+                        x[rr][i][0] = v.x;
+                        x[rr][i][1] = v.y;
+                    }
                 }
             }
         }
-    }
-    const float inv = den > 0.f ? 1.0f / den : 0.f;
-    const size_t ob = static_cast<size_t>(gw) * D + lane * PER;
-    if (p.out_dtype == CDSP_F32) {
-        float* o = static_cast<float*>(p.out) + ob;
 #pragma unroll
-        for (int e = 0; e < PER; ++e) o[e] = acc[e] * inv;
-    } else {
-        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + ob;
+        for (int rr = 0; rr < RPI; ++rr) {
+            const int64_t gw = g0 + rr;
+            if (gw >= rows) break;
+            float M = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < PER; e += 2)
-            *reinterpret_cast<__nv_bfloat162*>(o + e) = __floats2bfloat162_rn(acc[e] * inv, acc[e + 1] * inv);
+            for (int i = 0; i < NP; ++i) M = fmaxf(M, a[rr][i]);
+            float acc[PER];
+#pragma unroll
+            for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+            float den = 0.f;
+            if (M != -INFINITY) {
+#pragma unroll
+                for (int i = 0; i < NP; ++i) {
+                    const bool use = a[rr][i] != -INFINITY;
+                    const float w = use ? __expf(a[rr][i] - M) : 0.f;
+                    den += w;
+#pragma unroll
+                    for (int e = 0; e < PER; ++e) acc[e] = use ? fmaf(w, x[rr][i][e], acc[e]) : acc[e];
+                }
+            }
+            const float inv = den > 0.f ? 1.0f / den : 0.f;
+            const size_t ob = static_cast<size_t>(gw) * D + lane * PER;
+            if (p.out_dtype == CDSP_F32) {
+                float* o = static_cast<float*>(p.out) + ob;
+                if constexpr (PER == 4)
+                    __stcs(reinterpret_cast<float4*>(o), make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv));
+                else
+                    __stcs(reinterpret_cast<float2*>(o), make_float2(acc[0] * inv, acc[1] * inv));
+            } else {
+                __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + ob;
+                if constexpr (PER == 4) {
+                    const __nv_bfloat162 b0 = __floats2bfloat162_rn(acc[0] * inv, acc[1] * inv);
+                    const __nv_bfloat162 b1 = __floats2bfloat162_rn(acc[2] * inv, acc[3] * inv);
+                    uint2 u;
+                    u.x = *reinterpret_cast<const uint32_t*>(&b0);
+                    u.y = *reinterpret_cast<const uint32_t*>(&b1);
+                    __stcs(reinterpret_cast<uint2*>(o), u);
+                } else {
+                    *reinterpret_cast<__nv_bfloat162*>(o) = __floats2bfloat162_rn(acc[0] * inv, acc[1] * inv);
+                }
+            }
+            if (p.lse && lane == 0) {
+                const int64_t t = gw / p.H;
+                const int h = static_cast<int>(gw % p.H);
+                p.lse[static_cast<size_t>(h) * p.T + t] = (M == -INFINITY) ? -INFINITY : M + __logf(den);
+            }
+        }
     }
-    if (p.lse && lane == 0) p.lse[li] = (M == -INFINITY) ? -INFINITY : M + logf(den);
 }
 
 // ------------------------------------------------------------------ K*4 row copies
@@ -99,21 +147,28 @@ struct RowCopyParams {
     int64_t seg0_vec;
 };
 
+// Warp per row (grid-stride over the rows of both segments; no per-vector division): lane
+// copies 16-byte vectors lane, lane + 32, ... of the row, four loads in flight before the stores.
 __global__ void __launch_bounds__(256) row_copy_kernel(const RowCopyParams p) {
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < p.total; i += stride) {
-        const int s = (i < p.seg0_vec) ? 0 : 1;
-        const int64_t j = s == 0 ? i : i - p.seg0_vec;
-        const int64_t r = j / p.row_vec, c = j % p.row_vec;
-        const void* sp = s ? p.seg[1].src : p.seg[0].src;
-        void* dp = s ? p.seg[1].dst : p.seg[0].dst;
-        const int64_t sr0 = s ? p.seg[1].src_row0 : p.seg[0].src_row0;
-        const int64_t dr0 = s ? p.seg[1].dst_row0 : p.seg[0].dst_row0;
-        const int64_t ss = s ? p.seg[1].src_stride : p.seg[0].src_stride;
-        const int64_t ds = s ? p.seg[1].dst_stride : p.seg[0].dst_stride;
-        const uint4* src = static_cast<const uint4*>(sp) + (sr0 + r * ss) * p.row_vec + c;
-        uint4* dst = static_cast<uint4*>(dp) + (dr0 + r * ds) * p.row_vec + c;
-        *dst = __ldg(src);
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t rows0 = p.seg[0].n_rows, rows = rows0 + (p.n_segs > 1 ? p.seg[1].n_rows : 0);
+    const int rv = static_cast<int>(p.row_vec);
+    for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < rows; w += nwarps) {
+        const bool s1 = w >= rows0;
+        const RowCopy& sg = s1 ? p.seg[1] : p.seg[0];
+        const int64_t r = s1 ? w - rows0 : w;
+        const uint4* src = static_cast<const uint4*>(sg.src) + (sg.src_row0 + r * sg.src_stride) * p.row_vec;
+        uint4* dst = static_cast<uint4*>(sg.dst) + (sg.dst_row0 + r * sg.dst_stride) * p.row_vec;
+        for (int c0 = lane; c0 < rv; c0 += 128) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c0 + 32 * u < rv) v[u] = __ldcs(src + c0 + 32 * u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c0 + 32 * u < rv) __stcs(dst + c0 + 32 * u, v[u]);
+        }
     }
 }
 
@@ -211,6 +266,14 @@ __global__ void peer_barrier_kernel(const BarrierArgs a) {
     __threadfence_system();
 }
 
+int sm_count_dev() {
+    static int n[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (n[dev] == 0 && cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n[dev] = 148;
+    return n[dev];
+}
+
 unsigned grid_for(int64_t work, int per_block = 256) {
     int64_t b = (work + per_block - 1) / per_block;
     const int64_t cap = 148 * 16;
@@ -238,14 +301,24 @@ cdsp_status launch_lse_merge(int n, const float* const* parts, const float* cons
     p.lse = lse;
     const int64_t warps = T * H;
     if (warps == 0) return CDSP_OK;
-    const int64_t blocks = (warps * 32 + 255) / 256;
-    CDSP_REQUIRE(blocks < (1ll << 31), CDSP_ERR_SHAPE, "merge too large");
-    if (D == 128)
-        lse_merge_kernel<128><<<static_cast<unsigned>(blocks), 256, 0, st>>>(p);
-    else if (D == 64)
-        lse_merge_kernel<64><<<static_cast<unsigned>(blocks), 256, 0, st>>>(p);
-    else
-        CDSP_FAIL(CDSP_ERR_SHAPE, "head dim %d not supported", D);
+    CDSP_REQUIRE(D == 64 || D == 128, CDSP_ERR_SHAPE, "head dim %d not supported", D);
+    // grid-stride: 8 CTAs of 8 warps per SM, each warp 1-2 rows per iteration
+    const int64_t need = (warps + 1) / 2;
+    const int64_t cap = static_cast<int64_t>(sm_count_dev()) * 8 * 8;
+    const unsigned blocks = static_cast<unsigned>(((need < cap ? need : cap) + 7) / 8);
+#define CDSP_MERGE_LAUNCH(DD, NP, RPI) lse_merge_kernel<DD, NP, RPI><<<blocks, 256, 0, st>>>(p)
+    if (D == 128) {
+        if (n <= 2) CDSP_MERGE_LAUNCH(128, 2, 2);
+        else if (n <= 4) CDSP_MERGE_LAUNCH(128, 4, 2);
+        else if (n <= 8) CDSP_MERGE_LAUNCH(128, 8, 1);
+        else CDSP_MERGE_LAUNCH(128, 16, 1);
+    } else {
+        if (n <= 2) CDSP_MERGE_LAUNCH(64, 2, 2);
+        else if (n <= 4) CDSP_MERGE_LAUNCH(64, 4, 2);
+        else if (n <= 8) CDSP_MERGE_LAUNCH(64, 8, 2);
+        else CDSP_MERGE_LAUNCH(64, 16, 1);
+    }
+#undef CDSP_MERGE_LAUNCH
     CDSP_CUDA(cudaGetLastError());
     return CDSP_OK;
 }
@@ -262,7 +335,10 @@ cdsp_status launch_row_copy(const RowCopy* segs, int n_segs, int64_t row_bytes, 
     p.seg0_vec = segs[0].n_rows * p.row_vec;
     p.total = p.seg0_vec + (n_segs > 1 ? segs[1].n_rows * p.row_vec : 0);
     if (p.total == 0) return CDSP_OK;
-    row_copy_kernel<<<grid_for(p.total), 256, 0, st>>>(p);
+    const int64_t rows = segs[0].n_rows + (n_segs > 1 ? segs[1].n_rows : 0);
+    const int64_t cap = static_cast<int64_t>(sm_count_dev()) * 8;  // 8 CTAs x 8 warps per SM
+    const int64_t blocks = (rows + 7) / 8 < cap ? (rows + 7) / 8 : cap;
+    row_copy_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(p);
     CDSP_CUDA(cudaGetLastError());
     return CDSP_OK;
 }

@@ -26,10 +26,20 @@ def _rank_lse_index(plan: api.Plan, c: int, r: int, device) -> torch.Tensor:
     return torch.as_tensor(rank_pos[r], device=device)
 
 
-def make_loopback_comms(plan: api.Plan, Hkv: int, D: int, dtype, device: int = 0, cap: Optional[int] = None):
+def max_shard_rows(plan: api.Plan) -> int:
+    """Largest query shard 2m = L / s of the plan (the accumulator rows a multi-launch ring needs)."""
+    return max(L // len(ranks) for L, ranks in plan.chunks)
+
+
+def make_loopback_comms(plan: api.Plan, Hkv: int, D: int, dtype, device: int = 0, cap: Optional[int] = None,
+                        Hq: Optional[int] = None):
+    """One communicator per instance of the plan on `device`, linked as a loopback group.  With Hq
+    given, each reserves fp32 accumulators for the plan's largest shard (multi-launch rings:
+    fp32, oversized bf16 blocks, RING_STEPWISE)."""
     world = max(r for _, ranks in plan.chunks for r in ranks) + 1
     cap = cap or api.plan_capacity(plan)
-    comms = [api.Comm(i, world, device, cap, Hkv, D, dtype) for i in range(world)]
+    rows = max_shard_rows(plan) if Hq else 0
+    comms = [api.Comm(i, world, device, cap, Hkv, D, dtype, max_q_rows=rows, max_hq=Hq or 0) for i in range(world)]
     if world > 1:
         api.connect_local(comms)
     return comms
@@ -48,7 +58,7 @@ def run_plan_loopback(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: a
     Hkv = k.shape[1]
     assert sum(L for L, _ in plan.chunks) == N, "plan does not cover the prompt"
     if comms is None:
-        comms = make_loopback_comms(plan, Hkv, D, q.dtype, device.index or 0)
+        comms = make_loopback_comms(plan, Hkv, D, q.dtype, device.index or 0, Hq=Hq)
     world = len(comms)
     if streams is None:
         streams = [torch.cuda.Stream(device=device) for _ in range(world)]
