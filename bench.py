@@ -251,7 +251,10 @@ def main():
     q, k, v = qkv(L, Hq, Hkv, D, torch.bfloat16, seed=0, device=dev)
     plan = api.Plan([(L, list(range(s)))])
     m2 = L // s
-    comm = api.Comm(rank, world, local, api.plan_capacity(plan), Hkv, D, torch.bfloat16)
+    # fp32 accumulators for this shard: the fused ring uses their rows as scratch to split its
+    # heaviest units (s > 1); reserved once here, never on the timed path
+    comm = api.Comm(rank, world, local, api.plan_capacity(plan), Hkv, D, torch.bfloat16,
+                    max_q_rows=m2 if s > 1 else 0, max_hq=Hq if s > 1 else 0)
     from paper_2511_06247_b200 import dist_utils
     if world > 1:
         dist_utils.check_plan_consistent(plan.chunks)

@@ -424,8 +424,10 @@ CDSP_API cdsp_status cdsp_attention_fwd(const cdsp_tensor* q, const cdsp_tensor*
  * intermediate partial (a rank's local queries against every block of the ring; P:304
  * "zigzag ring attention for historical tokens").  This is the kernel of a fused ring step
  * sequence.  bf16 only for nblk > 1 (else CDSP_ERR_UNSUPPORTED); all blocks together <= 4096 KV
- * tiles of 128 keys at D = 128 (else CDSP_ERR_CAPACITY).  Other arguments and errors as
- * cdsp_attention_fwd. */
+ * tiles of 128 keys at D = 128 (else CDSP_ERR_CAPACITY).  In CDSP_ATTN_ONLY mode, o_acc / lse_acc
+ * (optional, shaped as for FIRST) are scratch: given, the launch may split its heaviest query
+ * units over two block ranges and merge the halves (R3) through those rows, so no single unit
+ * sets the launch's tail.  Other arguments and errors as cdsp_attention_fwd. */
 CDSP_API cdsp_status cdsp_attention_fwd_blocks(const cdsp_tensor* q, int32_t nblk, const cdsp_tensor* const* k,
                                                const cdsp_tensor* const* v, const cdsp_segments* seg,
                                                float softmax_scale, int32_t mode, float* o_acc, float* lse_acc,

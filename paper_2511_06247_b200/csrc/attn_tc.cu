@@ -159,7 +159,8 @@ struct Layout {
     // KV blocks of the launch: segment descriptors [kMaxBlk] and first-tile offsets [kMaxBlk + 1]
     static constexpr int OFF_SEG = OFF_SCHED + 2 * LISTMAX * 2;
     static constexpr int OFF_TOFF = OFF_SEG + kMaxBlk * static_cast<int>(sizeof(cdsp_segments));
-    static constexpr int SMEM = OFF_TOFF + (kMaxBlk + 1) * 4 + 1024;  // + alignment slack
+    static constexpr int OFF_ROLE = OFF_TOFF + (kMaxBlk + 1) * 4;  // [NG] split-unit role of the finishing group
+    static constexpr int SMEM = OFF_ROLE + NG * 4 + 1024;  // + alignment slack
 };
 
 constexpr uint32_t COL_O = 0;
@@ -192,6 +193,15 @@ struct TcParams {
     float* lse;
     int* claim;  // [2]: dynamic unit counter, finished-CTA counter (both zero at launch; the last CTA re-zeroes them)
     int n_pb;    // row blocks per head in units of the CTA group (PAIR: pairs of 128-row blocks)
+    // Split units (multi-block launches): every upper unit (the upper row blocks also see the
+    // later blocks' keys on a ring rank: the heavy units) runs as two
+    // sub-units, blocks [0, split_blk) and [split_blk, nblk), claimed back to back.  The first
+    // to finish writes its normalised partial and LSE into the o_acc / lse_acc rows of the unit
+    // (R3 operands), the second merges it with its own and writes the output: a heavy unit no
+    // longer sets the launch's tail.  split_cnt: per (unit, CTA) {arrivals, partial-ready}, zero
+    // between launches (the second finisher re-zeroes its pair).
+    int split, split_blk;
+    int* split_cnt;
 };
 
 // Debug timeline (build with -DCDSP_KTRACE): per-unit phase stamps (globaltimer) and SM id,
@@ -299,6 +309,11 @@ __device__ __forceinline__ void tmem_ld32p(uint32_t taddr, uint32_t* r) {
           "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 }
+
+template <int V>
+struct IntC {
+    static constexpr int value = V;
+};
 
 __device__ __forceinline__ int clamp_bn(int64_t x) { return x < 0 ? 0 : (x > BN ? BN : static_cast<int>(x)); }
 // bits [lo, hi) of the 32 columns starting at `base`
@@ -555,6 +570,32 @@ __device__ __forceinline__ void gate_wait(const TcParams& p, int b, int kvh) {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Role of a finishing group in a split unit's pair protocol (all BM threads of group g call it):
+// 1 = first (leave the partial in the accumulator rows), 0 = second (wait for the partner's
+// partial, re-zero the pair's counters).  Out of line: its registers stay out of the softmax.
+__device__ __noinline__ int split_role(int* scnt, volatile int* role, int g, int r) {
+    if (r == 0) *role = atomicAdd(scnt, 1);
+    named_bar_sync(12 + g, BM);
+    const int first = *role == 0;
+    if (!first) {
+        if (r == 0) {  // the partner is past its own atomicAdd: it is writing its partial
+            const uint64_t t0 = globaltimer();
+            for (;;) {
+                int f;
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(scnt + 1) : "memory");
+                if (f != 0) break;
+                if (globaltimer() - t0 > 3000000000ull) __trap();
+                __nanosleep(64);
+            }
+            scnt[0] = 0;  // both parties are done with the pair: zero for the next launch
+            scnt[1] = 0;
+        }
+        named_bar_sync(12 + g, BM);
+        __threadfence();
+    }
+    return first;
+}
+
 template <int HD, bool PAIR>
 __global__ void __maxnreg__(CDSP_MAXNREG)
     attn_tc_kernel(const __grid_constant__ TcMaps tm, const __grid_constant__ TcParams p) {
@@ -580,10 +621,39 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
     const int G = static_cast<int>(gridDim.x) / CL;  // CTA groups
     // the leader's barrier i as seen from this CTA (TMA bytes / arrivals of both CTAs land there)
     auto lbar = [&](int i) { return PAIR ? mapa_shared(bar(i), 0) : bar(i); };
-    auto unit_rows = [&](int x, int c, int& head, int64_t& row0) {
-        head = x / p.n_pb;
-        const int pb = p.n_pb - 1 - x % p.n_pb;
+    // unit x -> head, first row, part (-1: whole unit; 0 / 1: sub-unit of a split unit whose
+    // counter index is *ux) and its block range [*b0, *b1)
+    // Order: head-major (the units in flight share a few heads' K/V in L2: every unit of a head
+    // streams the same K/V tiles), heaviest row blocks first within a head.  Split launches:
+    // a head's upper units come as two adjacent sub-units each.
+    auto unit_map = [&](int x, int c, int& head, int64_t& row0, int& part, int& ux, int& b0, int& b1) {
+        int pb;
+        part = -1;
+        b0 = 0;
+        b1 = p.nblk;
+        ux = x;
+        if (p.split) {
+            const int hi = (p.n_pb + 1) / 2, lo = p.n_pb - hi, per = 2 * hi + lo;
+            head = x / per;
+            const int y = x - head * per;
+            if (y < 2 * hi) {
+                part = y & 1;
+                pb = p.n_pb - 1 - (y >> 1);
+                ux = head * hi + (y >> 1);
+                if (part == 0) b1 = p.split_blk;
+                else b0 = p.split_blk;
+            } else {
+                pb = lo - 1 - (y - 2 * hi);
+            }
+        } else {
+            head = x / p.n_pb;
+            pb = p.n_pb - 1 - x % p.n_pb;
+        }
         row0 = static_cast<int64_t>(PAIR ? 2 * pb + c : pb) * BM;
+    };
+    auto unit_rows = [&](int x, int c, int& head, int64_t& row0) {
+        int part, ux, b0, b1;
+        unit_map(x, c, head, row0, part, ux, b0, b1);
     };
 
     // ---- setup (once per CTA)
@@ -677,9 +747,9 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 }
                 break;
             }
-            int head;
+            int head, part, ux, blo, bhi;
             int64_t row0;
-            unit_rows(x, crank, head, row0);
+            unit_map(x, crank, head, row0, part, ux, blo, bhi);
             const int kvh = head / p.g;
             uint16_t* list = reinterpret_cast<uint16_t*>(smem + L::OFF_SCHED) + ub * L::LISTMAX;
             int64_t qlo, qhi, plo = 0, phi = 0;
@@ -692,7 +762,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 seg_qrange(sg, prow0, prow0 + BM, plo, phi, pany);
             }
             int cnt = 0;
-            for (int b = 0; b < p.nblk; ++b) {  // blocks in walk order, each block's tiles in order
+            for (int b = blo; b < bhi; ++b) {  // blocks in walk order, each block's tiles in order
                 const cdsp_segments& sb = segs[b];
                 const int t0 = toff[b], nt = toff[b + 1] - t0;
                 for (int j0 = 0; j0 < nt; j0 += 32) {  // 32 tiles per step, compacted in order
@@ -738,7 +808,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                     }
                 }
                 // merge modes: pull this unit's accumulator rows into L2 for the epilogue
-                if (p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST) {
+                if ((p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST) && part < 0) {
                     for (int rr = lane; rr < BM; rr += 32) {
                         const int64_t row = row0 + rr;
                         if (row < sg.nq) {
@@ -803,7 +873,10 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             mbar_wait(bar(L::B_UF + ub), (i >> 1) & 1);
             const UnitInfo u = uinfo[ub];
             if (u.x < 0) break;
-            const int kvh = (u.x / p.n_pb) / p.g;
+            int head;
+            int64_t row0_unused;
+            unit_rows(u.x, crank, head, row0_unused);
+            const int kvh = head / p.g;
             const uint16_t* list = reinterpret_cast<const uint16_t*>(smem + L::OFF_SCHED) + ub * L::LISTMAX;
             int blk = 0;
             uint32_t gated = 0;
@@ -936,8 +1009,9 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
         float* msh = reinterpret_cast<float*>(smem + L::OFF_M);  // [2][BM]
         const float sl2 = p.scale_log2;
         const int64_t nq = sg.nq;
-        const bool merge = p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST;
-        const bool to_acc = p.mode == CDSP_ATTN_FIRST || p.mode == CDSP_ATTN_MID;
+        const bool l_merge = p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST;
+        const bool l_to_acc = p.mode == CDSP_ATTN_FIRST || p.mode == CDSP_ATTN_MID;
+        volatile int* role_sh = reinterpret_cast<volatile int*>(smem + L::OFF_ROLE);  // [NG]
         auto arrive_leader = [&](int b) {  // lane 0, after the warp's tcgen05 ops are fenced
             if constexpr (PAIR) mbar_arrive_remote(lbar(b));
             else mbar_arrive(bar(b));
@@ -1108,7 +1182,16 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
 #ifdef CDSP_KTRACE
             if (r == 0 && g == 0) UNIT_STAMP(u.x * CL + crank, 6, gtime_ns());
 #endif
-            if (N == 0 && p.mode == CDSP_ATTN_MID) continue;  // merging an empty block is the identity
+            // split-unit part, derived again here rather than kept live through the tile loop
+            // (register pressure of the softmax)
+            int part = -1, ux = 0;
+            if (p.split) {
+                int xx = u.x, h2, b0, b1;
+                int64_t r2;
+                asm volatile("" : "+r"(xx));
+                unit_map(xx, crank, h2, r2, part, ux, b0, b1);
+            }
+            if (N == 0 && p.mode == CDSP_ATTN_MID && part < 0) continue;  // merging an empty block is the identity
 
             // ---------------- epilogue: normalise, then write / LSE-merge (R3) ----------------
             // One group finishes the unit: the group E that computed its last tile (it holds the
@@ -1146,139 +1229,163 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             // the accumulator / output belong to the previous launch until it completes (a no-op
             // unless this grid was launched as its programmatic dependent)
             asm volatile("griddepcontrol.wait;" ::: "memory");
-            const float lse_a = merge && row_ok ? p.lse_acc[static_cast<size_t>(head) * nq + row] : -INFINITY;
-            const float inv_l = l > 0.f ? 1.0f / l : 0.f;
-            const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
-            float wa = 0.f, wb = 1.f, lse_out = lse_b;
-            if (merge) merge_weights(lse_a, lse_b, wa, wb, lse_out);
-            const float sbw = wb * inv_l;
-            // PAIR: bf16 rows go through two 128B-swizzled boxes (64 columns each) and TMA stores;
-            // fp32 accumulator rows through each warp's 4 KB slices of the same boxes (coalesced)
-            const bool boxed = PAIR && N > 0 && (CDSP_EPI_COALESCED || !to_acc);
-            const uint32_t stg0 = sbase + L::OFF_STG;
-            const int64_t wrow0 = row0 + 32 * quad;
-            const int nvalid = static_cast<int>(nq - wrow0 < 32 ? (nq - wrow0 > 0 ? nq - wrow0 : 0) : 32);
-            const size_t rstride = static_cast<size_t>(p.Hq) * HD;
-#pragma unroll 1
-            for (int hh = 0; hh < HD / 64; ++hh) {  // O columns [64 hh, 64 hh + 64)
-                uint32_t o[64];
-                if (N > 0) {
-                    if (hh == 0) {
-                        mbar_wait(bar(L::B_OF), (n_units_done - 1) & 1);
-                        tc_fence_after();
-                    }
-                    tmem_ld32p(tO + 64 * hh, o);
-                    tmem_ld32p(tO + 64 * hh + 32, o + 32);
-                    tc_wait_ld();
-                    reg_tie32(o);
-                    reg_tie32(o + 32);
-                    if (hh == HD / 64 - 1) {  // O drained: TMEM back to the next unit's PV
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) arrive_leader(L::B_OE);
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 64; ++q) o[q] = 0u;
-                }
-                if (boxed && to_acc && CDSP_EPI_WIDE) {
-                    // fp32 accumulator, FIRST / MID: the finishing group alone uses the 32 KB of
-                    // boxes, so this warp's 8 KB (its rows of both boxes) carry a 64-column half
-                    // per round trip
-                    const uint32_t t0 = stg0 + static_cast<uint32_t>(quad) * (32 * 128);
-                    const uint32_t t1 = t0 + BM * 128;
-                    float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
-                    if (merge) {
-                        float a[64];
-                        warp_rows_load64(a, acc_w, rstride, nvalid, t0, t1, lane);
-#pragma unroll
-                        for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(fmaf(wa, a[q], __uint_as_float(o[q]) * sbw));
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * sbw);
-                    }
-                    warp_rows_store64(o, acc_w, rstride, nvalid, t0, t1, lane);
-                } else if (boxed) {
-                    const uint32_t box = stg0 + static_cast<uint32_t>(hh) * (BM * 128);
-                    const uint32_t wtile = box + static_cast<uint32_t>(quad) * (32 * 128);
-                    float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        float a[32];
-                        if (merge) warp_rows_load(a, acc_w + 32 * c, rstride, nvalid, wtile, lane);
-#pragma unroll
-                        for (int q = 0; q < 32; ++q) {
-                            float v = __uint_as_float(o[32 * c + q]) * sbw;
-                            if (merge) v = fmaf(wa, a[q], v);
-                            o[32 * c + q] = __float_as_uint(v);
+            // split unit: the first sub-unit to get here leaves its partial in the accumulator rows,
+            // the second merges it (R3) and writes the output
+            // split unit: the first sub-unit to get here leaves its partial in the accumulator rows,
+            // the second merges it (R3) and writes the output.  The epilogue is instantiated per
+            // role (merge / to_acc compile-time there): a per-unit runtime choice costs the
+            // softmax hundreds of bytes of register spills.
+            bool split_first = false;
+            int* scnt = nullptr;
+            if (part >= 0) {
+                scnt = p.split_cnt + 2 * (2 * ux + crank);
+                split_first = split_role(scnt, role_sh + g, g, r) != 0;
+            }
+            auto epilogue = [&](auto MG, auto TA) {  // 0 / 1: fixed; 2: the launch's mode
+                const bool merge = decltype(MG)::value == 2 ? l_merge : decltype(MG)::value == 1;
+                const bool to_acc = decltype(TA)::value == 2 ? l_to_acc : decltype(TA)::value == 1;
+                const float lse_a = merge && row_ok ? p.lse_acc[static_cast<size_t>(head) * nq + row] : -INFINITY;
+                const float inv_l = l > 0.f ? 1.0f / l : 0.f;
+                const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+                float wa = 0.f, wb = 1.f, lse_out = lse_b;
+                if (merge) merge_weights(lse_a, lse_b, wa, wb, lse_out);
+                const float sbw = wb * inv_l;
+                // PAIR: bf16 rows go through two 128B-swizzled boxes (64 columns each) and TMA stores;
+                // fp32 accumulator rows through each warp's 4 KB slices of the same boxes (coalesced)
+                const bool boxed = PAIR && N > 0 && (CDSP_EPI_COALESCED || !to_acc);
+                const uint32_t stg0 = sbase + L::OFF_STG;
+                const int64_t wrow0 = row0 + 32 * quad;
+                const int nvalid = static_cast<int>(nq - wrow0 < 32 ? (nq - wrow0 > 0 ? nq - wrow0 : 0) : 32);
+                const size_t rstride = static_cast<size_t>(p.Hq) * HD;
+    #pragma unroll 1
+                for (int hh = 0; hh < HD / 64; ++hh) {  // O columns [64 hh, 64 hh + 64)
+                    uint32_t o[64];
+                    if (N > 0) {
+                        if (hh == 0) {
+                            mbar_wait(bar(L::B_OF), (n_units_done - 1) & 1);
+                            tc_fence_after();
                         }
-                    }
-                    if (to_acc) {
-#pragma unroll
-                        for (int c = 0; c < 2; ++c) warp_rows_store(o + 32 * c, acc_w + 32 * c, rstride, nvalid, wtile, lane);
-                    } else {
-                        const uint32_t rsw = static_cast<uint32_t>(r & 7), rowa = box + static_cast<uint32_t>(r) * 128;
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {  // 16-byte chunk q of the 128-byte row
-                            const uint32_t* w = o + 8 * q;
-                            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rowa + ((static_cast<uint32_t>(q) ^ rsw) << 4)),
-                                         "r"(pack_bf16(__uint_as_float(w[0]), __uint_as_float(w[1]))),
-                                         "r"(pack_bf16(__uint_as_float(w[2]), __uint_as_float(w[3]))),
-                                         "r"(pack_bf16(__uint_as_float(w[4]), __uint_as_float(w[5]))),
-                                         "r"(pack_bf16(__uint_as_float(w[6]), __uint_as_float(w[7])))
-                                         : "memory");
+                        tmem_ld32p(tO + 64 * hh, o);
+                        tmem_ld32p(tO + 64 * hh + 32, o + 32);
+                        tc_wait_ld();
+                        reg_tie32(o);
+                        reg_tie32(o + 32);
+                        if (hh == HD / 64 - 1) {  // O drained: TMEM back to the next unit's PV
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) arrive_leader(L::B_OE);
                         }
+                    } else {
+    #pragma unroll
+                        for (int q = 0; q < 64; ++q) o[q] = 0u;
                     }
-                } else if (row_ok) {
-                    const size_t orow = (static_cast<size_t>(row) * p.Hq + head) * HD + 64 * hh;
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        float v[32];
-#pragma unroll
-                        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(o[32 * c + q]) * sbw;
+                    if (boxed && to_acc && CDSP_EPI_WIDE) {
+                        // fp32 accumulator, FIRST / MID: the finishing group alone uses the 32 KB of
+                        // boxes, so this warp's 8 KB (its rows of both boxes) carry a 64-column half
+                        // per round trip
+                        const uint32_t t0 = stg0 + static_cast<uint32_t>(quad) * (32 * 128);
+                        const uint32_t t1 = t0 + BM * 128;
+                        float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
                         if (merge) {
-                            const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                const float4 av = a4[q];
-                                v[4 * q + 0] = fmaf(wa, av.x, v[4 * q + 0]);
-                                v[4 * q + 1] = fmaf(wa, av.y, v[4 * q + 1]);
-                                v[4 * q + 2] = fmaf(wa, av.z, v[4 * q + 2]);
-                                v[4 * q + 3] = fmaf(wa, av.w, v[4 * q + 3]);
+                            float a[64];
+                            warp_rows_load64(a, acc_w, rstride, nvalid, t0, t1, lane);
+    #pragma unroll
+                            for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(fmaf(wa, a[q], __uint_as_float(o[q]) * sbw));
+                        } else {
+    #pragma unroll
+                            for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * sbw);
+                        }
+                        warp_rows_store64(o, acc_w, rstride, nvalid, t0, t1, lane);
+                    } else if (boxed) {
+                        const uint32_t box = stg0 + static_cast<uint32_t>(hh) * (BM * 128);
+                        const uint32_t wtile = box + static_cast<uint32_t>(quad) * (32 * 128);
+                        float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
+    #pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            float a[32];
+                            if (merge) warp_rows_load(a, acc_w + 32 * c, rstride, nvalid, wtile, lane);
+    #pragma unroll
+                            for (int q = 0; q < 32; ++q) {
+                                float v = __uint_as_float(o[32 * c + q]) * sbw;
+                                if (merge) v = fmaf(wa, a[q], v);
+                                o[32 * c + q] = __float_as_uint(v);
                             }
                         }
                         if (to_acc) {
-                            float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow + 32 * c);
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    #pragma unroll
+                            for (int c = 0; c < 2; ++c) warp_rows_store(o + 32 * c, acc_w + 32 * c, rstride, nvalid, wtile, lane);
                         } else {
-                            uint4* d4 = reinterpret_cast<uint4*>(p.out + orow + 32 * c);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                d4[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                                                   pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+                            const uint32_t rsw = static_cast<uint32_t>(r & 7), rowa = box + static_cast<uint32_t>(r) * 128;
+    #pragma unroll
+                            for (int q = 0; q < 8; ++q) {  // 16-byte chunk q of the 128-byte row
+                                const uint32_t* w = o + 8 * q;
+                                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rowa + ((static_cast<uint32_t>(q) ^ rsw) << 4)),
+                                             "r"(pack_bf16(__uint_as_float(w[0]), __uint_as_float(w[1]))),
+                                             "r"(pack_bf16(__uint_as_float(w[2]), __uint_as_float(w[3]))),
+                                             "r"(pack_bf16(__uint_as_float(w[4]), __uint_as_float(w[5]))),
+                                             "r"(pack_bf16(__uint_as_float(w[6]), __uint_as_float(w[7])))
+                                             : "memory");
+                            }
+                        }
+                    } else if (row_ok) {
+                        const size_t orow = (static_cast<size_t>(row) * p.Hq + head) * HD + 64 * hh;
+    #pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            float v[32];
+    #pragma unroll
+                            for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(o[32 * c + q]) * sbw;
+                            if (merge) {
+                                const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
+    #pragma unroll
+                                for (int q = 0; q < 8; ++q) {
+                                    const float4 av = a4[q];
+                                    v[4 * q + 0] = fmaf(wa, av.x, v[4 * q + 0]);
+                                    v[4 * q + 1] = fmaf(wa, av.y, v[4 * q + 1]);
+                                    v[4 * q + 2] = fmaf(wa, av.z, v[4 * q + 2]);
+                                    v[4 * q + 3] = fmaf(wa, av.w, v[4 * q + 3]);
+                                }
+                            }
+                            if (to_acc) {
+                                float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow + 32 * c);
+    #pragma unroll
+                                for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                            } else {
+                                uint4* d4 = reinterpret_cast<uint4*>(p.out + orow + 32 * c);
+    #pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    d4[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                                       pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+                            }
                         }
                     }
                 }
-            }
-            if (boxed && !to_acc) {
-                fence_proxy_async_smem();
-                named_bar_sync(8 + g, BM);  // this group's 128 rows are in the boxes
-                if (threadIdx.x == static_cast<unsigned>(g * BM)) {
-                    for (int hh = 0; hh < HD / 64; ++hh)
-                        tma_store_3d(&tm.out, stg0 + static_cast<uint32_t>(hh) * (BM * 128), 64 * hh, head,
-                                     static_cast<int>(row0));  // rows >= nq clipped
-                    bulk_commit();
-                    bulk_wait_read0();  // the boxes are free again (the next unit may finish in another group)
+                if (boxed && !to_acc) {
+                    fence_proxy_async_smem();
+                    named_bar_sync(8 + g, BM);  // this group's 128 rows are in the boxes
+                    if (threadIdx.x == static_cast<unsigned>(g * BM)) {
+                        for (int hh = 0; hh < HD / 64; ++hh)
+                            tma_store_3d(&tm.out, stg0 + static_cast<uint32_t>(hh) * (BM * 128), 64 * hh, head,
+                                         static_cast<int>(row0));  // rows >= nq clipped
+                        bulk_commit();
+                        bulk_wait_read0();  // the boxes are free again (the next unit may finish in another group)
+                    }
                 }
-            }
-            if (row_ok) {
-                const size_t li = static_cast<size_t>(head) * nq + row;
-                if (to_acc) {
-                    p.lse_acc[li] = lse_out;
-                } else if (p.lse) {
-                    p.lse[li] = lse_out;
+                if (row_ok) {
+                    const size_t li = static_cast<size_t>(head) * nq + row;
+                    if (to_acc) {
+                        p.lse_acc[li] = lse_out;
+                    } else if (p.lse) {
+                        p.lse[li] = lse_out;
+                    }
                 }
+            };
+            if (part < 0) epilogue(IntC<2>{}, IntC<2>{});
+            else if (split_first) epilogue(IntC<0>{}, IntC<1>{});
+            else epilogue(IntC<1>{}, IntC<0>{});
+            if (split_first) {  // publish the partial (every thread's stores, then one release)
+                __threadfence();
+                named_bar_sync(12 + g, BM);
+                if (r == 0) asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(scnt + 1), "r"(1) : "memory");
             }
 #ifdef CDSP_KTRACE
             if (r == 0) {
@@ -1349,22 +1456,45 @@ cdsp_status make_map(CUtensorMap* m, const void* base, int64_t T, int H, int D, 
     return CDSP_OK;
 }
 
-// Unit counters of the persistent kernel: one [claim, done] pair per launch, taken round-robin
-// from a zeroed ring (each launch's last CTA re-zeroes its pair; a pair is reused only after
-// kClaimSlots later launches, far more than can run concurrently).
+// Per-device kernel state, allocated once (attention_device_init, called by cdsp_comm_create;
+// a comm-less first cdsp_attention_fwd* call on a device allocates it then):
+//  * unit counters of the persistent kernel: one [claim, done] pair per launch, taken
+//    round-robin from a zeroed ring (each launch's last CTA re-zeroes its pair; a pair is reused
+//    only after kClaimSlots later launches, far more than can run concurrently);
+//  * split-unit counters: a launch with S split units takes 4 S ints ([unit][2 CTAs][arrivals,
+//    ready]) from a zeroed ring of kSplitRing ints (bump allocation; every pair is re-zeroed by
+//    its second finisher, and a range is reused only after the ring wrapped, i.e. after at
+//    least kSplitRing / (4 kSplitUnits) = 32 later split launches).
 constexpr int kClaimSlots = 4096;
-cdsp_status claim_slot(int** out) {
-    static int* ring[64] = {};
-    static unsigned counter[64] = {};
+constexpr int kSplitUnits = 32768;  // split units per launch (more: the launch runs unsplit)
+constexpr int64_t kSplitRing = 32ll * 4 * kSplitUnits;
+struct DevState {
+    int* ring = nullptr;
+    int* split = nullptr;
+    unsigned counter = 0;
+    int64_t split_next = 0;
+};
+DevState g_dev[64];
+
+cdsp_status device_state(DevState** out) {
     int dev = 0;
     CDSP_CUDA(cudaGetDevice(&dev));
     CDSP_REQUIRE(dev >= 0 && dev < 64, CDSP_ERR_CUDA, "device ordinal %d", dev);
-    if (!ring[dev]) {
-        CDSP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ring[dev]), kClaimSlots * 2 * sizeof(int)));
-        CDSP_CUDA(cudaMemset(ring[dev], 0, kClaimSlots * 2 * sizeof(int)));
+    DevState& d = g_dev[dev];
+    if (!d.ring) {
+        CDSP_CUDA(cudaMalloc(reinterpret_cast<void**>(&d.ring), kClaimSlots * 2 * sizeof(int)));
+        CDSP_CUDA(cudaMemset(d.ring, 0, kClaimSlots * 2 * sizeof(int)));
+        CDSP_CUDA(cudaMalloc(reinterpret_cast<void**>(&d.split), kSplitRing * sizeof(int)));
+        CDSP_CUDA(cudaMemset(d.split, 0, kSplitRing * sizeof(int)));
         CDSP_CUDA(cudaDeviceSynchronize());
     }
-    *out = ring[dev] + 2 * (__atomic_fetch_add(&counter[dev], 1u, __ATOMIC_RELAXED) % kClaimSlots);
+    *out = &d;
+    return CDSP_OK;
+}
+cdsp_status claim_slot(int** out) {
+    DevState* d = nullptr;
+    CDSP_CHECK_STATUS(device_state(&d));
+    *out = d->ring + 2 * (__atomic_fetch_add(&d->counter, 1u, __ATOMIC_RELAXED) % kClaimSlots);
     return CDSP_OK;
 }
 
@@ -1427,7 +1557,20 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     p.g = a.Hq / a.Hkv;
     p.n_rb = static_cast<int>((s0.nq + BM - 1) / BM);
     p.n_pb = PAIR ? (p.n_rb + 1) / 2 : p.n_rb;
-    const int64_t units = static_cast<int64_t>(p.n_pb) * a.Hq;
+    static const int split_env = getenv("CDSP_SPLIT") ? atoi(getenv("CDSP_SPLIT")) : 1;
+    const int hi = (p.n_pb + 1) / 2;
+    DevState* dst = nullptr;
+    CDSP_CHECK_STATUS(device_state(&dst));
+    p.split = split_env && a.split_ok && p.n_pb > 1 && a.nblk >= 2 && a.mode == CDSP_ATTN_ONLY && a.o_acc &&
+              a.lse_acc && static_cast<int64_t>(hi) * a.Hq <= kSplitUnits;
+    p.split_blk = (a.nblk + 1) / 2;
+    if (p.split) {
+        const int64_t need = 4ll * hi * a.Hq;
+        if (dst->split_next + need > kSplitRing) dst->split_next = 0;
+        p.split_cnt = dst->split + dst->split_next;
+        dst->split_next += need;
+    }
+    const int64_t units = static_cast<int64_t>(p.n_pb) * a.Hq + (p.split ? static_cast<int64_t>(hi) * a.Hq : 0);
     if (units == 0) return CDSP_OK;
     CDSP_REQUIRE(units < (1ll << 30), CDSP_ERR_SHAPE, "too many query tiles");
     p.n_units = static_cast<int>(units);
@@ -1499,6 +1642,11 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
+
+cdsp_status attention_device_init() {
+    DevState* d = nullptr;
+    return device_state(&d);
+}
 
 int attention_tc_max_tiles(int D) {
     static const bool no_pair = getenv("CDSP_ATTN_1SM") != nullptr;

@@ -473,6 +473,10 @@ cdsp_status phase_ring(cdsp_comm c, const ChunkInfo& ci, int r, int layer, const
         AttnArgs a = attn_args(c, q, Hq, scale, mode, out, lse);
         a.nblk = k1 - k0;
         a.pdl = i > 0;  // the accumulator is this chain's own
+        // one launch: heavy units may be split and merged through the accumulator rows when
+        // they are reserved for this shard
+        a.split_ok = rl.n == 1 && c->acc_rows >= m2 && c->acc_hq >= Hq;
+        if (!a.split_ok && rl.n == 1) a.o_acc = a.lse_acc = nullptr;
         for (int k = k0; k < k1; ++k) {
             const int b = k - k0;
             a.k[b] = k == 0 ? layer_k(c, c->self, layer) : c->recv_k[k - 1];
@@ -569,6 +573,7 @@ cdsp_status cdsp_comm_create_layers(cdsp_comm* out, int32_t rank, int32_t world,
     CDSP_REQUIRE(D == 64 || D == 128, CDSP_ERR_SHAPE, "head dim %d not in {64,128}", D);
     CDSP_REQUIRE(dtype_ok(dtype), CDSP_ERR_DTYPE, "bad dtype %d", dtype);
     CDSP_CUDA(cudaSetDevice(device));
+    CDSP_CHECK_STATUS(attention_device_init());  // kernel counters: no allocation on the prefill path
     cdsp_comm c = new cdsp_comm_s();
     c->rank = rank;
     c->world = world;
@@ -1217,6 +1222,7 @@ cdsp_status cdsp_attention_fwd_blocks(const cdsp_tensor* q, int32_t nblk, const 
     a.out = final_out ? out->ptr : nullptr;
     a.lse = lse;
     a.pdl = pdl;
+    a.split_ok = mode == CDSP_ATTN_ONLY && o_acc && lse_acc;  // scratch given: heavy units may split
     return run_attention(a, static_cast<cudaStream_t>(cuda_stream));
 }
 

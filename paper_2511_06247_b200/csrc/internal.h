@@ -35,7 +35,14 @@ struct AttnArgs {
     int gate_ng = 1, gate_hpg = 1;
     int* gate_err = nullptr;
     int spare_sms = 0;  // leave at least this many SMs to other kernels (persistent bf16 grid)
+    // an ONLY-mode multi-block launch may split its heavy units, merging them through o_acc /
+    // lse_acc (their rows are scratch then)
+    bool split_ok = false;
 };
+
+// Per-device kernel state (unit counters), allocated once; cdsp_comm_create calls it so the
+// prefill path never allocates.
+cdsp_status attention_device_init();
 
 // KV tiles (128 keys) the bf16 kernel can list per launch (all blocks together).
 int attention_tc_max_tiles(int D);

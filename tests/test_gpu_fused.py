@@ -67,6 +67,33 @@ def test_blocks_one_launch_equals_full_causal(s, m, h, Hq, Hkv, D):
         assert lerr <= LSE_TOL, (r, err, lerr)
 
 
+@pytest.mark.parametrize("s,m,h,Hq,Hkv", [(8, 256, 0, 4, 4), (4, 384, 128, 4, 2), (2, 512, 0, 2, 1), (8, 512, 256, 8, 2)])
+def test_blocks_split_units_with_scratch(s, m, h, Hq, Hkv):
+    """ONLY mode with o_acc / lse_acc scratch: heavy (upper) units run as two sub-units merged
+    in-kernel; every rank's rows still equal full causal attention (and the scratch-free launch)."""
+    D = 128
+    C = s * h
+    N = C + 2 * s * m
+    q, k, v = qkv(N, Hq, Hkv, D, torch.bfloat16, seed=s * 3 + m)
+    o_ref, l_ref = oracle.causal_rows(q.float().numpy(), k.float().numpy(), v.float().numpy(), 1.0 / math.sqrt(D))
+    for r in range(s):
+        ks, vs, segs, qrows = _ring_blocks(s, r, m, h, C, k, v)
+        qd = q[qrows].contiguous().cuda()
+        ks, vs = [x.cuda() for x in ks], [x.cuda() for x in vs]
+        acc = torch.full((2 * m, Hq, D), float("nan"), dtype=torch.float32, device="cuda")
+        lacc = torch.full((Hq, 2 * m), float("nan"), dtype=torch.float32, device="cuda")
+        out = torch.empty_like(qd)
+        lse = torch.empty((Hq, 2 * m), dtype=torch.float32, device="cuda")
+        for _ in range(3):  # repeated launches: the split counters are re-armed by each launch
+            api.attention_fwd_blocks(qd, ks, vs, segs, 0.0, api.ATTN_ONLY, o_acc=acc, lse_acc=lacc, out=out, lse=lse)
+        out2 = torch.empty_like(qd)
+        api.attention_fwd_blocks(qd, ks, vs, segs, 0.0, api.ATTN_ONLY, out=out2)
+        torch.cuda.synchronize()
+        assert_out_close(out.float().cpu().numpy(), o_ref[qrows.numpy()], True, f"rank {r} split")
+        assert np.abs(lse.cpu().numpy() - l_ref[:, qrows.numpy()]).max() <= LSE_TOL, r
+        assert_out_close(out2.float().cpu().numpy(), o_ref[qrows.numpy()], True, f"rank {r} unsplit")
+
+
 def test_blocks_first_last_chain_with_pdl():
     """The same union split into two launches (FIRST over blocks 0-1, LAST over 2-3, the LAST
     as a programmatic dependent) equals the one-launch result within tolerance."""
@@ -161,14 +188,18 @@ def test_multi_launch_ring_needs_reserved_accumulators():
 
 def test_control_run_reuses_prestaged_blocks():
     """RING_CONTROL: no pulls — a second call with the same inputs over the blocks the first
-    call pulled reproduces the first call's output bit for bit."""
+    call pulled reproduces the first call's output (up to the order in which split sub-units
+    merge, which is decided at run time: same tolerance as against the oracle)."""
     plan_list = [(4096, list(range(4)))]
     comms, out1, lse1, (q, k, v), plan = _loopback(plan_list, 4096, 4, 4, 128, torch.bfloat16, 0)
     for c in comms:
         c.set_ring_options(api.RING_CONTROL)
     out2, lse2 = run_plan_loopback(q.cuda(), k.cuda(), v.cuda(), plan, comms=comms)
     torch.cuda.synchronize()
-    assert torch.equal(out1, out2) and torch.equal(lse1, lse2)
+    o_ref, l_ref = oracle.causal_rows(q.float().numpy(), k.float().numpy(), v.float().numpy(), 1.0 / math.sqrt(128))
+    assert_out_close(out2.float().cpu().numpy(), o_ref, True, "control run")
+    assert np.abs(lse2.cpu().numpy() - l_ref).max() <= LSE_TOL
+    assert (out1.float() - out2.float()).abs().max().item() <= 2 ** -6  # one bf16 ulp at |o| < 2
     for c in comms:
         c.close()
 

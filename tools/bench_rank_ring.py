@@ -1,9 +1,11 @@
 """Per-GPU ring compute at SP = s, on one B200: the attention ONE rank of an s-GPU ring runs
 for a chunk, with the peer blocks already resident (the ring pulls run on copy engines and
 are timed by bench.py's `ring` field on a real multi-GPU run).  Two designs:
-  fused:    one cdsp_attention_fwd_blocks launch walking all s blocks (step 0 self/causal,
-            then src = (r - k) mod s, P:59 / R10-R11) with O resident in TMEM — what
-            cdsp_prefill_chunk runs;
+  split:    one cdsp_attention_fwd_blocks launch walking all s blocks (step 0 self/causal,
+            then src = (r - k) mod s, P:59 / R10-R11) with O resident in TMEM, heavy units split
+            over two block ranges and merged through the accumulator scratch — what
+            cdsp_prefill_chunk runs when accumulators are reserved;
+  fused:    the same without scratch (no splitting);
   stepwise: s cdsp_attention_fwd launches FIRST / MID / LAST merged through fp32
             accumulators (MID / LAST as programmatic dependents) — the round-1 design.
 Every rank r = 0..s-1 is timed on its own, back to back on one stream; a real ring ends when
@@ -33,7 +35,7 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--sizes", default="1,2,4,8")
     ap.add_argument("--hist-per-rank", type=int, default=0)
-    ap.add_argument("--modes", default="fused,stepwise")
+    ap.add_argument("--modes", default="split,fused,stepwise")
     ap.add_argument("--ranks", default="all", help="'all' or a comma list of ring ranks to time")
     args = ap.parse_args()
     L, H, D = args.seq, args.heads, 128
@@ -67,10 +69,11 @@ def main():
             return api.segments(2 * m, m, pos0(r), pos1(r), h + 2 * m, h, m, pos0(src), pos1(src))
 
         def run_rank(r, mode):
-            if mode == "fused" or s == 1:
+            if mode in ("fused", "split") or s == 1:
                 srcs = [(r - step) % s for step in range(s)]
+                scratch = dict(o_acc=o_acc, lse_acc=lse_acc) if mode == "split" else {}
                 api.attention_fwd_blocks(shards[r][0], [shards[x][1] for x in srcs], [shards[x][2] for x in srcs],
-                                         [seg(r, x) for x in srcs], 0.0, api.ATTN_ONLY, out=out)
+                                         [seg(r, x) for x in srcs], 0.0, api.ATTN_ONLY, out=out, **scratch)
                 return
             for step in range(s):
                 src = (r - step) % s

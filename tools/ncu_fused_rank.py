@@ -19,6 +19,7 @@ ap.add_argument("--seq", type=int, default=32768)
 ap.add_argument("--heads", type=int, default=32)
 ap.add_argument("--kv-heads", type=int, default=None)
 ap.add_argument("--launches", type=int, default=2)
+ap.add_argument("--split", action="store_true", help="pass accumulator scratch (heavy units split)")
 a = ap.parse_args()
 L, H, D, s, r = a.seq, a.heads, 128, a.s, a.r
 Hkv = a.kv_heads or H
@@ -28,8 +29,12 @@ sh = [(api.zigzag_gather(q, s, x), api.zigzag_gather(k, s, x), api.zigzag_gather
 srcs = [(r - step) % s for step in range(s)]
 segs = [api.segments(2 * m, m, r * m, (2 * s - 1 - r) * m, 2 * m, 0, m, x * m, (2 * s - 1 - x) * m) for x in srcs]
 out = torch.empty_like(sh[r][0])
+kw = {}
+if a.split:
+    kw = dict(o_acc=torch.empty(2 * m, H, D, dtype=torch.float32, device="cuda"),
+              lse_acc=torch.empty(H, 2 * m, dtype=torch.float32, device="cuda"))
 for _ in range(a.launches):
     api.attention_fwd_blocks(sh[r][0], [sh[x][1] for x in srcs], [sh[x][2] for x in srcs], segs, 0.0, api.ATTN_ONLY,
-                             out=out)
+                             out=out, **kw)
 torch.cuda.synchronize()
 print("flops", 4.0 * D * H * L * (L + 1) / 2 / s)

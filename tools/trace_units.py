@@ -87,3 +87,21 @@ if __name__ == "__main__":
     torch.cuda.synchronize()
     print("== s=8 ring step (r=3, src=1), MID")
     analyze(os.path.join(out_dir, "trace_ring.bin"), (2 * m // 128) * H)
+    # fused ring launches of ranks 0 and 7 (all 8 blocks in one launch)
+    sh = [(api.zigzag_gather(q, s, x), api.zigzag_gather(k, s, x), api.zigzag_gather(v, s, x)) for x in range(s)]
+    acc = torch.empty(2 * m, H, D, dtype=torch.float32, device="cuda")
+    lacc = torch.empty(H, 2 * m, dtype=torch.float32, device="cuda")
+    for r, split in ((0, False), (0, True), (7, False), (7, True)):
+        srcs = [(r - st) % s for st in range(s)]
+        segs = [api.segments(2 * m, m, r * m, (2 * s - 1 - r) * m, 2 * m, 0, m, x * m, (2 * s - 1 - x) * m) for x in srcs]
+        outr = torch.empty_like(sh[r][0])
+        args = (sh[r][0], [sh[x][1] for x in srcs], [sh[x][2] for x in srcs], segs, 0.0, api.ATTN_ONLY)
+        kw = dict(out=outr, o_acc=acc, lse_acc=lacc) if split else dict(out=outr)
+        api.attention_fwd_blocks(*args, **kw)
+        torch.cuda.synchronize()
+        os.environ["CDSP_TRACE"] = os.path.join(out_dir, f"trace_fused_r{r}.bin")
+        api.attention_fwd_blocks(*args, **kw)
+        torch.cuda.synchronize()
+        del os.environ["CDSP_TRACE"]
+        print(f"== s=8 fused ring launch, rank {r}{' (split units)' if split else ''}")
+        analyze(os.path.join(out_dir, f"trace_fused_r{r}.bin"), (2 * m // 128) * H * (2 if split else 1))
