@@ -52,6 +52,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "attn_common.cuh"
 #include "common.cuh"
@@ -87,6 +88,10 @@
 
 #ifndef CDSP_EPI_COALESCED  // fp32 accumulator epilogue through the warp-transpose tiles (PAIR)
 #define CDSP_EPI_COALESCED 1
+#endif
+
+#ifndef CDSP_KV_POLICY  // L2 policy of the K / V tile loads: 0 evict_last, 1 evict_normal, 2 evict_first
+#define CDSP_KV_POLICY 0
 #endif
 
 #ifndef CDSP_EMU_MASK
@@ -193,14 +198,15 @@ struct TcParams {
     float* lse;
     int* claim;  // [2]: dynamic unit counter, finished-CTA counter (both zero at launch; the last CTA re-zeroes them)
     int n_pb;    // row blocks per head in units of the CTA group (PAIR: pairs of 128-row blocks)
-    // Split units (multi-block launches): every upper unit (the upper row blocks also see the
-    // later blocks' keys on a ring rank: the heavy units) runs as two
-    // sub-units, blocks [0, split_blk) and [split_blk, nblk), claimed back to back.  The first
+    // Split units (multi-block launches): the n_split heaviest units of every head (the top row
+    // blocks: a unit's work grows with its rows' positions) run as two sub-units, blocks
+    // [0, split_blk) and [split_blk, nblk), claimed back to back.  The first
     // to finish writes its normalised partial and LSE into the o_acc / lse_acc rows of the unit
     // (R3 operands), the second merges it with its own and writes the output: a heavy unit no
     // longer sets the launch's tail.  split_cnt: per (unit, CTA) {arrivals, partial-ready}, zero
     // between launches (the second finisher re-zeroes its pair).
-    int split, split_blk;
+    int split, split_blk;  // split: number of split units per head of region B (0: none)
+    int n_light, heads_a;  // unit order regions (see unit_map)
     int* split_cnt;
 };
 
@@ -308,6 +314,16 @@ __device__ __forceinline__ void tmem_ld32p(uint32_t taddr, uint32_t* r) {
           "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
           "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
+}
+
+__device__ __forceinline__ uint64_t kv_policy() {
+#if CDSP_KV_POLICY == 1
+    return policy_evict_normal();
+#elif CDSP_KV_POLICY == 2
+    return policy_evict_first();
+#else
+    return policy_evict_last();
+#endif
 }
 
 template <int V>
@@ -623,31 +639,43 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
     auto lbar = [&](int i) { return PAIR ? mapa_shared(bar(i), 0) : bar(i); };
     // unit x -> head, first row, part (-1: whole unit; 0 / 1: sub-unit of a split unit whose
     // counter index is *ux) and its block range [*b0, *b1)
-    // Order: head-major (the units in flight share a few heads' K/V in L2: every unit of a head
-    // streams the same K/V tiles), heaviest row blocks first within a head.  Split launches:
-    // a head's upper units come as two adjacent sub-units each.
+    // Order (three regions):
+    //  A  heads [0, heads_a): the heavy row blocks (pb >= n_light) head-major, heaviest first
+    //     within a head — the units in flight share a few heads' K/V in L2 (every unit of a head
+    //     streams the same tiles);
+    //  B  heads [heads_a, Hq): the same, the n_split heaviest units of each head as two adjacent
+    //     sub-units (the launch's last wave comes in halves: no heavy unit sets the tail);
+    //  C  every head's light row blocks (pb < n_light), which fill the tail.
     auto unit_map = [&](int x, int c, int& head, int64_t& row0, int& part, int& ux, int& b0, int& b1) {
         int pb;
         part = -1;
         b0 = 0;
         b1 = p.nblk;
         ux = x;
-        if (p.split) {
-            const int hi = (p.n_pb + 1) / 2, lo = p.n_pb - hi, per = 2 * hi + lo;
-            head = x / per;
-            const int y = x - head * per;
-            if (y < 2 * hi) {
+        const int nh = p.n_pb - p.n_light;       // heavy row blocks per head
+        const int na = p.heads_a * nh;           // region A units
+        const int nbh = nh + p.split;            // region B units per head
+        const int nb = (p.Hq - p.heads_a) * nbh;
+        if (x < na) {
+            head = x / nh;
+            pb = p.n_pb - 1 - (x - head * nh);
+        } else if (x < na + nb) {
+            const int xb = x - na;
+            const int hb = xb / nbh, y = xb - hb * nbh;
+            head = p.heads_a + hb;
+            if (y < 2 * p.split) {
                 part = y & 1;
                 pb = p.n_pb - 1 - (y >> 1);
-                ux = head * hi + (y >> 1);
+                ux = hb * p.split + (y >> 1);
                 if (part == 0) b1 = p.split_blk;
                 else b0 = p.split_blk;
             } else {
-                pb = lo - 1 - (y - 2 * hi);
+                pb = p.n_pb - 1 - (y - p.split);
             }
         } else {
-            head = x / p.n_pb;
-            pb = p.n_pb - 1 - x % p.n_pb;
+            const int xc = x - na - nb;
+            head = xc / p.n_light;
+            pb = p.n_light - 1 - (xc - head * p.n_light);
         }
         row0 = static_cast<int64_t>(PAIR ? 2 * pb + c : pb) * BM;
     };
@@ -717,7 +745,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
         // ======== unit scheduler + TMA producer of Q and K: for each unit, list its used KV
         // tiles in order (empty ones skipped), publish the unit (u_full[i&1]) and stream its
         // Q tile and K tiles (3 stages) ========
-        const uint64_t pol_kv = policy_evict_last();
+        const uint64_t pol_kv = kv_policy();
         const uint64_t pol_q = policy_evict_first();
         int x = static_cast<int>(blockIdx.x) / CL;
         int x_pre = 0;  // leader lane 0: the unit after x, claimed one unit ahead
@@ -866,7 +894,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
         }
     } else if (warp == W_V) {
         // ======== TMA producer of V, following the published units ========
-        const uint64_t pol_kv = policy_evict_last();
+        const uint64_t pol_kv = kv_policy();
         int it = 0;
         for (int i = 0;; ++i) {
             const int ub = i & 1;
@@ -1506,6 +1534,39 @@ int sm_count() {
     return n[dev];
 }
 
+// KV tiles (BN keys) a query row range [r0, r1) touches in block b (b < 0: all blocks): history
+// tiles, then the tiles of the key rows of each segment whose positions reach the range's
+// largest query position.  Host-side estimate for unit weights (exact for unmasked rows).
+int64_t unit_tiles(const cdsp_segments* seg, int nblk, int64_t r0, int64_t r1, int only_b) {
+    int64_t qlo, qhi;
+    bool any;
+    seg_qrange(seg[0], r0, r1, qlo, qhi, any);
+    if (!any) return 0;
+    int64_t t = 0;
+    for (int b = 0; b < nblk; ++b) {
+        if (only_b >= 0 && b != only_b) continue;
+        const cdsp_segments& s = seg[b];
+        const int64_t st = s.pos_stride > 0 ? s.pos_stride : 1;
+        auto upto = [&](int64_t pos0, int64_t len) -> int64_t {  // rows of a segment with pos <= qhi
+            if (len <= 0 || qhi < pos0) return 0;
+            const int64_t n = (qhi - pos0) / st + 1;
+            return n < len ? n : len;
+        };
+        const int64_t e0 = s.kv_hist + s.kv_len0;
+        const int64_t a_end = s.kv_hist + upto(s.kv_pos0, s.kv_len0);  // rows [0, a_end) used
+        const int64_t b_len = upto(s.kv_pos1, s.nkv - e0);              // rows [e0, e0 + b_len) used
+        const int64_t ta = (a_end + BN - 1) / BN;
+        int64_t tb = 0;
+        if (b_len > 0) {
+            const int64_t j0 = e0 / BN, j1 = (e0 + b_len - 1) / BN;
+            const int64_t shared = j0 < ta ? (ta - j0 < j1 - j0 + 1 ? ta - j0 : j1 - j0 + 1) : 0;
+            tb = j1 - j0 + 1 - shared;
+        }
+        t += ta + tb;
+    }
+    return t;
+}
+
 template <int HD, bool PAIR>
 cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     using Lt = Layout<HD, PAIR>;
@@ -1558,19 +1619,62 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     p.n_rb = static_cast<int>((s0.nq + BM - 1) / BM);
     p.n_pb = PAIR ? (p.n_rb + 1) / 2 : p.n_rb;
     static const int split_env = getenv("CDSP_SPLIT") ? atoi(getenv("CDSP_SPLIT")) : 1;
-    const int hi = (p.n_pb + 1) / 2;
+    static const int light_env = getenv("CDSP_LIGHT_LAST") ? atoi(getenv("CDSP_LIGHT_LAST")) : 1;
     DevState* dst = nullptr;
     CDSP_CHECK_STATUS(device_state(&dst));
-    p.split = split_env && a.split_ok && p.n_pb > 1 && a.nblk >= 2 && a.mode == CDSP_ATTN_ONLY && a.o_acc &&
-              a.lse_acc && static_cast<int64_t>(hi) * a.Hq <= kSplitUnits;
+    p.split = 0;
     p.split_blk = (a.nblk + 1) / 2;
-    if (p.split) {
-        const int64_t need = 4ll * hi * a.Hq;
-        if (dst->split_next + need > kSplitRing) dst->split_next = 0;
-        p.split_cnt = dst->split + dst->split_next;
-        dst->split_next += need;
+    p.n_light = 0;
+    p.heads_a = a.Hq;
+    if (p.n_pb > 1 && (light_env || split_env)) {
+        // unit weights (KV tiles) per row block; non-decreasing in pb (a row's keys grow with
+        // its position)
+        std::vector<int64_t> w(p.n_pb);
+        int64_t W = 0;
+        for (int pb = 0; pb < p.n_pb; ++pb) {
+            w[pb] = unit_tiles(a.seg, a.nblk, static_cast<int64_t>(pb) * (PAIR ? 2 : 1) * BM,
+                               static_cast<int64_t>(pb + 1) * (PAIR ? 2 : 1) * BM, -1);
+            W += w[pb];
+        }
+        const int64_t wmax = w[p.n_pb - 1];
+        if (light_env)  // light units: under 1/8 of the heaviest (they go last and fill the tail)
+            while (p.n_light < p.n_pb - 1 && w[p.n_light] * 8 < wmax) ++p.n_light;
+        // split (ONLY-mode multi-block launches with scratch): units heavier than a sixth of a CTA
+        // group's share, in the heads of the last ~1.5 waves, at the block boundary that halves
+        // the heaviest unit
+        const double share = static_cast<double>(W) * a.Hq / max_groups;
+        int n = 0;
+        if (split_env && a.split_ok && a.nblk >= 2 && a.mode == CDSP_ATTN_ONLY && a.o_acc && a.lse_acc)
+            while (n < p.n_pb - p.n_light && w[p.n_pb - 1 - n] * 6.0 > share && w[p.n_pb - 1 - n] >= 32) ++n;
+        if (n > 0) {
+            const int per_head = p.n_pb - p.n_light + n;
+            int hb = static_cast<int>((3 * max_groups / 2 + per_head - 1) / per_head);
+            if (split_env >= 2) hb = a.Hq;  // CDSP_SPLIT=2: split in every head (measurement)
+            if (hb > a.Hq) hb = a.Hq;
+            if (static_cast<int64_t>(hb) * n <= kSplitUnits) {
+                p.split = n;
+                p.heads_a = a.Hq - hb;
+                const int64_t top0 = static_cast<int64_t>(p.n_pb - 1) * (PAIR ? 2 : 1) * BM;
+                const int64_t top1 = static_cast<int64_t>(p.n_pb) * (PAIR ? 2 : 1) * BM;
+                int64_t acc = 0, best_d = INT64_MAX;
+                int best = 1;
+                for (int b = 0; b + 1 < a.nblk; ++b) {
+                    acc += unit_tiles(a.seg, a.nblk, top0, top1, b);
+                    const int64_t d = acc * 2 - wmax < 0 ? wmax - acc * 2 : acc * 2 - wmax;
+                    if (d < best_d) {
+                        best_d = d;
+                        best = b + 1;
+                    }
+                }
+                p.split_blk = best;
+                const int64_t need = 4ll * hb * n;
+                if (dst->split_next + need > kSplitRing) dst->split_next = 0;
+                p.split_cnt = dst->split + dst->split_next;
+                dst->split_next += need;
+            }
+        }
     }
-    const int64_t units = static_cast<int64_t>(p.n_pb) * a.Hq + (p.split ? static_cast<int64_t>(hi) * a.Hq : 0);
+    const int64_t units = static_cast<int64_t>(p.n_pb) * a.Hq + static_cast<int64_t>(p.split) * (a.Hq - p.heads_a);
     if (units == 0) return CDSP_OK;
     CDSP_REQUIRE(units < (1ll << 30), CDSP_ERR_SHAPE, "too many query tiles");
     p.n_units = static_cast<int>(units);
@@ -1624,6 +1728,13 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
     }
     cfg.attrs = at;
     cfg.numAttrs = na;
+#ifdef CDSP_KTRACE
+    if (getenv("CDSP_TRACE")) {  // debug builds: a clean per-unit record for this launch
+        void* gc = nullptr;
+        CDSP_CUDA(cudaGetSymbolAddress(&gc, g_cta));
+        CDSP_CUDA(cudaMemsetAsync(gc, 0, sizeof(unsigned long long) * 65536 * 8, st));
+    }
+#endif
     CDSP_CUDA(cudaLaunchKernelEx(&cfg, kern, tm, p));
 #ifdef CDSP_KTRACE
     if (const char* path = getenv("CDSP_TRACE")) {  // debug builds only: synchronous dump

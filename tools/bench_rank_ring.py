@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--kv-heads", type=int, default=None)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--per", type=int, default=4, help="back-to-back rank runs per timed sample")
     ap.add_argument("--sizes", default="1,2,4,8")
     ap.add_argument("--hist-per-rank", type=int, default=0)
     ap.add_argument("--modes", default="split,fused,stepwise")
@@ -91,13 +92,14 @@ def main():
                     run_rank(r, mode)
                 torch.cuda.synchronize()
                 ts = []
-                for _ in range(args.iters):
+                for _ in range(args.iters):  # `per` back-to-back rank runs per sample: host launch work overlaps
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
-                    run_rank(r, mode)
+                    for _ in range(args.per):
+                        run_rank(r, mode)
                     e1.record()
                     torch.cuda.synchronize()
-                    ts.append(e0.elapsed_time(e1))
+                    ts.append(e0.elapsed_time(e1) / args.per)
                 per_rank.append(sorted(ts)[len(ts) // 2])
             flops = 4.0 * D * H * (L * C + L * (L + 1) / 2)
             tmax = max(per_rank)

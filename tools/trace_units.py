@@ -35,6 +35,13 @@ def analyze(path, n_units):
     print(f"  SM tail idle median {np.median(tails) / 1e3:.1f} us, max {np.max(tails) / 1e3:.1f} us")
     b, a = np.polyfit(nu[ok], (loop_end - first_s)[ok], 1)
     print(f"  fit loop time: {a / 1e3:.2f} us + {b:.1f} ns per tile")
+    # where the span goes, averaged over SMs: tiles (loop), unit boundaries, epilogues, tail
+    n_sm = len(set(sm[ok].tolist()))
+    loop_t = (loop_end - first_s)[ok].sum() / n_sm / 1e3
+    tiles_per_sm = nu[ok].sum() / n_sm
+    print(f"  per SM: {tiles_per_sm:.0f} tiles, loop {loop_t:.1f} us ({loop_t * 1e3 / max(tiles_per_sm, 1):.0f} ns/tile),"
+          f" units {ok.sum() / n_sm:.1f}, boundary total {np.sum(gaps) / n_sm / 1e3:.1f} us,"
+          f" tail {np.mean(tails) / 1e3:.1f} us, span {span / 1e3:.1f} us")
     it = raw[65536 * 8:].reshape(4, 512, 16).astype(np.int64)
     d = it[0]
     n = int((d[:, 8] > 0).sum())
@@ -104,4 +111,4 @@ if __name__ == "__main__":
         torch.cuda.synchronize()
         del os.environ["CDSP_TRACE"]
         print(f"== s=8 fused ring launch, rank {r}{' (split units)' if split else ''}")
-        analyze(os.path.join(out_dir, f"trace_fused_r{r}.bin"), (2 * m // 128) * H * (2 if split else 1))
+        analyze(os.path.join(out_dir, f"trace_fused_r{r}.bin"), 65536)
