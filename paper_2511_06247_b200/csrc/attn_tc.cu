@@ -90,6 +90,15 @@
 #define CDSP_EPI_COALESCED 1
 #endif
 
+// Hand-over barriers (unit list / positions, row-sum slots): every lane arrives (1), so each
+// lane's own shared-memory accesses are ordered by its own arrive — the happens-before
+// compute-sanitizer's racecheck verifies — or lane 0 arrives after __syncwarp (0).
+#ifndef CDSP_ALL_LANE_ARRIVE
+#define CDSP_ALL_LANE_ARRIVE 1
+#endif
+#define ARRIVERS (CDSP_ALL_LANE_ARRIVE ? 32 : 1)
+#define ARRIVE_LANE (CDSP_ALL_LANE_ARRIVE || lane == 0)
+
 #ifndef CDSP_KV_POLICY  // L2 policy of the K / V tile loads: 0 evict_last, 1 evict_normal, 2 evict_first
 #define CDSP_KV_POLICY 0
 #endif
@@ -688,8 +697,8 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
     if (warp == W_K) {
         if (lane == 0) {
             for (int i = 0; i < 2; ++i) {
-                mbar_init(bar(L::B_UF + i), 1);
-                mbar_init(bar(L::B_UE + i), 4 * NG + 2);  // softmax warps, V producer, MMA warp
+                mbar_init(bar(L::B_UF + i), ARRIVERS);  // the scheduler warp (its list / position writes)
+                mbar_init(bar(L::B_UE + i), ARRIVERS * (4 * NG + 2));  // softmax warps, V producer, MMA warp
                 mbar_init(bar(L::B_CF + i), 1);
                 mbar_init(bar(L::B_CE + i), 1);
             }
@@ -709,8 +718,8 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             mbar_init(bar(L::B_OF), 1);
             mbar_init(bar(L::B_OE), 4 * CL);  // the finishing group's 4 warps (x CTAs of a pair)
             for (int i = 0; i < 2; ++i) {
-                mbar_init(bar(L::B_LF + i), 4 * (NG - 1));
-                mbar_init(bar(L::B_LE + i), 4);
+                mbar_init(bar(L::B_LF + i), ARRIVERS * 4 * (NG - 1));  // the handing-over groups' warps
+                mbar_init(bar(L::B_LE + i), ARRIVERS * 4);
             }
             fence_barrier_init();
             tma_prefetch_desc(&tm.q);
@@ -766,13 +775,12 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             }
             if (i >= 2) mbar_wait(bar(L::B_UE + ub), ((i - 2) >> 1) & 1);  // every consumer is done with unit i-2
             if (x >= p.n_units) {
-                if (lane == 0) {
-                    uinfo[ub].x = -1;
-                    mbar_arrive(bar(L::B_UF + ub));
-                    // no more units here: a programmatically dependent launch (the next ring step)
-                    // may start on the SMs this grid frees from now on
-                    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-                }
+                if (lane == 0) uinfo[ub].x = -1;
+                __syncwarp();
+                if (ARRIVE_LANE) mbar_arrive(bar(L::B_UF + ub));
+                // no more units here: a programmatically dependent launch (the next ring step)
+                // may start on the SMs this grid frees from now on
+                if (lane == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
                 break;
             }
             int head, part, ux, blo, bhi;
@@ -818,7 +826,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             if (lane == 0) uinfo[ub] = UnitInfo{x, cnt};
             __threadfence_block();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar(L::B_UF + ub));  // publish (release)
+            if (ARRIVE_LANE) mbar_arrive(bar(L::B_UF + ub));  // publish (release)
             if (cnt > 0) {
                 // Q buffer qb is free once the last S of the unit that used it (n_ne - QST) is done
                 const int qb = n_ne % L::QST;
@@ -936,7 +944,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 ++it;
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar(L::B_UE + ub));
+            if (ARRIVE_LANE) mbar_arrive(bar(L::B_UE + ub));
         }
     } else if (warp == W_MMA) {
         // ================= MMA issuer (warp-uniform loop, one lane issues; PAIR: the even CTA) =================
@@ -995,7 +1003,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             MMA_WAIT(bar(L::B_UF + ub), (i >> 1) & 1);  // unit published
             const UnitInfo u = uinfo[ub];
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar(L::B_UE + ub));
+            if (ARRIVE_LANE) mbar_arrive(bar(L::B_UE + ub));
             if (u.x < 0) break;
             const int N = u.n_used;
             if (N == 0 || !leader) continue;
@@ -1206,7 +1214,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 if (lane == 0 && quad == 0) KTRACE(4 * g + 3, gn);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar(L::B_UE + ub));  // done with the unit's schedule / positions
+            if (ARRIVE_LANE) mbar_arrive(bar(L::B_UE + ub));  // done with the unit's schedule / positions
 #ifdef CDSP_KTRACE
             if (r == 0 && g == 0) UNIT_STAMP(u.x * CL + crank, 6, gtime_ns());
 #endif
@@ -1236,7 +1244,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                     if (use >= 1) mbar_wait(bar(L::B_LE + pu), (use - 1) & 1);  // slot read by the unit 2 back
                     lsh[g * BM + r] = make_float2(m_used, lacc.x + lacc.y);
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(bar(L::B_LF + pu));
+                    if (ARRIVE_LANE) mbar_arrive(bar(L::B_LF + pu));
                     continue;
                 }
                 mbar_wait(bar(L::B_LF + pu), use & 1);
@@ -1250,7 +1258,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar(L::B_LE + pu));
+                if (ARRIVE_LANE) mbar_arrive(bar(L::B_LE + pu));
             } else if (g != E) {
                 continue;
             }
