@@ -28,14 +28,15 @@ def _models():
     return {int(s): (m["a"], m["b"], m["c"], m["d"]) for s, m in d.items()}
 
 
-@pytest.mark.parametrize("queue", [
-    [0.0] * 8,                                        # idle pool: one chunk at the best SP size
-    [0.0, 0.0, 0.4, 0.4, 0.9, 0.9, 1.6, 1.6],         # staggered queues (ms): CDSP splits the prompt
-    [0.0, 0.2, 0.2, 0.2, 2.0, 2.0, 2.0, 2.0],
+@pytest.mark.parametrize("L,queue", [
+    (32768, [0.0] * 8),                                    # idle pool: one chunk at the best SP size
+    (32768, [0.0, 0.0, 0.4, 0.4, 0.9, 0.9, 1.6, 1.6]),     # staggered queues (ms): CDSP splits the prompt
+    (32768, [0.0, 0.2, 0.2, 0.2, 2.0, 2.0, 2.0, 2.0]),
+    (131072, [0, 5, 10, 15, 20, 25, 30, 35]),              # 3 chunks, groups 1 -> 2 -> 4 (cache balancing)
 ])
-def test_b200_fitted_schedule_runs_end_to_end(queue):
+def test_b200_fitted_schedule_runs_end_to_end(L, queue):
     models = _models()
-    L, granule = 32768, 2 * 8 * 64
+    granule = 2 * 8 * 64
     plan_list, ttft = api.schedule_prefill(L, queue, 8, models, 0.05, granule)
     assert sum(c[0] for c in plan_list) == L and ttft > 0
     plan = api.Plan(plan_list)
