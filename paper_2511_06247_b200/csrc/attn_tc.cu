@@ -114,15 +114,43 @@ namespace {
 
 // two softmax groups of 4 warps (a third group, 15 warps, was measured: not faster, the
 // 128-register cap of 4 warps per sub-partition costs what the extra latency slack gains)
-constexpr int NG = 2;
-constexpr int kThreads = 32 * (4 * NG + 3);  // softmax groups + K producer + V producer + MMA
+// softmax groups (warpgroups taking tiles n mod NG).  3 (with setmaxnreg: 12 x 152 registers) was
+// measured slower: 1068 TF/s holding whole score rows (spills), 1264 / 1225 with 64-score halves
+#ifndef CDSP_NGROUPS
+#define CDSP_NGROUPS 2
+#endif
+constexpr int NG = CDSP_NGROUPS;
+// CDSP_EPI_WARPS=1 (measured, not the default): a dedicated epilogue warpgroup finishes every
+// unit (O drain, normalisation, output / accumulator writes), so both softmax groups run
+// straight into the next unit.  Same box, 32K s=1: 1331 / 1316 vs 1337 / 1304 TF/s — the unit
+// boundary is not what bounds the kernel (the softmax groups' per-tile stream is).  The
+// CTA is 4 whole warpgroups (setmaxnreg acts per warpgroup; the fourth has one idle warp) and
+// launches at 128 registers per thread, redistributed with setmaxnreg: softmax 168, epilogue
+// 112, producers / MMA / idle 64 (8 x 168 + 4 x 112 + 4 x 64 = 16 x 128: an .inc beyond the
+// CTA's pool would wait forever).  0: the group that computed a unit's last tile finishes it
+// (round 1).
+#ifndef CDSP_EPI_WARPS
+#define CDSP_EPI_WARPS 0
+#endif
+constexpr int NEPI = CDSP_EPI_WARPS ? 4 : 0;
+// register redistribution (setmaxnreg) whenever the CTA outgrows 11 warps at 168 registers:
+// softmax / epilogue / producers+MMA+idle; 16 warps launched at 128 registers each
+#define CDSP_REGSPLIT (CDSP_EPI_WARPS || CDSP_NGROUPS > 2)
+constexpr int kThreads = 32 * (4 * NG + NEPI + 3 + (CDSP_REGSPLIT ? 1 : 0));  // softmax, epilogue, K / V producers, MMA (+ idle)
+static_assert(!CDSP_REGSPLIT || kThreads == 512, "register split assumes 16 warps");
+static_assert(NG == 2 || (NG == 3 && !CDSP_EPI_WARPS), "NG = 3 runs without the epilogue group");
+#define CDSP_SOFTMAX_REGS (NG == 3 ? 152 : 168)
+#define CDSP_PRODUCER_REGS (NG == 3 ? 56 : 64)
 constexpr int BM = 128;                 // query rows per CTA (TMEM lanes)
 constexpr int BN = 128;                 // KV rows per tile
 constexpr int NSB = 3;                  // S/P buffers in TMEM
 constexpr int kBox = 128 * 128;         // TMA box: 128 rows x 64 bf16 (128-byte swizzle rows)
 constexpr int kSchedMax = 8192;         // KV tiles per launch (1M keys)
 constexpr int kMaxBlk = CDSP_MAX_SP;    // KV blocks one launch walks (a rank's whole ring)
-constexpr int W_K = 4 * NG, W_V = 4 * NG + 1, W_MMA = 4 * NG + 2;
+// roles are warpgroup-aligned (setmaxnreg acts per warpgroup): softmax 0..4NG-1, epilogue
+// 4NG..4NG+3 (TMEM quadrants 0..3), then K producer, V producer, MMA
+constexpr int W_EPI0 = 4 * NG;
+constexpr int W_K = 4 * NG + NEPI, W_V = W_K + 1, W_MMA = W_K + 2;
 
 // PAIR: 2-SM variant (HD = 128).  A CTA pair (cluster of 2) runs M = 256 MMAs (cta_group::2):
 // each CTA holds its own 128 query rows of Q and of S / P / O in its TMEM, and HALF of every
@@ -598,9 +626,9 @@ __device__ __forceinline__ void gate_wait(const TcParams& p, int b, int kvh) {
 // Role of a finishing group in a split unit's pair protocol (all BM threads of group g call it):
 // 1 = first (leave the partial in the accumulator rows), 0 = second (wait for the partner's
 // partial, re-zero the pair's counters).  Out of line: its registers stay out of the softmax.
-__device__ __noinline__ int split_role(int* scnt, volatile int* role, int g, int r) {
+__device__ __noinline__ int split_role(int* scnt, volatile int* role, int bar_id, int r) {
     if (r == 0) *role = atomicAdd(scnt, 1);
-    named_bar_sync(12 + g, BM);
+    named_bar_sync(bar_id, BM);
     const int first = *role == 0;
     if (!first) {
         if (r == 0) {  // the partner is past its own atomicAdd: it is writing its partial
@@ -615,14 +643,14 @@ __device__ __noinline__ int split_role(int* scnt, volatile int* role, int g, int
             scnt[0] = 0;  // both parties are done with the pair: zero for the next launch
             scnt[1] = 0;
         }
-        named_bar_sync(12 + g, BM);
+        named_bar_sync(bar_id, BM);
         __threadfence();
     }
     return first;
 }
 
 template <int HD, bool PAIR>
-__global__ void __maxnreg__(CDSP_MAXNREG)
+__global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
     attn_tc_kernel(const __grid_constant__ TcMaps tm, const __grid_constant__ TcParams p) {
     using L = Layout<HD, PAIR>;
     extern __shared__ uint8_t smem_raw[];
@@ -698,7 +726,7 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
         if (lane == 0) {
             for (int i = 0; i < 2; ++i) {
                 mbar_init(bar(L::B_UF + i), ARRIVERS);  // the scheduler warp (its list / position writes)
-                mbar_init(bar(L::B_UE + i), ARRIVERS * (4 * NG + 2));  // softmax warps, V producer, MMA warp
+                mbar_init(bar(L::B_UE + i), ARRIVERS * (4 * NG + NEPI + 2));  // softmax, epilogue, V producer, MMA warps
                 mbar_init(bar(L::B_CF + i), 1);
                 mbar_init(bar(L::B_CE + i), 1);
             }
@@ -718,7 +746,9 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             mbar_init(bar(L::B_OF), 1);
             mbar_init(bar(L::B_OE), 4 * CL);  // the finishing group's 4 warps (x CTAs of a pair)
             for (int i = 0; i < 2; ++i) {
-                mbar_init(bar(L::B_LF + i), ARRIVERS * 4 * (NG - 1));  // the handing-over groups' warps
+                // row statistics hand-over: every softmax group to the epilogue group (CDSP_EPI_WARPS),
+                // else the other groups to the finishing one
+                mbar_init(bar(L::B_LF + i), ARRIVERS * 4 * (CDSP_EPI_WARPS ? NG : NG - 1));
                 mbar_init(bar(L::B_LE + i), ARRIVERS * 4);
             }
             fence_barrier_init();
@@ -750,6 +780,9 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+#if CDSP_REGSPLIT
+    if (warp >= W_K) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CDSP_PRODUCER_REGS) : "memory");  // producers, MMA issuer
+#endif
     if (warp == W_K) {
         // ======== unit scheduler + TMA producer of Q and K: for each unit, list its used KV
         // tiles in order (empty ones skipped), publish the unit (u_full[i&1]) and stream its
@@ -1037,6 +1070,9 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
         }
     } else if (warp < 4 * NG) {
         // ========= softmax group g (tiles gn = g, g+2, ... over all units): thread = one query row =========
+#if CDSP_REGSPLIT
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CDSP_SOFTMAX_REGS) : "memory");
+#endif
         const int g = warp >> 2;
         const int quad = warp & 3;  // TMEM lane quadrant
         const int r = quad * 32 + lane;
@@ -1215,6 +1251,233 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             }
             __syncwarp();
             if (ARRIVE_LANE) mbar_arrive(bar(L::B_UE + ub));  // done with the unit's schedule / positions
+#if CDSP_EPI_WARPS
+            // hand this group's row statistics to the epilogue group: (the max the row sum is
+            // relative to, the row sum); the group of the unit's last tile holds the final max
+            if (N > 0) {
+                const int pu = n_units_done & 1, use = n_units_done >> 1;
+                float2* lsh = reinterpret_cast<float2*>(smem + L::OFF_L) + pu * NG * BM;
+                if (use >= 1) mbar_wait(bar(L::B_LE + pu), (use - 1) & 1);  // slot read by the unit 2 back
+                lsh[g * BM + r] = make_float2(m_used, lacc.x + lacc.y);
+                __syncwarp();
+                if (ARRIVE_LANE) mbar_arrive(bar(L::B_LF + pu));
+                gn0 += N;
+                ++n_units_done;
+            }
+        }
+    } else if (CDSP_EPI_WARPS && warp < W_EPI0 + NEPI) {
+        // ========= epilogue group: finishes every unit in order (one thread = one query row) =========
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 112;" ::: "memory");
+        const int quad = warp & 3;  // TMEM lane quadrant
+        const int r = quad * 32 + lane;
+        const int g = 0;  // (named barriers / role slot of the epilogue group)
+        const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+        const uint32_t tO = tmem + lane_off + COL_O;
+        const int64_t nq = sg.nq;
+        const bool l_merge = p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST;
+        const bool l_to_acc = p.mode == CDSP_ATTN_FIRST || p.mode == CDSP_ATTN_MID;
+        volatile int* role_sh = reinterpret_cast<volatile int*>(smem + L::OFF_ROLE);
+        const int stage_bar = 8 + NG;
+        const unsigned stage_lead = static_cast<unsigned>(W_EPI0 * 32);
+        auto arrive_leader = [&](int b) {
+            if constexpr (PAIR) mbar_arrive_remote(lbar(b));
+            else mbar_arrive(bar(b));
+        };
+        int gn0 = 0, n_units_done = 0;
+        for (int i = 0;; ++i) {
+            const int ub = i & 1;
+            mbar_wait(bar(L::B_UF + ub), (i >> 1) & 1);
+            const UnitInfo u = uinfo[ub];
+            __syncwarp();
+            if (ARRIVE_LANE) mbar_arrive(bar(L::B_UE + ub));  // only the unit id and tile count are needed
+            if (u.x < 0) break;
+            const int N = u.n_used;
+            int head, part, ux, b0_unused, b1_unused;
+            int64_t row0;
+            unit_map(u.x, crank, head, row0, part, ux, b0_unused, b1_unused);
+            const int64_t row = row0 + r;
+            const bool row_ok = row < nq;
+            const int E = N > 0 ? (gn0 + N - 1) % NG : 0;
+            float l = 0.f, m = -INFINITY;
+            if (N > 0) {  // combine the groups' row sums relative to the final max (the last tile's group)
+                const int pu = n_units_done & 1, use = n_units_done >> 1;
+                const float2* lsh = reinterpret_cast<const float2*>(smem + L::OFF_L) + pu * NG * BM;
+                mbar_wait(bar(L::B_LF + pu), use & 1);
+                m = lsh[E * BM + r].x;
+                if (m != -INFINITY) {  // (m = -inf: no visible key; the FMA-pipe exp2 floors at 2^-126)
+#pragma unroll
+                    for (int gg = 0; gg < NG; ++gg) {
+                        const float2 ml = lsh[gg * BM + r];
+                        if (ml.y > 0.f) l += gg == E ? ml.y : ml.y * ex2(ml.x - m);
+                    }
+                }
+                __syncwarp();
+                if (ARRIVE_LANE) mbar_arrive(bar(L::B_LE + pu));
+                gn0 += N;
+                ++n_units_done;
+            }
+            if (N == 0 && p.mode == CDSP_ATTN_MID && part < 0) continue;  // merging an empty block is the identity
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            bool split_first = false;
+            int* scnt = nullptr;
+            if (part >= 0) {
+                scnt = p.split_cnt + 2 * (2 * ux + crank);
+                split_first = split_role(scnt, role_sh, 12, r) != 0;
+            }
+            // the staging boxes: the previous unit's TMA store has read them
+            if (threadIdx.x == stage_lead) bulk_wait_read0();
+            named_bar_sync(stage_bar, BM);
+            auto epilogue = [&](auto MG, auto TA) {  // 0 / 1: fixed; 2: the launch's mode
+                const bool merge = decltype(MG)::value == 2 ? l_merge : decltype(MG)::value == 1;
+                const bool to_acc = decltype(TA)::value == 2 ? l_to_acc : decltype(TA)::value == 1;
+                const float lse_a = merge && row_ok ? p.lse_acc[static_cast<size_t>(head) * nq + row] : -INFINITY;
+                const float inv_l = l > 0.f ? 1.0f / l : 0.f;
+                const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+                float wa = 0.f, wb = 1.f, lse_out = lse_b;
+                if (merge) merge_weights(lse_a, lse_b, wa, wb, lse_out);
+                const float sbw = wb * inv_l;
+                // PAIR: bf16 rows go through two 128B-swizzled boxes (64 columns each) and TMA stores;
+                // fp32 accumulator rows through each warp's 4 KB slices of the same boxes (coalesced)
+                const bool boxed = PAIR && N > 0 && (CDSP_EPI_COALESCED || !to_acc);
+                const uint32_t stg0 = sbase + L::OFF_STG;
+                const int64_t wrow0 = row0 + 32 * quad;
+                const int nvalid = static_cast<int>(nq - wrow0 < 32 ? (nq - wrow0 > 0 ? nq - wrow0 : 0) : 32);
+                const size_t rstride = static_cast<size_t>(p.Hq) * HD;
+    #pragma unroll 1
+                for (int hh = 0; hh < HD / 64; ++hh) {  // O columns [64 hh, 64 hh + 64)
+                    uint32_t o[64];
+                    if (N > 0) {
+                        if (hh == 0) {
+                            mbar_wait(bar(L::B_OF), (n_units_done - 1) & 1);
+                            tc_fence_after();
+                        }
+                        tmem_ld32p(tO + 64 * hh, o);
+                        tmem_ld32p(tO + 64 * hh + 32, o + 32);
+                        tc_wait_ld();
+                        reg_tie32(o);
+                        reg_tie32(o + 32);
+                        if (hh == HD / 64 - 1) {  // O drained: TMEM back to the next unit's PV
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) arrive_leader(L::B_OE);
+                        }
+                    } else {
+    #pragma unroll
+                        for (int q = 0; q < 64; ++q) o[q] = 0u;
+                    }
+                    if (boxed && to_acc && CDSP_EPI_WIDE) {
+                        // fp32 accumulator, FIRST / MID: the finishing group alone uses the 32 KB of
+                        // boxes, so this warp's 8 KB (its rows of both boxes) carry a 64-column half
+                        // per round trip
+                        const uint32_t t0 = stg0 + static_cast<uint32_t>(quad) * (32 * 128);
+                        const uint32_t t1 = t0 + BM * 128;
+                        float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
+                        if (merge) {
+                            float a[64];
+                            warp_rows_load64(a, acc_w, rstride, nvalid, t0, t1, lane);
+    #pragma unroll
+                            for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(fmaf(wa, a[q], __uint_as_float(o[q]) * sbw));
+                        } else {
+    #pragma unroll
+                            for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * sbw);
+                        }
+                        warp_rows_store64(o, acc_w, rstride, nvalid, t0, t1, lane);
+                    } else if (boxed) {
+                        const uint32_t box = stg0 + static_cast<uint32_t>(hh) * (BM * 128);
+                        const uint32_t wtile = box + static_cast<uint32_t>(quad) * (32 * 128);
+                        float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
+    #pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            float a[32];
+                            if (merge) warp_rows_load(a, acc_w + 32 * c, rstride, nvalid, wtile, lane);
+    #pragma unroll
+                            for (int q = 0; q < 32; ++q) {
+                                float v = __uint_as_float(o[32 * c + q]) * sbw;
+                                if (merge) v = fmaf(wa, a[q], v);
+                                o[32 * c + q] = __float_as_uint(v);
+                            }
+                        }
+                        if (to_acc) {
+    #pragma unroll
+                            for (int c = 0; c < 2; ++c) warp_rows_store(o + 32 * c, acc_w + 32 * c, rstride, nvalid, wtile, lane);
+                        } else {
+                            const uint32_t rsw = static_cast<uint32_t>(r & 7), rowa = box + static_cast<uint32_t>(r) * 128;
+    #pragma unroll
+                            for (int q = 0; q < 8; ++q) {  // 16-byte chunk q of the 128-byte row
+                                const uint32_t* w = o + 8 * q;
+                                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rowa + ((static_cast<uint32_t>(q) ^ rsw) << 4)),
+                                             "r"(pack_bf16(__uint_as_float(w[0]), __uint_as_float(w[1]))),
+                                             "r"(pack_bf16(__uint_as_float(w[2]), __uint_as_float(w[3]))),
+                                             "r"(pack_bf16(__uint_as_float(w[4]), __uint_as_float(w[5]))),
+                                             "r"(pack_bf16(__uint_as_float(w[6]), __uint_as_float(w[7])))
+                                             : "memory");
+                            }
+                        }
+                    } else if (row_ok) {
+                        const size_t orow = (static_cast<size_t>(row) * p.Hq + head) * HD + 64 * hh;
+    #pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            float v[32];
+    #pragma unroll
+                            for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(o[32 * c + q]) * sbw;
+                            if (merge) {
+                                const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
+    #pragma unroll
+                                for (int q = 0; q < 8; ++q) {
+                                    const float4 av = a4[q];
+                                    v[4 * q + 0] = fmaf(wa, av.x, v[4 * q + 0]);
+                                    v[4 * q + 1] = fmaf(wa, av.y, v[4 * q + 1]);
+                                    v[4 * q + 2] = fmaf(wa, av.z, v[4 * q + 2]);
+                                    v[4 * q + 3] = fmaf(wa, av.w, v[4 * q + 3]);
+                                }
+                            }
+                            if (to_acc) {
+                                float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow + 32 * c);
+    #pragma unroll
+                                for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                            } else {
+                                uint4* d4 = reinterpret_cast<uint4*>(p.out + orow + 32 * c);
+    #pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    d4[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                                       pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+                            }
+                        }
+                    }
+                }
+                if (boxed && !to_acc) {
+                    fence_proxy_async_smem();
+                    named_bar_sync(stage_bar, BM);  // this group's 128 rows are in the boxes
+                    if (threadIdx.x == stage_lead) {
+                        for (int hh = 0; hh < HD / 64; ++hh)
+                            tma_store_3d(&tm.out, stg0 + static_cast<uint32_t>(hh) * (BM * 128), 64 * hh, head,
+                                         static_cast<int>(row0));  // rows >= nq clipped
+                        bulk_commit();
+                        // the boxes are free again once the engine has read them: at once when both
+                        // softmax groups share them, else before this group's next use (epilogue group)
+                        if (!CDSP_EPI_WARPS) bulk_wait_read0();
+                    }
+                }
+                if (row_ok) {
+                    const size_t li = static_cast<size_t>(head) * nq + row;
+                    if (to_acc) {
+                        p.lse_acc[li] = lse_out;
+                    } else if (p.lse) {
+                        p.lse[li] = lse_out;
+                    }
+                }
+            };
+            if (part < 0) epilogue(IntC<2>{}, IntC<2>{});
+            else if (split_first) epilogue(IntC<0>{}, IntC<1>{});
+            else epilogue(IntC<1>{}, IntC<0>{});
+            if (split_first) {  // publish the partial (every thread's stores, then one release)
+                __threadfence();
+                named_bar_sync(12, BM);
+                if (r == 0) asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(scnt + 1), "r"(1) : "memory");
+            }
+        }
+    }
+#else
 #ifdef CDSP_KTRACE
             if (r == 0 && g == 0) UNIT_STAMP(u.x * CL + crank, 6, gtime_ns());
 #endif
@@ -1273,9 +1536,11 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
             // softmax hundreds of bytes of register spills.
             bool split_first = false;
             int* scnt = nullptr;
+            const int stage_bar = 8 + g;
+            const unsigned stage_lead = static_cast<unsigned>(g * BM);
             if (part >= 0) {
                 scnt = p.split_cnt + 2 * (2 * ux + crank);
-                split_first = split_role(scnt, role_sh + g, g, r) != 0;
+                split_first = split_role(scnt, role_sh + g, 12 + g, r) != 0;
             }
             auto epilogue = [&](auto MG, auto TA) {  // 0 / 1: fixed; 2: the launch's mode
                 const bool merge = decltype(MG)::value == 2 ? l_merge : decltype(MG)::value == 1;
@@ -1397,13 +1662,15 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
                 }
                 if (boxed && !to_acc) {
                     fence_proxy_async_smem();
-                    named_bar_sync(8 + g, BM);  // this group's 128 rows are in the boxes
-                    if (threadIdx.x == static_cast<unsigned>(g * BM)) {
+                    named_bar_sync(stage_bar, BM);  // this group's 128 rows are in the boxes
+                    if (threadIdx.x == stage_lead) {
                         for (int hh = 0; hh < HD / 64; ++hh)
                             tma_store_3d(&tm.out, stg0 + static_cast<uint32_t>(hh) * (BM * 128), 64 * hh, head,
                                          static_cast<int>(row0));  // rows >= nq clipped
                         bulk_commit();
-                        bulk_wait_read0();  // the boxes are free again (the next unit may finish in another group)
+                        // the boxes are free again once the engine has read them: at once when both
+                        // softmax groups share them, else before this group's next use (epilogue group)
+                        if (!CDSP_EPI_WARPS) bulk_wait_read0();
                     }
                 }
                 if (row_ok) {
@@ -1437,9 +1704,11 @@ __global__ void __maxnreg__(CDSP_MAXNREG)
 #endif
         }
     }
+#endif
 
     // ---- teardown
-    if (PAIR && warp < 4 * NG && (threadIdx.x % BM) == 0) bulk_wait_all0();  // staged output stores done
+    if (PAIR && (CDSP_EPI_WARPS ? threadIdx.x == W_EPI0 * 32 : (warp < 4 * NG && (threadIdx.x % BM) == 0)))
+        bulk_wait_all0();  // staged output stores done
     tc_fence_before();
     if constexpr (PAIR) cluster_sync_all();  // no remote arrive / DSMEM access into a CTA that exits
     else __syncthreads();
