@@ -361,23 +361,38 @@ struct RingLaunches {
     int first[kMaxWorld + 1] = {};  // launch i covers blocks [first[i], first[i + 1])
     bool fused = false;
 };
-cdsp_status ring_launches(cdsp_comm c, const ChunkInfo& ci, int r, RingLaunches* out) {
+// A launch's units each walk all of its blocks, and the units in flight (head-major) are at
+// different points of that walk: the K / V of one KV head over all the launch's blocks is the
+// L2 working set.  Blocks are grouped so that it stays within this budget (the whole ring in one
+// launch for the 32K-token chunk at s = 8: 16.8 MB; one launch per block for a 512K chunk).
+int64_t ring_l2_budget() {
+    static const int64_t mb = getenv("CDSP_RING_L2_MB") ? atoll(getenv("CDSP_RING_L2_MB")) : 32;
+    return mb << 20;
+}
+cdsp_status ring_launches(cdsp_comm c, const ChunkInfo& ci, int r, RingLaunches* out, int Hq) {
     const bool fused = c->dtype == CDSP_BF16 && !(c->ring_opts & CDSP_RING_STEPWISE);
+    // the L2 grouping needs the merge accumulators; without them the whole ring is one launch
+    const bool acc_ok = c->acc_rows >= 2 * ci.m && c->acc_hq >= Hq;
     const int max_t = c->dtype == CDSP_BF16 ? attention_tc_max_tiles(c->D) : 0;
+    const int64_t head_bytes_per_row = 2ll * c->D * static_cast<int64_t>(c->esize);  // K + V of one KV head
     out->n = 0;
     out->fused = fused;
-    int64_t acc = 0;
+    int64_t acc = 0, acc_bytes = 0;
     for (int k = 0; k < ci.s; ++k) {
         const int src = (r - k + ci.s) % ci.s;
-        const int64_t t = (ci.hist[src] + 2 * ci.m + 127) / 128;
+        const int64_t rows = ci.hist[src] + 2 * ci.m;
+        const int64_t t = (rows + 127) / 128;
         CDSP_REQUIRE(c->dtype != CDSP_BF16 || t <= max_t, CDSP_ERR_CAPACITY,
                      "ring block of %lld tiles exceeds the %d KV tiles of one launch", static_cast<long long>(t),
                      max_t);
-        if (k == 0 || !fused || acc + t > max_t) {
+        const int64_t bytes = rows * head_bytes_per_row;
+        if (k == 0 || !fused || acc + t > max_t || (acc_ok && acc_bytes + bytes > ring_l2_budget())) {
             out->first[out->n++] = k;
             acc = 0;
+            acc_bytes = 0;
         }
         acc += t;
+        acc_bytes += bytes;
     }
     out->first[out->n] = ci.s;
     return CDSP_OK;
@@ -399,7 +414,7 @@ cdsp_status phase_ring(cdsp_comm c, const ChunkInfo& ci, int r, int layer, const
     const int64_t m2 = 2 * ci.m;
     const int s = ci.s;
     RingLaunches rl;
-    CDSP_CHECK_STATUS(ring_launches(c, ci, r, &rl));
+    CDSP_CHECK_STATUS(ring_launches(c, ci, r, &rl, Hq));
     const bool control = (c->ring_opts & CDSP_RING_CONTROL) != 0;
     bool remote_all = true;
     for (int k = 1; k < s; ++k)
@@ -998,7 +1013,7 @@ cdsp_status cdsp_prefill_chunk_layer(const cdsp_tensor* q, const cdsp_tensor* k,
     const int Hq = static_cast<int>(q->H);
     if (ci.s > 1) {  // the ring's launch structure; several launches merge through the reserved accumulators
         RingLaunches rl;
-        CDSP_CHECK_STATUS(ring_launches(c, ci, r, &rl));
+        CDSP_CHECK_STATUS(ring_launches(c, ci, r, &rl, Hq));
         CDSP_REQUIRE(rl.n == 1 || (c->acc_rows >= m2 && c->acc_hq >= Hq), CDSP_ERR_CAPACITY,
                      "this ring runs as %d launches merged in fp32 accumulators: reserve %lld rows x %d heads with "
                      "cdsp_comm_reserve (reserved %lld x %d)",

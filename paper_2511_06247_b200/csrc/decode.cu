@@ -452,8 +452,14 @@ __global__ void __launch_bounds__(kThreads) decode_attn_kernel(const DecodeParam
 // (the A operand of O += P V, V via ldmatrix.trans).  ~200 instructions per 16 tokens.  This is
 // an HBM stream: one query row per head gives no M to fill a tcgen05 tile, so the legacy
 // warp-level MMA is the right tool (its rate is far above the ~360 FLOP/clk/SM needed).
-constexpr int kMmaWarps = 4;
-constexpr int kStages = 3;
+#ifndef CDSP_DEC_WARPS  // warps per CTA of the bf16 decode kernel (each streams its own token steps)
+#define CDSP_DEC_WARPS 4
+#endif
+#ifndef CDSP_DEC_STAGES  // cp.async ring depth per warp (16-token K + V steps)
+#define CDSP_DEC_STAGES 3
+#endif
+constexpr int kMmaWarps = CDSP_DEC_WARPS;
+constexpr int kStages = CDSP_DEC_STAGES;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(pred ? 16 : 0)

@@ -175,6 +175,19 @@ def test_ring_split_into_several_launches(monkeypatch):
         c.close()
 
 
+def test_ring_grouped_by_l2_budget(monkeypatch):
+    """With accumulators reserved, the ring's blocks are grouped into launches whose per-KV-head
+    K / V fits the L2 budget (forced to 1 MB here: one launch per block, merged in fp32)."""
+    monkeypatch.setenv("CDSP_RING_L2_MB", "1")
+    import subprocess, sys  # the budget is read once per process: run the check in a fresh one
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_fused as t; "
+            "t._loopback([(2048, [0, 1]), (6144, list(range(8)))], 8192, 4, 2, 128, t.torch.bfloat16)")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                         env=dict(os.environ, CDSP_RING_L2_MB="1"))
+    assert out.returncode == 0, out.stderr[-3000:]
+
+
 def test_multi_launch_ring_needs_reserved_accumulators():
     plan = api.Plan([(512, [0, 1])])
     comms = make_loopback_comms(plan, 2, 64, torch.float32)  # no Hq: nothing reserved

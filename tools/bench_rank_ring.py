@@ -33,7 +33,7 @@ def main():
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--kv-heads", type=int, default=None)
     ap.add_argument("--iters", type=int, default=10)
-    ap.add_argument("--per", type=int, default=4, help="back-to-back rank runs per timed sample")
+    ap.add_argument("--per", type=int, default=1, help="back-to-back rank runs per timed sample")
     ap.add_argument("--sizes", default="1,2,4,8")
     ap.add_argument("--hist-per-rank", type=int, default=0)
     ap.add_argument("--modes", default="split,fused,stepwise")
@@ -92,8 +92,9 @@ def main():
                     run_rank(r, mode)
                 torch.cuda.synchronize()
                 ts = []
-                for _ in range(args.iters):  # `per` back-to-back rank runs per sample: host launch work overlaps
+                for _ in range(args.iters):  # `per` back-to-back rank runs per sample
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    torch.cuda._sleep(3_000_000)  # GPU busy while the host marshals and enqueues: device time only
                     e0.record()
                     for _ in range(args.per):
                         run_rank(r, mode)

@@ -37,6 +37,7 @@ def timed(fn, iters):
     ts = []
     for _ in range(iters):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(3_000_000)  # GPU busy while the host enqueues: the events bracket device time
         e0.record()
         fn()
         e1.record()
@@ -64,6 +65,7 @@ def t_s1(C, L, iters, dev):
         history()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(3_000_000)
         e0.record()
         api.prefill_chunk(qc, kc, vc, comm.kvstore(), api.SpGroup(comm, plan, c_idx), 0.0, out)
         e1.record()
