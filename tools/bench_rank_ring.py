@@ -106,6 +106,7 @@ def main():
             tmax = max(per_rank)
             res[f"s{s}_{mode if s > 1 else 'single'}"] = {
                 "rank_ms_max": tmax, "rank_ms_min": min(per_rank), "ranks_timed": len(per_rank),
+                "rank_ms": [round(x, 4) for x in per_rank],
                 "tflops_per_gpu": flops / s / (tmax * 1e-3) / 1e12}
     print(json.dumps({"metric": "per-GPU ring attention TFLOP/s at SP=s (one rank's launches, peer blocks resident)",
                       "seq": L, "heads": H, "kv_heads": Hkv, "head_dim": D, "hist_per_rank": h, "results": res}))
