@@ -1914,8 +1914,14 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
             W += w[pb];
         }
         const int64_t wmax = w[p.n_pb - 1];
-        if (light_env)  // light units: under 1/8 of the heaviest (they go last and fill the tail)
-            while (p.n_light < p.n_pb - 1 && w[p.n_light] * 8 < wmax) ++p.n_light;
+        // light units (they go last and fill the tail): under 1/4 of the heaviest on a ring launch
+        // (its lower row blocks see few blocks: KTRACE s=8 rank 2 tail 134 -> 26 us), under 1/8
+        // for one causal block (smaller tail pieces: s=1 tail 22 vs 45 us)
+        const int light_div = a.nblk > 1 ? 4 : 8;
+        if (light_env)
+            while (p.n_light < p.n_pb - 1 && w[p.n_light] * light_div < wmax) ++p.n_light;
+        int64_t w_light = 0, w_heavy = 0;  // per head
+        for (int pb = 0; pb < p.n_pb; ++pb) (pb < p.n_light ? w_light : w_heavy) += w[pb];
         // split (ONLY-mode multi-block launches with scratch): units heavier than a sixth of a CTA
         // group's share, in the heads of the last ~1.5 waves, at the block boundary that halves
         // the heaviest unit
@@ -1924,8 +1930,10 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
         if (split_env && a.split_ok && a.nblk >= 2 && a.mode == CDSP_ATTN_ONLY && a.o_acc && a.lse_acc)
             while (n < p.n_pb - p.n_light && w[p.n_pb - 1 - n] * 6.0 > share && w[p.n_pb - 1 - n] >= 32) ++n;
         if (n > 0) {
-            const int per_head = p.n_pb - p.n_light + n;
-            int hb = static_cast<int>((3 * max_groups / 2 + per_head - 1) / per_head);
+            // region B + C (pieces no larger than half the heaviest unit) carries at least 1.5
+            // heaviest units of work per CTA group: whatever region A's units leave uneven
+            const double need = 1.5 * max_groups * static_cast<double>(wmax) - static_cast<double>(w_light) * a.Hq;
+            int hb = need <= 0.0 ? 1 : static_cast<int>(need / static_cast<double>(w_heavy > 0 ? w_heavy : 1)) + 1;
             if (split_env >= 2) hb = a.Hq;  // CDSP_SPLIT=2: split in every head (measurement)
             if (hb > a.Hq) hb = a.Hq;
             if (static_cast<int64_t>(hb) * n <= kSplitUnits) {

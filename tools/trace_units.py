@@ -98,7 +98,9 @@ if __name__ == "__main__":
     sh = [(api.zigzag_gather(q, s, x), api.zigzag_gather(k, s, x), api.zigzag_gather(v, s, x)) for x in range(s)]
     acc = torch.empty(2 * m, H, D, dtype=torch.float32, device="cuda")
     lacc = torch.empty(H, 2 * m, dtype=torch.float32, device="cuda")
-    for r, split in ((0, False), (0, True), (7, False), (7, True)):
+    ranks_env = os.environ.get("TRACE_RANKS")
+    combos = [(int(x), True) for x in ranks_env.split(",")] if ranks_env else [(0, False), (0, True), (7, False), (7, True)]
+    for r, split in combos:
         srcs = [(r - st) % s for st in range(s)]
         segs = [api.segments(2 * m, m, r * m, (2 * s - 1 - r) * m, 2 * m, 0, m, x * m, (2 * s - 1 - x) * m) for x in srcs]
         outr = torch.empty_like(sh[r][0])
