@@ -721,6 +721,162 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
         unit_map(x, c, head, row0, part, ux, b0, b1);
     };
 
+    // ---- unit epilogue (one group's finish of a unit): normalise O, then write the bf16 output
+    // or the fp32 accumulator / LSE-merge with it (R3).  Instantiated per role (MG: merge with
+    // the accumulator, TA: write to it; 0 / 1 fixed, 2 the launch's mode).  Columns [64 hh0,
+    // 64 hh1) of O; wide_ok: 64-column accumulator round trips through this group's 8 KB per
+    // warp of staging; write_lse: this group writes the row's LSE.
+    const int64_t nq = sg.nq;
+    const bool l_merge = p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST;
+    const bool l_to_acc = p.mode == CDSP_ATTN_FIRST || p.mode == CDSP_ATTN_MID;
+    auto arrive_leader = [&](int b) {  // lane 0, after the warp's tcgen05 ops are fenced
+        if constexpr (PAIR) mbar_arrive_remote(lbar(b));
+        else mbar_arrive(bar(b));
+    };
+    auto run_epilogue = [&](auto MG, auto TA, const int head, const int64_t row0, const int64_t row, const bool row_ok,
+                            const int r, const int quad, const int N, const float l, const float m,
+                            const int n_units_done, const uint32_t tO, const int stage_bar, const unsigned stage_lead,
+                            const int hh0, const int hh1, const bool wide_ok, const bool write_lse) {
+        const bool merge = decltype(MG)::value == 2 ? l_merge : decltype(MG)::value == 1;
+        const bool to_acc = decltype(TA)::value == 2 ? l_to_acc : decltype(TA)::value == 1;
+        const float lse_a = merge && row_ok ? p.lse_acc[static_cast<size_t>(head) * nq + row] : -INFINITY;
+        const float inv_l = l > 0.f ? 1.0f / l : 0.f;
+        const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+        float wa = 0.f, wb = 1.f, lse_out = lse_b;
+        if (merge) merge_weights(lse_a, lse_b, wa, wb, lse_out);
+        const float sbw = wb * inv_l;
+        // PAIR: bf16 rows go through two 128B-swizzled boxes (64 columns each) and TMA stores;
+        // fp32 accumulator rows through each warp's 4 KB slices of the same boxes (coalesced)
+        const bool boxed = PAIR && N > 0 && (CDSP_EPI_COALESCED || !to_acc);
+        const uint32_t stg0 = sbase + L::OFF_STG;
+        const int64_t wrow0 = row0 + 32 * quad;
+        const int nvalid = static_cast<int>(nq - wrow0 < 32 ? (nq - wrow0 > 0 ? nq - wrow0 : 0) : 32);
+        const size_t rstride = static_cast<size_t>(p.Hq) * HD;
+#pragma unroll 1
+        for (int hh = hh0; hh < hh1; ++hh) {  // O columns [64 hh, 64 hh + 64)
+            uint32_t o[64];
+            if (N > 0) {
+                if (hh == 0) {
+                    mbar_wait(bar(L::B_OF), (n_units_done - 1) & 1);
+                    tc_fence_after();
+                }
+                tmem_ld32p(tO + 64 * hh, o);
+                tmem_ld32p(tO + 64 * hh + 32, o + 32);
+                tc_wait_ld();
+                reg_tie32(o);
+                reg_tie32(o + 32);
+                if (hh == hh1 - 1) {  // O drained: TMEM back to the next unit's PV
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) arrive_leader(L::B_OE);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 64; ++q) o[q] = 0u;
+            }
+            if (boxed && to_acc && CDSP_EPI_WIDE && wide_ok) {
+                // fp32 accumulator, FIRST / MID: the finishing group alone uses the 32 KB of
+                // boxes, so this warp's 8 KB (its rows of both boxes) carry a 64-column half
+                // per round trip
+                const uint32_t t0 = stg0 + static_cast<uint32_t>(quad) * (32 * 128);
+                const uint32_t t1 = t0 + BM * 128;
+                float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
+                if (merge) {
+                    float a[64];
+                    warp_rows_load64(a, acc_w, rstride, nvalid, t0, t1, lane);
+#pragma unroll
+                    for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(fmaf(wa, a[q], __uint_as_float(o[q]) * sbw));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * sbw);
+                }
+                warp_rows_store64(o, acc_w, rstride, nvalid, t0, t1, lane);
+            } else if (boxed) {
+                const uint32_t box = stg0 + static_cast<uint32_t>(hh) * (BM * 128);
+                const uint32_t wtile = box + static_cast<uint32_t>(quad) * (32 * 128);
+                float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    float a[32];
+                    if (merge) warp_rows_load(a, acc_w + 32 * c, rstride, nvalid, wtile, lane);
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        float v = __uint_as_float(o[32 * c + q]) * sbw;
+                        if (merge) v = fmaf(wa, a[q], v);
+                        o[32 * c + q] = __float_as_uint(v);
+                    }
+                }
+                if (to_acc) {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) warp_rows_store(o + 32 * c, acc_w + 32 * c, rstride, nvalid, wtile, lane);
+                } else {
+                    const uint32_t rsw = static_cast<uint32_t>(r & 7), rowa = box + static_cast<uint32_t>(r) * 128;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {  // 16-byte chunk q of the 128-byte row
+                        const uint32_t* w = o + 8 * q;
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rowa + ((static_cast<uint32_t>(q) ^ rsw) << 4)),
+                                     "r"(pack_bf16(__uint_as_float(w[0]), __uint_as_float(w[1]))),
+                                     "r"(pack_bf16(__uint_as_float(w[2]), __uint_as_float(w[3]))),
+                                     "r"(pack_bf16(__uint_as_float(w[4]), __uint_as_float(w[5]))),
+                                     "r"(pack_bf16(__uint_as_float(w[6]), __uint_as_float(w[7])))
+                                     : "memory");
+                    }
+                }
+            } else if (row_ok) {
+                const size_t orow = (static_cast<size_t>(row) * p.Hq + head) * HD + 64 * hh;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    float v[32];
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(o[32 * c + q]) * sbw;
+                    if (merge) {
+                        const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 av = a4[q];
+                            v[4 * q + 0] = fmaf(wa, av.x, v[4 * q + 0]);
+                            v[4 * q + 1] = fmaf(wa, av.y, v[4 * q + 1]);
+                            v[4 * q + 2] = fmaf(wa, av.z, v[4 * q + 2]);
+                            v[4 * q + 3] = fmaf(wa, av.w, v[4 * q + 3]);
+                        }
+                    }
+                    if (to_acc) {
+                        float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow + 32 * c);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    } else {
+                        uint4* d4 = reinterpret_cast<uint4*>(p.out + orow + 32 * c);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            d4[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                               pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+                    }
+                }
+            }
+        }
+        if (boxed && !to_acc) {
+            fence_proxy_async_smem();
+            named_bar_sync(stage_bar, BM);  // this group's 128 rows are in the boxes
+            if (threadIdx.x == stage_lead) {
+                for (int hh = hh0; hh < hh1; ++hh)
+                    tma_store_3d(&tm.out, stg0 + static_cast<uint32_t>(hh) * (BM * 128), 64 * hh, head,
+                                 static_cast<int>(row0));  // rows >= nq clipped
+                bulk_commit();
+                // the boxes are free again once the engine has read them: at once when both
+                // softmax groups share them, else before this group's next use (epilogue group)
+                if (!CDSP_EPI_WARPS) bulk_wait_read0();
+            }
+        }
+        if (row_ok && write_lse) {
+            const size_t li = static_cast<size_t>(head) * nq + row;
+            if (to_acc) {
+                p.lse_acc[li] = lse_out;
+            } else if (p.lse) {
+                p.lse[li] = lse_out;
+            }
+        }
+    };
+
     // ---- setup (once per CTA)
     if (warp == W_K) {
         if (lane == 0) {
@@ -1080,14 +1236,7 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
         const uint32_t tO = tmem + lane_off + COL_O;
         float* msh = reinterpret_cast<float*>(smem + L::OFF_M);  // [2][BM]
         const float sl2 = p.scale_log2;
-        const int64_t nq = sg.nq;
-        const bool l_merge = p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST;
-        const bool l_to_acc = p.mode == CDSP_ATTN_FIRST || p.mode == CDSP_ATTN_MID;
         volatile int* role_sh = reinterpret_cast<volatile int*>(smem + L::OFF_ROLE);  // [NG]
-        auto arrive_leader = [&](int b) {  // lane 0, after the warp's tcgen05 ops are fenced
-            if constexpr (PAIR) mbar_arrive_remote(lbar(b));
-            else mbar_arrive(bar(b));
-        };
         int gn0 = 0, n_units_done = 0;
         for (int i = 0;; ++i) {
             const int ub = i & 1;
@@ -1273,16 +1422,9 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
         const int g = 0;  // (named barriers / role slot of the epilogue group)
         const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
         const uint32_t tO = tmem + lane_off + COL_O;
-        const int64_t nq = sg.nq;
-        const bool l_merge = p.mode == CDSP_ATTN_MID || p.mode == CDSP_ATTN_LAST;
-        const bool l_to_acc = p.mode == CDSP_ATTN_FIRST || p.mode == CDSP_ATTN_MID;
         volatile int* role_sh = reinterpret_cast<volatile int*>(smem + L::OFF_ROLE);
         const int stage_bar = 8 + NG;
         const unsigned stage_lead = static_cast<unsigned>(W_EPI0 * 32);
-        auto arrive_leader = [&](int b) {
-            if constexpr (PAIR) mbar_arrive_remote(lbar(b));
-            else mbar_arrive(bar(b));
-        };
         int gn0 = 0, n_units_done = 0;
         for (int i = 0;; ++i) {
             const int ub = i & 1;
@@ -1327,149 +1469,9 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
             // the staging boxes: the previous unit's TMA store has read them
             if (threadIdx.x == stage_lead) bulk_wait_read0();
             named_bar_sync(stage_bar, BM);
-            auto epilogue = [&](auto MG, auto TA) {  // 0 / 1: fixed; 2: the launch's mode
-                const bool merge = decltype(MG)::value == 2 ? l_merge : decltype(MG)::value == 1;
-                const bool to_acc = decltype(TA)::value == 2 ? l_to_acc : decltype(TA)::value == 1;
-                const float lse_a = merge && row_ok ? p.lse_acc[static_cast<size_t>(head) * nq + row] : -INFINITY;
-                const float inv_l = l > 0.f ? 1.0f / l : 0.f;
-                const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
-                float wa = 0.f, wb = 1.f, lse_out = lse_b;
-                if (merge) merge_weights(lse_a, lse_b, wa, wb, lse_out);
-                const float sbw = wb * inv_l;
-                // PAIR: bf16 rows go through two 128B-swizzled boxes (64 columns each) and TMA stores;
-                // fp32 accumulator rows through each warp's 4 KB slices of the same boxes (coalesced)
-                const bool boxed = PAIR && N > 0 && (CDSP_EPI_COALESCED || !to_acc);
-                const uint32_t stg0 = sbase + L::OFF_STG;
-                const int64_t wrow0 = row0 + 32 * quad;
-                const int nvalid = static_cast<int>(nq - wrow0 < 32 ? (nq - wrow0 > 0 ? nq - wrow0 : 0) : 32);
-                const size_t rstride = static_cast<size_t>(p.Hq) * HD;
-    #pragma unroll 1
-                for (int hh = 0; hh < HD / 64; ++hh) {  // O columns [64 hh, 64 hh + 64)
-                    uint32_t o[64];
-                    if (N > 0) {
-                        if (hh == 0) {
-                            mbar_wait(bar(L::B_OF), (n_units_done - 1) & 1);
-                            tc_fence_after();
-                        }
-                        tmem_ld32p(tO + 64 * hh, o);
-                        tmem_ld32p(tO + 64 * hh + 32, o + 32);
-                        tc_wait_ld();
-                        reg_tie32(o);
-                        reg_tie32(o + 32);
-                        if (hh == HD / 64 - 1) {  // O drained: TMEM back to the next unit's PV
-                            tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) arrive_leader(L::B_OE);
-                        }
-                    } else {
-    #pragma unroll
-                        for (int q = 0; q < 64; ++q) o[q] = 0u;
-                    }
-                    if (boxed && to_acc && CDSP_EPI_WIDE) {
-                        // fp32 accumulator, FIRST / MID: the finishing group alone uses the 32 KB of
-                        // boxes, so this warp's 8 KB (its rows of both boxes) carry a 64-column half
-                        // per round trip
-                        const uint32_t t0 = stg0 + static_cast<uint32_t>(quad) * (32 * 128);
-                        const uint32_t t1 = t0 + BM * 128;
-                        float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
-                        if (merge) {
-                            float a[64];
-                            warp_rows_load64(a, acc_w, rstride, nvalid, t0, t1, lane);
-    #pragma unroll
-                            for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(fmaf(wa, a[q], __uint_as_float(o[q]) * sbw));
-                        } else {
-    #pragma unroll
-                            for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * sbw);
-                        }
-                        warp_rows_store64(o, acc_w, rstride, nvalid, t0, t1, lane);
-                    } else if (boxed) {
-                        const uint32_t box = stg0 + static_cast<uint32_t>(hh) * (BM * 128);
-                        const uint32_t wtile = box + static_cast<uint32_t>(quad) * (32 * 128);
-                        float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
-    #pragma unroll
-                        for (int c = 0; c < 2; ++c) {
-                            float a[32];
-                            if (merge) warp_rows_load(a, acc_w + 32 * c, rstride, nvalid, wtile, lane);
-    #pragma unroll
-                            for (int q = 0; q < 32; ++q) {
-                                float v = __uint_as_float(o[32 * c + q]) * sbw;
-                                if (merge) v = fmaf(wa, a[q], v);
-                                o[32 * c + q] = __float_as_uint(v);
-                            }
-                        }
-                        if (to_acc) {
-    #pragma unroll
-                            for (int c = 0; c < 2; ++c) warp_rows_store(o + 32 * c, acc_w + 32 * c, rstride, nvalid, wtile, lane);
-                        } else {
-                            const uint32_t rsw = static_cast<uint32_t>(r & 7), rowa = box + static_cast<uint32_t>(r) * 128;
-    #pragma unroll
-                            for (int q = 0; q < 8; ++q) {  // 16-byte chunk q of the 128-byte row
-                                const uint32_t* w = o + 8 * q;
-                                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rowa + ((static_cast<uint32_t>(q) ^ rsw) << 4)),
-                                             "r"(pack_bf16(__uint_as_float(w[0]), __uint_as_float(w[1]))),
-                                             "r"(pack_bf16(__uint_as_float(w[2]), __uint_as_float(w[3]))),
-                                             "r"(pack_bf16(__uint_as_float(w[4]), __uint_as_float(w[5]))),
-                                             "r"(pack_bf16(__uint_as_float(w[6]), __uint_as_float(w[7])))
-                                             : "memory");
-                            }
-                        }
-                    } else if (row_ok) {
-                        const size_t orow = (static_cast<size_t>(row) * p.Hq + head) * HD + 64 * hh;
-    #pragma unroll
-                        for (int c = 0; c < 2; ++c) {
-                            float v[32];
-    #pragma unroll
-                            for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(o[32 * c + q]) * sbw;
-                            if (merge) {
-                                const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
-    #pragma unroll
-                                for (int q = 0; q < 8; ++q) {
-                                    const float4 av = a4[q];
-                                    v[4 * q + 0] = fmaf(wa, av.x, v[4 * q + 0]);
-                                    v[4 * q + 1] = fmaf(wa, av.y, v[4 * q + 1]);
-                                    v[4 * q + 2] = fmaf(wa, av.z, v[4 * q + 2]);
-                                    v[4 * q + 3] = fmaf(wa, av.w, v[4 * q + 3]);
-                                }
-                            }
-                            if (to_acc) {
-                                float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow + 32 * c);
-    #pragma unroll
-                                for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                            } else {
-                                uint4* d4 = reinterpret_cast<uint4*>(p.out + orow + 32 * c);
-    #pragma unroll
-                                for (int q = 0; q < 4; ++q)
-                                    d4[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                                                       pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
-                            }
-                        }
-                    }
-                }
-                if (boxed && !to_acc) {
-                    fence_proxy_async_smem();
-                    named_bar_sync(stage_bar, BM);  // this group's 128 rows are in the boxes
-                    if (threadIdx.x == stage_lead) {
-                        for (int hh = 0; hh < HD / 64; ++hh)
-                            tma_store_3d(&tm.out, stg0 + static_cast<uint32_t>(hh) * (BM * 128), 64 * hh, head,
-                                         static_cast<int>(row0));  // rows >= nq clipped
-                        bulk_commit();
-                        // the boxes are free again once the engine has read them: at once when both
-                        // softmax groups share them, else before this group's next use (epilogue group)
-                        if (!CDSP_EPI_WARPS) bulk_wait_read0();
-                    }
-                }
-                if (row_ok) {
-                    const size_t li = static_cast<size_t>(head) * nq + row;
-                    if (to_acc) {
-                        p.lse_acc[li] = lse_out;
-                    } else if (p.lse) {
-                        p.lse[li] = lse_out;
-                    }
-                }
-            };
-            if (part < 0) epilogue(IntC<2>{}, IntC<2>{});
-            else if (split_first) epilogue(IntC<0>{}, IntC<1>{});
-            else epilogue(IntC<1>{}, IntC<0>{});
+            if (part < 0) run_epilogue(IntC<2>{}, IntC<2>{}, head, row0, row, row_ok, r, quad, N, l, m, n_units_done, tO, stage_bar, stage_lead, 0, HD / 64, true, true);
+            else if (split_first) run_epilogue(IntC<0>{}, IntC<1>{}, head, row0, row, row_ok, r, quad, N, l, m, n_units_done, tO, stage_bar, stage_lead, 0, HD / 64, true, true);
+            else run_epilogue(IntC<1>{}, IntC<0>{}, head, row0, row, row_ok, r, quad, N, l, m, n_units_done, tO, stage_bar, stage_lead, 0, HD / 64, true, true);
             if (split_first) {  // publish the partial (every thread's stores, then one release)
                 __threadfence();
                 named_bar_sync(12, BM);
@@ -1542,149 +1544,9 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
                 scnt = p.split_cnt + 2 * (2 * ux + crank);
                 split_first = split_role(scnt, role_sh + g, 12 + g, r) != 0;
             }
-            auto epilogue = [&](auto MG, auto TA) {  // 0 / 1: fixed; 2: the launch's mode
-                const bool merge = decltype(MG)::value == 2 ? l_merge : decltype(MG)::value == 1;
-                const bool to_acc = decltype(TA)::value == 2 ? l_to_acc : decltype(TA)::value == 1;
-                const float lse_a = merge && row_ok ? p.lse_acc[static_cast<size_t>(head) * nq + row] : -INFINITY;
-                const float inv_l = l > 0.f ? 1.0f / l : 0.f;
-                const float lse_b = l > 0.f ? (m + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
-                float wa = 0.f, wb = 1.f, lse_out = lse_b;
-                if (merge) merge_weights(lse_a, lse_b, wa, wb, lse_out);
-                const float sbw = wb * inv_l;
-                // PAIR: bf16 rows go through two 128B-swizzled boxes (64 columns each) and TMA stores;
-                // fp32 accumulator rows through each warp's 4 KB slices of the same boxes (coalesced)
-                const bool boxed = PAIR && N > 0 && (CDSP_EPI_COALESCED || !to_acc);
-                const uint32_t stg0 = sbase + L::OFF_STG;
-                const int64_t wrow0 = row0 + 32 * quad;
-                const int nvalid = static_cast<int>(nq - wrow0 < 32 ? (nq - wrow0 > 0 ? nq - wrow0 : 0) : 32);
-                const size_t rstride = static_cast<size_t>(p.Hq) * HD;
-    #pragma unroll 1
-                for (int hh = 0; hh < HD / 64; ++hh) {  // O columns [64 hh, 64 hh + 64)
-                    uint32_t o[64];
-                    if (N > 0) {
-                        if (hh == 0) {
-                            mbar_wait(bar(L::B_OF), (n_units_done - 1) & 1);
-                            tc_fence_after();
-                        }
-                        tmem_ld32p(tO + 64 * hh, o);
-                        tmem_ld32p(tO + 64 * hh + 32, o + 32);
-                        tc_wait_ld();
-                        reg_tie32(o);
-                        reg_tie32(o + 32);
-                        if (hh == HD / 64 - 1) {  // O drained: TMEM back to the next unit's PV
-                            tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) arrive_leader(L::B_OE);
-                        }
-                    } else {
-    #pragma unroll
-                        for (int q = 0; q < 64; ++q) o[q] = 0u;
-                    }
-                    if (boxed && to_acc && CDSP_EPI_WIDE) {
-                        // fp32 accumulator, FIRST / MID: the finishing group alone uses the 32 KB of
-                        // boxes, so this warp's 8 KB (its rows of both boxes) carry a 64-column half
-                        // per round trip
-                        const uint32_t t0 = stg0 + static_cast<uint32_t>(quad) * (32 * 128);
-                        const uint32_t t1 = t0 + BM * 128;
-                        float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
-                        if (merge) {
-                            float a[64];
-                            warp_rows_load64(a, acc_w, rstride, nvalid, t0, t1, lane);
-    #pragma unroll
-                            for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(fmaf(wa, a[q], __uint_as_float(o[q]) * sbw));
-                        } else {
-    #pragma unroll
-                            for (int q = 0; q < 64; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * sbw);
-                        }
-                        warp_rows_store64(o, acc_w, rstride, nvalid, t0, t1, lane);
-                    } else if (boxed) {
-                        const uint32_t box = stg0 + static_cast<uint32_t>(hh) * (BM * 128);
-                        const uint32_t wtile = box + static_cast<uint32_t>(quad) * (32 * 128);
-                        float* acc_w = p.o_acc + (static_cast<size_t>(nvalid > 0 ? wrow0 : 0) * p.Hq + head) * HD + 64 * hh;
-    #pragma unroll
-                        for (int c = 0; c < 2; ++c) {
-                            float a[32];
-                            if (merge) warp_rows_load(a, acc_w + 32 * c, rstride, nvalid, wtile, lane);
-    #pragma unroll
-                            for (int q = 0; q < 32; ++q) {
-                                float v = __uint_as_float(o[32 * c + q]) * sbw;
-                                if (merge) v = fmaf(wa, a[q], v);
-                                o[32 * c + q] = __float_as_uint(v);
-                            }
-                        }
-                        if (to_acc) {
-    #pragma unroll
-                            for (int c = 0; c < 2; ++c) warp_rows_store(o + 32 * c, acc_w + 32 * c, rstride, nvalid, wtile, lane);
-                        } else {
-                            const uint32_t rsw = static_cast<uint32_t>(r & 7), rowa = box + static_cast<uint32_t>(r) * 128;
-    #pragma unroll
-                            for (int q = 0; q < 8; ++q) {  // 16-byte chunk q of the 128-byte row
-                                const uint32_t* w = o + 8 * q;
-                                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(rowa + ((static_cast<uint32_t>(q) ^ rsw) << 4)),
-                                             "r"(pack_bf16(__uint_as_float(w[0]), __uint_as_float(w[1]))),
-                                             "r"(pack_bf16(__uint_as_float(w[2]), __uint_as_float(w[3]))),
-                                             "r"(pack_bf16(__uint_as_float(w[4]), __uint_as_float(w[5]))),
-                                             "r"(pack_bf16(__uint_as_float(w[6]), __uint_as_float(w[7])))
-                                             : "memory");
-                            }
-                        }
-                    } else if (row_ok) {
-                        const size_t orow = (static_cast<size_t>(row) * p.Hq + head) * HD + 64 * hh;
-    #pragma unroll
-                        for (int c = 0; c < 2; ++c) {
-                            float v[32];
-    #pragma unroll
-                            for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(o[32 * c + q]) * sbw;
-                            if (merge) {
-                                const float4* a4 = reinterpret_cast<const float4*>(p.o_acc + orow + 32 * c);
-    #pragma unroll
-                                for (int q = 0; q < 8; ++q) {
-                                    const float4 av = a4[q];
-                                    v[4 * q + 0] = fmaf(wa, av.x, v[4 * q + 0]);
-                                    v[4 * q + 1] = fmaf(wa, av.y, v[4 * q + 1]);
-                                    v[4 * q + 2] = fmaf(wa, av.z, v[4 * q + 2]);
-                                    v[4 * q + 3] = fmaf(wa, av.w, v[4 * q + 3]);
-                                }
-                            }
-                            if (to_acc) {
-                                float4* d4 = reinterpret_cast<float4*>(p.o_acc + orow + 32 * c);
-    #pragma unroll
-                                for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                            } else {
-                                uint4* d4 = reinterpret_cast<uint4*>(p.out + orow + 32 * c);
-    #pragma unroll
-                                for (int q = 0; q < 4; ++q)
-                                    d4[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                                                       pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
-                            }
-                        }
-                    }
-                }
-                if (boxed && !to_acc) {
-                    fence_proxy_async_smem();
-                    named_bar_sync(stage_bar, BM);  // this group's 128 rows are in the boxes
-                    if (threadIdx.x == stage_lead) {
-                        for (int hh = 0; hh < HD / 64; ++hh)
-                            tma_store_3d(&tm.out, stg0 + static_cast<uint32_t>(hh) * (BM * 128), 64 * hh, head,
-                                         static_cast<int>(row0));  // rows >= nq clipped
-                        bulk_commit();
-                        // the boxes are free again once the engine has read them: at once when both
-                        // softmax groups share them, else before this group's next use (epilogue group)
-                        if (!CDSP_EPI_WARPS) bulk_wait_read0();
-                    }
-                }
-                if (row_ok) {
-                    const size_t li = static_cast<size_t>(head) * nq + row;
-                    if (to_acc) {
-                        p.lse_acc[li] = lse_out;
-                    } else if (p.lse) {
-                        p.lse[li] = lse_out;
-                    }
-                }
-            };
-            if (part < 0) epilogue(IntC<2>{}, IntC<2>{});
-            else if (split_first) epilogue(IntC<0>{}, IntC<1>{});
-            else epilogue(IntC<1>{}, IntC<0>{});
+            if (part < 0) run_epilogue(IntC<2>{}, IntC<2>{}, head, row0, row, row_ok, r, quad, N, l, m, n_units_done, tO, stage_bar, stage_lead, 0, HD / 64, true, true);
+            else if (split_first) run_epilogue(IntC<0>{}, IntC<1>{}, head, row0, row, row_ok, r, quad, N, l, m, n_units_done, tO, stage_bar, stage_lead, 0, HD / 64, true, true);
+            else run_epilogue(IntC<1>{}, IntC<0>{}, head, row0, row, row_ok, r, quad, N, l, m, n_units_done, tO, stage_bar, stage_lead, 0, HD / 64, true, true);
             if (split_first) {  // publish the partial (every thread's stores, then one release)
                 __threadfence();
                 named_bar_sync(12 + g, BM);
