@@ -2038,6 +2038,11 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
 
 }  // namespace
 
+// [rows, H, D] bf16 tensor map (128-byte swizzle, box box_rows x 1 head x 64 d) for other kernels
+cdsp_status make_tile_map(CUtensorMap* m, const void* base, int64_t rows, int H, int D, int box_rows) {
+    return make_map(m, base, rows, H, D, box_rows);
+}
+
 cdsp_status attention_device_init() {
     DevState* d = nullptr;
     return device_state(&d);

@@ -39,6 +39,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace cdsp {
 namespace {
@@ -52,6 +53,11 @@ __device__ __forceinline__ void dstamp(int slot) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g_dtrace[blockIdx.x * 8 + slot] = t;
+        if (slot == 0) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_dtrace[blockIdx.x * 8 + 7] = smid + 1;
+        }
     }
 }
 #else
@@ -60,7 +66,10 @@ __device__ __forceinline__ void dstamp(int) {}
 
 constexpr int kThreads = 256, kWarps = 8;
 constexpr int kNI = 8;          // 16-byte vectors per lane per step (log2 = 3)
-constexpr int kGroup = 16;      // splits merged by a level-1 merger
+#ifndef CDSP_DEC_MERGE  // 1: slice-parallel merge by the last finishers; 0: two-level group merge
+#define CDSP_DEC_MERGE 1
+#endif
+constexpr int kGroup = 16;      // splits merged by a level-1 merger (CDSP_DEC_MERGE = 0)
 constexpr int kMaxSplit = 512;  // splits per KV head
 constexpr int kMaxGroups = kMaxSplit / kGroup;
 
@@ -207,6 +216,99 @@ __device__ void merge_parts(const float* o_src, const float* l_src, int n, float
     }
 }
 
+// Split merge by the last finishers (CDSP_DEC_MERGE = 1).  Every split CTA has written its
+// partial (o normalised, lse in log2 units); the partials are merged column-slice-parallel:
+// slice sl = 8 consecutive elements of the [G][HD] output, merged over ALL n splits by one CTA
+// (w_j = 2^(lse_j - M) / sum_k 2^(lse_k - M), R3 in base 2).  The CTAs doing it are the LAST K
+// = min(G HD / 8, n) to finish (their finishing rank is an atomic count): each waits for the
+// count to reach n (the others are resident: the grid is one wave) and merges slices q, q + K,
+// ...  One L2 round trip for all of a slice's loads (n <= 512 partials: <= 4 lse and <= 8
+// float4 per thread), instead of a two-level chain of merges after the last split.
+template <typename T, int HD, int G>
+__device__ void merge_slice(const DecodeParams& p, int kvh, int sl) {
+    __shared__ float w_all[kMaxSplit];
+    __shared__ float red[32];
+    __shared__ float4 red4[32][2];
+    const int tid = threadIdx.x, nt = blockDim.x, n = p.n_split;
+    const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+    const int c0 = sl * 8, h = c0 / HD, half = tid & 1, hn = nt >> 1;
+    const float* l1 = p.l1 + static_cast<size_t>(kvh) * kMaxSplit * G + h;
+    const float* o1 = p.o1 + static_cast<size_t>(kvh) * kMaxSplit * G * HD + c0 + 4 * half;
+    float lv[4];
+    float4 ov[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int j = tid + i * nt;
+        lv[i] = j < n ? __ldcg(l1 + static_cast<size_t>(j) * G) : -INFINITY;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int j = (tid >> 1) + i * hn;
+        ov[i] = j < n ? __ldcg(reinterpret_cast<const float4*>(o1 + static_cast<size_t>(j) * G * HD))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float mx = fmaxf(fmaxf(lv[0], lv[1]), fmaxf(lv[2], lv[3]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (lane == 0) red[wid] = mx;
+    __syncthreads();
+    float M = -INFINITY;
+    for (int w = 0; w < nw; ++w) M = fmaxf(M, red[w]);
+    float den = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int j = tid + i * nt;
+        const float w = lv[i] == -INFINITY ? 0.f : ex2f(lv[i] - M);
+        if (j < n) w_all[j] = w;
+        den += w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xFFFFFFFFu, den, o);
+    __syncthreads();  // red[] read by all; w_all complete
+    if (lane == 0) red[wid] = den;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int j = (tid >> 1) + i * hn;
+        if (j < n) {
+            const float w = w_all[j];
+            acc.x = fmaf(w, ov[i].x, acc.x);
+            acc.y = fmaf(w, ov[i].y, acc.y);
+            acc.z = fmaf(w, ov[i].z, acc.z);
+            acc.w = fmaf(w, ov[i].w, acc.w);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 1; o >>= 1) {  // lanes of the same half
+        acc.x += __shfl_xor_sync(0xFFFFFFFFu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xFFFFFFFFu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xFFFFFFFFu, acc.z, o);
+        acc.w += __shfl_xor_sync(0xFFFFFFFFu, acc.w, o);
+    }
+    if (lane < 2) red4[wid][lane] = acc;
+    __syncthreads();
+    if (tid < 2) {
+        float D = 0.f;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int w = 0; w < nw; ++w) {
+            D += red[w];
+            a.x += red4[w][tid].x;
+            a.y += red4[w][tid].y;
+            a.z += red4[w][tid].z;
+            a.w += red4[w][tid].w;
+        }
+        const float inv = D > 0.f ? 1.f / D : 0.f;
+        T* out = static_cast<T*>(p.out) + static_cast<size_t>(kvh) * G * HD + c0 + 4 * tid;
+        Vec<T>::store(out, a.x * inv);
+        Vec<T>::store(out + 1, a.y * inv);
+        Vec<T>::store(out + 2, a.z * inv);
+        Vec<T>::store(out + 3, a.w * inv);
+        if (tid == 0 && c0 % HD == 0 && p.lse)
+            p.lse[kvh * G + h] = D > 0.f ? (M + __log2f(D)) * 0.69314718055994530942f : -INFINITY;
+    }
+    __syncthreads();  // shared scratch reused by the next slice
+}
+
 // Tail shared by both kernels: NS per-slot states (m, l in log2 units, unnormalised o) are in
 // shared memory; merge them (R3), then write the output (one split) or this split's partial
 // and run the in-kernel two-level split merge.
@@ -253,6 +355,36 @@ __device__ void finish_cta(const DecodeParams& p, const int NS, const float* sm_
     }
     dstamp(2);
     if (single) return;
+#if CDSP_DEC_MERGE
+    {
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) *s_last = atomicAdd(p.cnt2 + kvh, 1);
+        __syncthreads();
+        const int n = p.n_split, nsl = G * HD / 8;
+        const int K = min(nsl, n), r = *s_last;
+        if (r < n - K) return;
+        if (threadIdx.x == 0) {  // wait for every split's partial
+            const uint64_t t0 = ptx::globaltimer();
+            for (;;) {
+                int c;
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(c) : "l"(p.cnt2 + kvh) : "memory");
+                if (c >= n) break;
+                if (ptx::globaltimer() - t0 > 4000000000ull) __trap();
+                __nanosleep(32);
+            }
+        }
+        __syncthreads();
+        dstamp(4);
+        for (int sl = r - (n - K); sl < nsl; sl += K) merge_slice<T, HD, G>(p, kvh, sl);
+        if (threadIdx.x == 0 && atomicAdd(p.cnt1 + kvh * kMaxGroups, 1) == K - 1) {
+            p.cnt2[kvh] = 0;  // every merger has seen the full count: leave the workspace zeroed
+            p.cnt1[kvh * kMaxGroups] = 0;
+        }
+        dstamp(6);
+        return;
+    }
+#endif
 
     // ---- level 1: the last CTA of this group of kGroup splits merges them
     const int grp = split / kGroup;
@@ -669,6 +801,227 @@ __global__ void __launch_bounds__(kMmaWarps * 32) decode_mma_kernel(const Decode
     dstamp(3);
 }
 
+// ---------------------------------------------------------------------------------------
+// bf16, block size >= 16: TMA-fed decode.  One producer thread streams the CTA's token range
+// in 64-token stages (4 sub-tiles of 16 tokens = one page piece each: 128-byte-swizzled TMA
+// boxes of 16 rows x 64 d of K and of V, pages looked up in the block table; a sub-tile past
+// the range or on an out-of-range page is loaded from beyond the tensor, i.e. zero-filled)
+// into an NST-deep ring of mbarrier-tracked stages; consumer warp w computes sub-tile w of
+// every stage with mma.sync exactly as decode_mma_kernel does.  Against the per-warp cp.async
+// rings: 8 TMA instructions per 64 tokens instead of 2 x 16 cp.async per lane per 16, and the
+// bytes in flight per SM are set by the ring depth, not by the warps' issue.
+#ifndef CDSP_DEC_TMA
+#define CDSP_DEC_TMA 1
+#endif
+#ifndef CDSP_DEC_TMA_STAGES  // 64-token K + V stages per CTA (32 KB each at d = 128)
+#define CDSP_DEC_TMA_STAGES 3
+#endif
+#ifndef CDSP_DEC_TMA_WARPS  // consumer warps per CTA (one 16-token sub-tile of each stage each)
+#define CDSP_DEC_TMA_WARPS 4
+#endif
+constexpr int kTW = CDSP_DEC_TMA_WARPS;
+#ifndef CDSP_DEC_NOCOMPUTE
+#define CDSP_DEC_NOCOMPUTE 0
+#endif
+constexpr int kTStage = 16 * kTW;            // tokens per stage
+constexpr int kTNst = CDSP_DEC_TMA_STAGES;
+
+struct DecTmaArgs {
+    CUtensorMap k, v;  // [num_blocks * B, Hkv_t, D], box 16 rows x 1 head x 64 d
+    DecodeParams p;
+    int64_t oob_row;   // a row coordinate past the tensor (zero-filled box)
+};
+
+template <int HD>
+struct TmaDecLayout {
+    static constexpr int NH = HD / 64;                  // 64-d boxes per token row
+    static constexpr int BOX = 16 * 128;                // 16 rows x 128 bytes
+    static constexpr int SUB = NH * BOX;                // one 16-token sub-tile of K (or V)
+    static constexpr int STAGE = 2 * kTW * SUB;         // K sub-tiles, then V sub-tiles
+    static constexpr int RING = kTNst * STAGE;
+    static constexpr int SMEM = RING + 1024;            // + alignment
+};
+template <int HD>
+__device__ __forceinline__ uint32_t tdec_chunk(uint32_t sub, int tok, int ch) {  // 16-byte chunk ch of row tok
+    return sub + static_cast<uint32_t>((ch >> 3) * TmaDecLayout<HD>::BOX + tok * 128 + (((ch & 7) ^ (tok & 7)) << 4));
+}
+
+template <int HD, int G>
+__global__ void __launch_bounds__((kTW + 1) * 32) decode_tma_kernel(const __grid_constant__ DecTmaArgs a) {
+    using L = TmaDecLayout<HD>;
+    constexpr int KS = HD / 16, ND = HD / 8;
+    const DecodeParams& p = a.p;
+    extern __shared__ uint8_t dsm_t[];
+    __shared__ __align__(8) uint64_t full_b[kTNst], empty_b[kTNst];
+    __shared__ int s_last;
+    dstamp(0);
+    uint8_t* sm = dsm_t + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(dsm_t)) & 1023u)) & 1023u);
+    const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kvh = blockIdx.y, split = blockIdx.x;
+    const int64_t t0 = static_cast<int64_t>(split) * p.tok_per_split;
+    const int64_t t1 = min(p.n_ctx, t0 + p.tok_per_split);
+    const int n_st = static_cast<int>((t1 - t0 + kTStage - 1) / kTStage);
+    auto fb = [&](int i) { return static_cast<uint32_t>(__cvta_generic_to_shared(&full_b[i])); };
+    auto eb = [&](int i) { return static_cast<uint32_t>(__cvta_generic_to_shared(&empty_b[i])); };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kTNst; ++i) {
+            ptx::mbar_init(fb(i), 1);
+            ptx::mbar_init(eb(i), kTW);
+        }
+        ptx::fence_barrier_init();
+    }
+    __syncthreads();
+
+    // states for the CTA merge alias the ring (written after the last stage is consumed)
+    float* sm_o = reinterpret_cast<float*>(sm);     // [kTW][G][HD]
+    float* sm_ml = sm_o + kTW * G * HD;             // [kTW][G][2]
+    float* w_sh = sm_ml + kTW * G * 2;              // [32][G]
+    float* lse_sh = w_sh + 32 * G;
+    static_assert((kTW * G * HD + kTW * G * 2 + 33 * G) * 4 <= L::RING, "merge state must fit in the ring");
+
+    const int g = lane >> 2, t = lane & 3;
+    float o[ND][2];
+#pragma unroll
+    for (int nd = 0; nd < ND; ++nd) o[nd][0] = o[nd][1] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    if (warp == kTW) {
+        // ===== producer: one thread issues every TMA of the CTA's range
+        if (lane == 0) {
+            ptx::tma_prefetch_desc(&a.k);
+            ptx::tma_prefetch_desc(&a.v);
+            for (int j = 0; j < n_st; ++j) {
+                const int st = j % kTNst;
+                if (j >= kTNst) ptx::mbar_wait(eb(st), ((j / kTNst) - 1) & 1);
+                ptx::mbar_expect_tx(fb(st), L::STAGE);
+                const uint32_t sb = ring + static_cast<uint32_t>(st) * L::STAGE;
+#pragma unroll
+                for (int w = 0; w < kTW; ++w) {
+                    const int64_t base = t0 + static_cast<int64_t>(j) * kTStage + 16 * w;
+                    int64_t row = a.oob_row;
+                    if (base < t1) {
+                        const int64_t blk = __ldg(p.bt + (base >> p.b_shift));
+                        if (blk >= 0 && blk < p.num_blocks) row = (blk << p.b_shift) | (base & ((int64_t{1} << p.b_shift) - 1));
+                    }
+#pragma unroll
+                    for (int h = 0; h < L::NH; ++h) {
+                        ptx::tma_load_3d(sb + w * L::SUB + h * L::BOX, &a.k, fb(st), 64 * h, kvh, static_cast<int>(row));
+                        ptx::tma_load_3d(sb + (kTW + w) * L::SUB + h * L::BOX, &a.v, fb(st), 64 * h, kvh,
+                                         static_cast<int>(row));
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ===== consumer warp w: sub-tile w of every stage
+        uint32_t qa[KS][2];
+        {
+            const __nv_bfloat16* qp = static_cast<const __nv_bfloat16*>(p.q) + (static_cast<size_t>(kvh) * G + g) * HD;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk) {
+                qa[kk][0] = g < G ? *reinterpret_cast<const uint32_t*>(qp + 16 * kk + 2 * t) : 0u;
+                qa[kk][1] = g < G ? *reinterpret_cast<const uint32_t*>(qp + 16 * kk + 2 * t + 8) : 0u;
+            }
+        }
+        for (int j = 0; j < n_st; ++j) {
+            const int st = j % kTNst;
+            const int64_t base = t0 + static_cast<int64_t>(j) * kTStage + 16 * warp;
+            ptx::mbar_wait(fb(st), (j / kTNst) & 1);
+            const uint32_t sk = ring + static_cast<uint32_t>(st) * L::STAGE + warp * L::SUB;
+            const uint32_t sv = sk + kTW * L::SUB;
+            if (!CDSP_DEC_NOCOMPUTE && base < t1) {  // (NOCOMPUTE: dev probe of the stream alone)
+                int64_t blk = __ldg(p.bt + (base >> p.b_shift));
+                const bool page_ok = blk >= 0 && blk < p.num_blocks;
+                const int nvis = page_ok ? static_cast<int>((t1 - base < 16 ? t1 - base : int64_t{16})) : 0;
+                if (nvis < 16 && page_ok) {
+                    // rows past the range are real cache rows (maybe never written): zero their V
+                    // so that P = 0 cannot meet a NaN
+                    for (int x = lane; x < (16 - nvis) * (HD / 8); x += 32) {
+                        const int tok = nvis + x / (HD / 8), ch = x % (HD / 8);
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(tdec_chunk<HD>(sv, tok, ch)), "r"(0u)
+                                     : "memory");
+                    }
+                    __syncwarp();
+                }
+                float s[2][2] = {{0.f, 0.f}, {0.f, 0.f}}, s2[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+                for (int kk = 0; kk < KS; kk += 2) {
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt) {
+                        const int tok = 8 * nt + (lane & 7), ch = 2 * kk + (lane >> 3);
+                        uint32_t b0, b1, b2, b3;
+                        ldsm_x4(tdec_chunk<HD>(sk, tok, ch), b0, b1, b2, b3);
+                        mma_top(s[nt][0], s[nt][1], qa[kk][0], qa[kk][1], b0, b1);
+                        mma_top(s2[nt][0], s2[nt][1], qa[kk + 1][0], qa[kk + 1][1], b2, b3);
+                    }
+                }
+                float mx = -INFINITY;
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int tk = 8 * nt + 2 * t + e;
+                        const float sv2 = s[nt][e] + s2[nt][e];
+                        s[nt][e] = tk < nvis ? sv2 * p.scale_log2 : -INFINITY;
+                        mx = fmaxf(mx, s[nt][e]);
+                    }
+                mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, 1));
+                mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, 2));
+                if (__any_sync(0xFFFFFFFFu, mx > m + 8.f)) {  // lazy max (P <= 2^8), as decode_mma_kernel
+                    const float mn = fmaxf(m, mx);
+                    const float alpha = ex2f(m - mn);
+                    m = mn;
+                    l *= alpha;
+#pragma unroll
+                    for (int nd = 0; nd < ND; ++nd) {
+                        o[nd][0] *= alpha;
+                        o[nd][1] *= alpha;
+                    }
+                }
+                const float mu = m == -INFINITY ? 0.f : m;
+                float pr[2][2];
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        pr[nt][e] = ex2f(s[nt][e] - mu);
+                        l += pr[nt][e];
+                    }
+                const uint32_t pa0 = pack_bf16x2(pr[0][0], pr[0][1]), pa2 = pack_bf16x2(pr[1][0], pr[1][1]);
+#pragma unroll
+                for (int nd = 0; nd < ND; nd += 2) {
+                    const int tok = (lane & 7) + 8 * ((lane >> 3) & 1), ch = nd + (lane >> 4);
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4_t(tdec_chunk<HD>(sv, tok, ch), b0, b1, b2, b3);
+                    mma_top(o[nd][0], o[nd][1], pa0, pa2, b0, b1);
+                    mma_top(o[nd + 1][0], o[nd + 1][1], pa0, pa2, b2, b3);
+                }
+                if (nvis < 16 && page_ok) ptx::fence_proxy_async_smem();  // generic writes before the next TMA
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(eb(st));
+        }
+        l += __shfl_xor_sync(0xFFFFFFFFu, l, 1);
+        l += __shfl_xor_sync(0xFFFFFFFFu, l, 2);
+    }
+    __syncthreads();  // every stage consumed: the ring is free for the merge state
+    dstamp(1);
+    if (warp < kTW && g < G) {
+#pragma unroll
+        for (int nd = 0; nd < ND; ++nd) {
+            sm_o[(warp * G + g) * HD + 8 * nd + 2 * t] = o[nd][0];
+            sm_o[(warp * G + g) * HD + 8 * nd + 2 * t + 1] = o[nd][1];
+        }
+        if (t == 0) {
+            sm_ml[(warp * G + g) * 2] = m;
+            sm_ml[(warp * G + g) * 2 + 1] = l;
+        }
+    }
+    finish_cta<__nv_bfloat16, HD, G>(p, kTW, sm_o, sm_ml, w_sh, lse_sh, &s_last);
+    dstamp(3);
+}
+
 struct WsLayout {
     size_t cnt1, cnt2, l1, l2, o1, o2, total;
 };
@@ -696,23 +1049,33 @@ constexpr size_t mma_smem() {
     return static_cast<size_t>(kMmaWarps) * kStages * 2 * 16 * HD * 2;
 }
 
-// The kernel a call runs: bf16 -> tensor-core kernel, f32 -> SIMT kernel.
+// The kernel a call runs: bf16 -> tensor-core kernel (TMA-fed for block size >= 16), f32 ->
+// SIMT kernel.
 struct Sel {
     const void* fn;
     int threads;
     size_t smem;
-    int step;  // tokens per warp step
+    int step;  // tokens per split granule
+    bool tma;
 };
+template <int HD>
+Sel select_tma(int G) {
+    const void* fn = G == 1 ? reinterpret_cast<const void*>(decode_tma_kernel<HD, 1>)
+                   : G == 2 ? reinterpret_cast<const void*>(decode_tma_kernel<HD, 2>)
+                   : G == 4 ? reinterpret_cast<const void*>(decode_tma_kernel<HD, 4>)
+                            : reinterpret_cast<const void*>(decode_tma_kernel<HD, 8>);
+    return {fn, (kTW + 1) * 32, static_cast<size_t>(TmaDecLayout<HD>::SMEM), kTStage, true};
+}
 template <typename T, int HD, int G>
 Sel select_t(bool ps) {
     if constexpr (sizeof(T) == 2) {
         const void* fn = ps ? reinterpret_cast<const void*>(decode_mma_kernel<HD, G, true>)
                             : reinterpret_cast<const void*>(decode_mma_kernel<HD, G, false>);
-        return {fn, kMmaWarps * 32, mma_smem<HD>(), 16};
+        return {fn, kMmaWarps * 32, mma_smem<HD>(), 16, false};
     } else {
         constexpr int TPI = 32 / (HD / 4);
         return {reinterpret_cast<const void*>(decode_attn_kernel<T, HD, G>), kThreads, simt_smem<T, HD, G>(),
-                kNI * TPI};
+                kNI * TPI, false};
     }
 }
 template <typename T, int HD>
@@ -725,6 +1088,7 @@ Sel select_g(int G, bool ps) {
     }
 }
 Sel select(int32_t dtype, int D, int G, bool ps) {
+    if (CDSP_DEC_TMA && dtype == CDSP_BF16 && ps) return D == 128 ? select_tma<128>(G) : select_tma<64>(G);
     if (dtype == CDSP_BF16) return D == 128 ? select_g<__nv_bfloat16, 128>(G, ps) : select_g<__nv_bfloat16, 64>(G, ps);
     return D == 128 ? select_g<float, 128>(G, ps) : select_g<float, 64>(G, ps);
 }
@@ -841,6 +1205,21 @@ cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_decode_target
     p.out = out->ptr;
     p.lse = lse;
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (k.tma) {
+        const int64_t rows = cache->num_blocks * B;
+        CDSP_REQUIRE(rows < (int64_t{1} << 31) - 1, CDSP_ERR_CAPACITY, "cache of %lld rows exceeds the TMA coordinate range",
+                     static_cast<long long>(rows));
+        DecTmaArgs ta;
+        std::memset(&ta, 0, sizeof(ta));
+        CDSP_CHECK_STATUS(make_tile_map(&ta.k, cache->k_cache[t], rows, hkv_local, D, 16));
+        CDSP_CHECK_STATUS(make_tile_map(&ta.v, cache->v_cache[t], rows, hkv_local, D, 16));
+        ta.p = p;
+        ta.oob_row = rows;
+        void* targs[] = {&ta};
+        CDSP_CUDA(cudaLaunchKernel(k.fn, dim3(static_cast<unsigned>(p.n_split), static_cast<unsigned>(hkv_local)),
+                                   dim3(static_cast<unsigned>(k.threads)), targs, k.smem, st));
+        return CDSP_OK;
+    }
     void* args[] = {&p};
     CDSP_CUDA(cudaLaunchKernel(k.fn, dim3(static_cast<unsigned>(p.n_split), static_cast<unsigned>(hkv_local)),
                                dim3(static_cast<unsigned>(k.threads)), args, k.smem, st));

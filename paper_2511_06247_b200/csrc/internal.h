@@ -1,6 +1,7 @@
 // internal.h — launchers shared between the libcdsp.so translation units (not exported).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -46,6 +47,9 @@ cdsp_status attention_device_init();
 
 // KV tiles (128 keys) the bf16 kernel can list per launch (all blocks together).
 int attention_tc_max_tiles(int D);
+// TMA descriptor of a [rows, H, D] bf16 tensor: 128-byte swizzle, box = box_rows x 1 head x 64 d
+// (zero fill out of bounds); defined in attn_tc.cu, used by the decode kernel
+cdsp_status make_tile_map(CUtensorMap* m, const void* base, int64_t rows, int H, int D, int box_rows);
 
 cdsp_status launch_attention_tc(const AttnArgs& a, cudaStream_t st);    // bf16, tcgen05/TMEM/TMA
 cdsp_status launch_attention_simt(const AttnArgs& a, cudaStream_t st);  // fp32, FFMA

@@ -52,5 +52,15 @@ for it in range(4):
             continue
         print(f"  {name:9s} n={len(x):4d} q0={np.min(x):7.2f} q10={np.quantile(x, .1):7.2f} q50={np.median(x):7.2f} "
               f"q90={np.quantile(x, .9):7.2f} max={np.max(x):7.2f}")
+    sm = t[:, 7] - 1
+    le = rel[:, 1]
+    by_sm = {}
+    for i in range(n):
+        by_sm.setdefault(int(sm[i]), []).append(le[i])
+    last = np.array([max(v) for v in by_sm.values()])
+    print(f"  SMs used {len(by_sm)}; per-SM last loop_end q10={np.quantile(last, .1):.2f} q50={np.median(last):.2f} "
+          f"q90={np.quantile(last, .9):.2f}; CTAs/SM {sorted(set(len(v) for v in by_sm.values()))}")
+    lo = sorted(by_sm, key=lambda x: max(by_sm[x]))
+    print(f"  slowest SMs {lo[-8:]}  fastest SMs {lo[:8]}")
     buf[:] = 0
     torch.cuda.synchronize()
