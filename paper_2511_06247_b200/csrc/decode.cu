@@ -11,10 +11,11 @@
 //
 // B200 design.  One query row per head makes this a pure HBM stream: per token 2 Hkv_t D
 // elements are read once and every byte feeds G = Hq_t/Hkv_t dot products, ~4 FLOP/B, far
-// below any tensor-core ridge, so it is sized for bandwidth.  The bf16 path
-// (decode_mma_kernel, below) streams K/V with cp.async and computes S and PV with the legacy
-// warp MMA (mma.sync m16n8k16: one query row per head leaves no M for a tcgen05 tile); the
-// f32 path (decode_attn_kernel, described here) runs on the FMA pipe:
+// below any tensor-core ridge, so it is sized for bandwidth.  The bf16 paths compute S and PV
+// with the legacy warp MMA (mma.sync m16n8k16: one query row per head leaves no M for a
+// tcgen05 tile) and are fed by TMA page boxes (decode_tma_kernel, block size >= 16) or per-warp
+// cp.async rings (decode_mma_kernel, any block size); the f32 path (decode_attn_kernel,
+// described here) runs on the FMA pipe:
 //  * grid = (n_split, Hkv_t), 256 threads; n_split x Hkv_t = one wave of resident CTAs
 //    (occupancy x 148) so that every SM streams; each CTA owns a contiguous token range, its
 //    8 warps interleave 8-vector steps.
@@ -28,8 +29,8 @@
 //    are gathered back (8 shuffles), so every lane runs the online softmax of its token
 //    slot locally (no cross-lane max) and P V needs no further exchange.
 //  * partials: the CTA merges its 8 x TPI lane-group states in shared memory; splits merge
-//    in two levels inside the same launch (the last CTA of each group of 16 splits, then the
-//    last group): no second kernel, no host round trip.  Weights 2^(m_j - M) (R3 in base 2).
+//    inside the same launch (merge_slice: the last finishers, column slices in parallel):
+//    no second kernel, no host round trip.  Weights 2^(m_j - M) (R3 in base 2).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
