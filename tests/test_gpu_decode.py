@@ -21,14 +21,15 @@ TOL = {torch.bfloat16: 2e-2, torch.float32: 1e-4}
 LSE_TOL = 1e-3
 
 
-def _caches(k, v, tp, B, seed=7, spare=8):
-    """Fill tp paged caches with k/v [N,Hkv,D] through cdsp_kv_transfer_to_decode (s=1 plan)."""
+def _caches(k, v, tp, B, seed=7, spare=8, fill=0.0):
+    """Fill tp paged caches with k/v [N,Hkv,D] through cdsp_kv_transfer_to_decode (s=1 plan);
+    every other cache row holds `fill` (NaN: rows no token was ever written to)."""
     N, Hkv, D = k.shape
     n_logical = (N + B - 1) // B
     nb = n_logical + spare
     bt = block_table(n_logical, nb, seed=seed).cuda()
-    kc = [torch.zeros((nb, B, Hkv // tp, D), dtype=k.dtype, device="cuda") for _ in range(tp)]
-    vc = [torch.zeros_like(x) for x in kc]
+    kc = [torch.full((nb, B, Hkv // tp, D), fill, dtype=k.dtype, device="cuda") for _ in range(tp)]
+    vc = [torch.full_like(x, fill) for x in kc]
     dst = api.DecodeTarget(kc, vc, B, bt)
     plan = api.Plan([(N, [0])])
     comm = api.Comm(0, 1, 0, N, Hkv, D, k.dtype)
@@ -83,10 +84,22 @@ def test_decode_block_sizes(B):
         _check_rank(q[-1:], k, v, dst, t, 8, n_ctx, torch.bfloat16)
 
 
-def test_decode_sharp_long_context_two_level_merge():
-    """n_ctx large enough for > 16 splits per KV head (both in-kernel merge levels), sharp
-    queries (q x 4) stress the online softmax; the workspace is reused across calls and
-    ranks (every call must leave its counters zeroed)."""
+@pytest.mark.parametrize("B,n_ctx", [(16, 1000), (16, 4097), (64, 1000), (256, 3001), (8, 1000)])
+def test_decode_never_written_rows_are_nan(B, n_ctx):
+    """Cache rows past n_ctx in the last page (and every unused page) hold NaN, as memory no
+    token was ever written to may: they must not reach the output (the TMA kernel loads whole
+    16-row page pieces and zeroes V past the range; the cp.async kernel zero-fills)."""
+    q, k, v = qkv(n_ctx + (n_ctx % 2), 32, 8, 128, torch.bfloat16, seed=B + n_ctx)
+    dst = _caches(k, v, 8, B, fill=float("nan"))
+    for t in (0, 7):
+        out, lse = _check_rank(q[n_ctx - 1:n_ctx], k, v, dst, t, 8, n_ctx, torch.bfloat16)
+        assert torch.isfinite(out.float()).all() and torch.isfinite(lse).all()
+
+
+def test_decode_sharp_long_context_many_splits():
+    """n_ctx large enough for hundreds of splits per KV head (the last-finisher slice merge
+    over all of them), sharp queries (q x 4) stress the online softmax; the workspace is
+    reused across calls and ranks (every call must leave its counters zeroed)."""
     n_ctx = 150001
     q, k, v = qkv(n_ctx + 1, 32, 8, 128, torch.bfloat16, seed=3, sharp=True)
     dst = _caches(k, v, 8, 16)
