@@ -64,35 +64,71 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 50 ms during the timed region."""
+    """SM clock / throttle reasons sampled during the timed region: NVML every 5 ms (the
+    attention kernel meets the 1000 W cap within ~45 ms of load, so a coarser sampler misses
+    the drop), else nvidia-smi every 50 ms."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+    NVML_BITS = (0x8, 0x40, 0x20, 0x4)  # nvmlClocksEventReason{HwSlowdown,HwThermalSlowdown,SwThermalSlowdown,SwPowerCap}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, [reason names])
+        self.source = None
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
-        try:
-            p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                  "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE,
-                                 stderr=subprocess.DEVNULL, text=True)
+    def _run_nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = None
+        try:  # the CUDA device's own GPU (NVML ignores CUDA_VISIBLE_DEVICES)
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
         except Exception:
-            return
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        self.source = "nvml, 5 ms"
+        while not self._stop.is_set():
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append((float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)), float(mx),
+                              [n for n, b in zip(self.NAMES, self.NVML_BITS) if r & b]))
+            time.sleep(0.005)
+
+    def _run_smi(self):
+        p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                              "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE,
+                             stderr=subprocess.DEVNULL, text=True)
+        self.source = "nvidia-smi, 50 ms"
         while not self._stop.is_set():
             line = p.stdout.readline()
             if not line:
                 break
-            self.rows.append([x.strip() for x in line.split(",")])
+            r = [x.strip() for x in line.split(",")]
+            if len(r) >= 2 and r[0].replace(".", "").isdigit() and r[1].replace(".", "").isdigit():
+                self.rows.append((float(r[0]), float(r[1]),
+                                  [self.NAMES[i] for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"]))
         p.terminate()
+
+    def _run(self):
+        try:
+            self._run_nvml()
+            return
+        except Exception:
+            self.rows = []
+        try:
+            self._run_smi()
+        except Exception:
+            return
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        time.sleep(0.3)
+        time.sleep(0.3)  # sampler up (NVML init / nvidia-smi start); idle samples are not kept
+        self.rows = []
         return self
 
     def __exit__(self, *a):
@@ -101,13 +137,13 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n in r[2]})
+        capped = sum(1 for r in self.rows if "sw_power_cap" in r[2])
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "sw_power_cap_frac": capped / len(self.rows),
+                "source": self.source}
 
 
 # ------------------------------------------------------------------------------ CPU oracle
