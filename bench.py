@@ -330,18 +330,17 @@ def main():
         comm.reset(stream)
         if s == 1:
             # one rank: the zigzag partition (S_0 then S_1) is the identity, so the shard IS the
-            # chunk and a2 moves no data; the output is written in place
-            # the attention is enqueued first: its persistent grid takes every SM, and the
-            # transfer (same dependencies, own stream) fills SMs as the attention's tail frees
-            # them -- enqueued first, the scatter's CTAs would hold SMs the attention needs
-            ev_kv.record(stream)
-            if xfer_first and not no_xfer:  # measurement control: the scatter enqueued first
+            # chunk and a2 moves no data; the output is written in place.  a4 + a7 in one call:
+            # the library enqueues the attention first (its persistent grid takes every SM), then
+            # the scatter on its transfer stream, which fills SMs as the attention's tail frees them
+            if not (xfer_first or no_xfer):
+                api.prefill_chunk_transfer(qq, kk, vv, comm.kvstore(), group, dst, 0.0, oo, lse_s, stream)
+                return
+            if xfer_first:  # measurement control: the scatter enqueued first (holds SMs the attention needs)
+                ev_kv.record(stream)
                 xfer.wait_event(ev_kv)
                 api.kv_transfer_to_decode(kk, vv, group, dst, xfer)
             api.prefill_chunk(qq, kk, vv, comm.kvstore(), group, 0.0, oo, lse_s, stream)
-            if not xfer_first and not no_xfer:
-                xfer.wait_event(ev_kv)
-                api.kv_transfer_to_decode(kk, vv, group, dst, xfer)
             stream.wait_stream(xfer)
             return
         api.zigzag_gather(qq, s, rank, qs, stream)

@@ -45,7 +45,7 @@ extern "C" {
 #define CDSP_API
 #endif
 
-#define CDSP_ABI_VERSION 3
+#define CDSP_ABI_VERSION 4
 #define CDSP_IPC_HANDLE_BYTES 64   /* one cudaIpcMemHandle_t */
 #define CDSP_MAX_SP 8
 
@@ -303,6 +303,19 @@ typedef struct {
 CDSP_API cdsp_status cdsp_kv_transfer_to_decode(const cdsp_tensor* k, const cdsp_tensor* v,
                                                 const cdsp_sp_group* sp_group,
                                                 const cdsp_decode_target* dst, void* cuda_stream);
+
+/* cdsp_prefill_chunk and cdsp_kv_transfer_to_decode of the same k / v in one call (P:135,
+ * each chunk's KV is streamed to the decode instance as the chunk is prefilled): the
+ * same results, the same decode caches bit for bit and the same error count
+ * (cdsp_kv_transfer_errors) as the two calls on cuda_stream.  The attention is enqueued first;
+ * the scatter runs on the communicator's own transfer stream (it only reads k / v), filling SMs
+ * as the attention's persistent grid frees them, and cuda_stream waits for both.  (Storing
+ * each KV tile from the attention's shared-memory stages inside the attention launch was
+ * measured slower: DESIGN §6.1.)  Errors: those of the two calls. */
+CDSP_API cdsp_status cdsp_prefill_chunk_transfer(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
+                                                 cdsp_kvstore* prev_kv, const cdsp_sp_group* sp_group,
+                                                 float softmax_scale, cdsp_tensor* out, float* lse,
+                                                 const cdsp_decode_target* dst, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------------
  * CDSP prefill scheduler (§5.1).  Host-only, pure.

@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = (
     "cdsp_comm_profile_read", "cdsp_decode_workspace_bytes", "cdsp_decode_attention", "cdsp_comm_profile_ring",
     "cdsp_comm_create_layers", "cdsp_kvstore_get_layer", "cdsp_prefill_chunk_layer",
     "cdsp_striped_gather", "cdsp_striped_scatter", "cdsp_fit_latency_model", "cdsp_schedule_prefill",
-    "cdsp_comm_reserve", "cdsp_comm_set_ring_options", "cdsp_attention_fwd_blocks",
+    "cdsp_comm_reserve", "cdsp_comm_set_ring_options", "cdsp_attention_fwd_blocks", "cdsp_prefill_chunk_transfer",
 )
 
 
@@ -134,6 +134,10 @@ def lib():
             "cdsp_prefill_chunk": [ctypes.POINTER(Tensor)] * 3 + [ctypes.POINTER(KvStoreC),
                                                                   ctypes.POINTER(SpGroupC), f32,
                                                                   ctypes.POINTER(Tensor), P, P],
+            "cdsp_prefill_chunk_transfer": [ctypes.POINTER(Tensor)] * 3 + [ctypes.POINTER(KvStoreC),
+                                                                           ctypes.POINTER(SpGroupC), f32,
+                                                                           ctypes.POINTER(Tensor), P,
+                                                                           ctypes.POINTER(DecodeTargetC), P],
             "cdsp_lse_merge": [i32, ctypes.POINTER(ctypes.POINTER(Tensor)), ctypes.POINTER(P),
                                ctypes.POINTER(Tensor), P, P],
             "cdsp_kv_transfer_to_decode": [ctypes.POINTER(Tensor), ctypes.POINTER(Tensor),
@@ -417,6 +421,20 @@ def prefill_chunk(q, k, v, prev_kv: KvStore, sp_group: SpGroup, softmax_scale: f
         _check(lib().cdsp_prefill_chunk_layer(ctypes.byref(tq), ctypes.byref(tk), ctypes.byref(tv),
                                               ctypes.byref(prev_kv.c), ctypes.byref(sp_group.c), int(layer),
                                               float(softmax_scale), ctypes.byref(to), _ptr(lse), _stream(stream)))
+    return out
+
+
+def prefill_chunk_transfer(q, k, v, prev_kv: KvStore, sp_group: SpGroup, dst: "DecodeTarget",
+                           softmax_scale: float = 0.0, out: Optional[torch.Tensor] = None,
+                           lse: Optional[torch.Tensor] = None, stream=None):
+    """cdsp_prefill_chunk_transfer: prefill_chunk + kv_transfer_to_decode of the same shard (the
+    transfer fused into the attention launch where the library can)."""
+    if out is None:
+        out = torch.empty_like(q)
+    tq, tk, tv, to = as_tensor(q), as_tensor(k), as_tensor(v), as_tensor(out)
+    _check(lib().cdsp_prefill_chunk_transfer(ctypes.byref(tq), ctypes.byref(tk), ctypes.byref(tv),
+                                             ctypes.byref(prev_kv.c), ctypes.byref(sp_group.c), float(softmax_scale),
+                                             ctypes.byref(to), _ptr(lse), ctypes.byref(dst.c), _stream(stream)))
     return out
 
 

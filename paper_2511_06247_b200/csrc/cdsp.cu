@@ -127,6 +127,8 @@ struct cdsp_comm_s {
     int* err_dev = nullptr;
     unsigned long long* bad_count = nullptr;
     cudaStream_t comm_stream = nullptr;
+    cudaStream_t xfer_stream = nullptr;  // cdsp_prefill_chunk_transfer's decode-cache scatter
+    cudaEvent_t ev_x0 = nullptr, ev_x1 = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
     // layers (cdsp_comm_create_layers): one K/V store per layer, positions shared
     int n_layers = 1;
@@ -673,7 +675,9 @@ cdsp_status cdsp_comm_create_layers(cdsp_comm* out, int32_t rank, int32_t world,
     if (e != cudaSuccess) return fail(e, "cudaMemset");
     e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return fail(e, "cudaStreamCreate");
-    cudaEvent_t* evs[5] = {&c->ev_ready, &c->ev_done, &c->ev_bal, &c->ev_app, &c->ev_fin};
+    e = cudaStreamCreateWithFlags(&c->xfer_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(e, "cudaStreamCreate");
+    cudaEvent_t* evs[7] = {&c->ev_ready, &c->ev_done, &c->ev_bal, &c->ev_app, &c->ev_fin, &c->ev_x0, &c->ev_x1};
     for (auto* ev : evs) {
         e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
         if (e != cudaSuccess) return fail(e, "cudaEventCreate");
@@ -887,10 +891,11 @@ cdsp_status cdsp_comm_destroy(cdsp_comm c) {
     if (c->bad_count) cudaFree(c->bad_count);
     if (c->err_host) cudaFreeHost(c->err_host);
     if (c->lg && --c->lg->refs == 0) delete c->lg;
-    cudaEvent_t evs[5] = {c->ev_ready, c->ev_done, c->ev_bal, c->ev_app, c->ev_fin};
+    cudaEvent_t evs[7] = {c->ev_ready, c->ev_done, c->ev_bal, c->ev_app, c->ev_fin, c->ev_x0, c->ev_x1};
     for (auto ev : evs)
         if (ev) cudaEventDestroy(ev);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->xfer_stream) cudaStreamDestroy(c->xfer_stream);
     delete c;
     return CDSP_OK;
 }
@@ -968,9 +973,60 @@ cdsp_status cdsp_prefill_chunk(const cdsp_tensor* q, const cdsp_tensor* k, const
     return cdsp_prefill_chunk_layer(q, k, v, prev_kv, sp_group, 0, softmax_scale, out, lse, cuda_stream);
 }
 
+namespace cdsp {
+namespace {
+// The decode target's checks shared by cdsp_kv_transfer_to_decode and the fused path.
+static cdsp_status check_decode_target(const cdsp_decode_target* dst, const cdsp_tensor* k, const ChunkInfo& ci) {
+    CDSP_REQUIRE(dst->tp >= 1 && dst->tp <= 8, CDSP_ERR_INVALID, "decode tp %d not in [1,8]", dst->tp);
+    CDSP_REQUIRE(k->H % dst->tp == 0, CDSP_ERR_UNSUPPORTED,
+                 "Hkv=%lld not divisible by decode tp=%d (KV-head replication is not defined)",
+                 static_cast<long long>(k->H), dst->tp);
+    CDSP_REQUIRE(dst->block_size >= 1 && dst->num_blocks >= 1 && dst->block_table && dst->k_cache && dst->v_cache,
+                 CDSP_ERR_INVALID, "bad decode target");
+    CDSP_REQUIRE(dst->n_table * dst->block_size >= ci.C + ci.L, CDSP_ERR_CAPACITY,
+                 "block table covers %lld positions, chunk ends at %lld",
+                 static_cast<long long>(dst->n_table * dst->block_size), static_cast<long long>(ci.C + ci.L));
+    for (int t = 0; t < dst->tp; ++t)
+        CDSP_REQUIRE(dst->k_cache[t] && dst->v_cache[t], CDSP_ERR_INVALID, "NULL cache pointer for tp rank %d", t);
+    return CDSP_OK;
+}
+
+static cdsp_status prefill_impl(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v, cdsp_kvstore* prev_kv,
+                                const cdsp_sp_group* sp_group, int32_t layer, float softmax_scale, cdsp_tensor* out,
+                                float* lse, void* cuda_stream);
+}  // namespace
+}  // namespace cdsp
+
 cdsp_status cdsp_prefill_chunk_layer(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
                                      cdsp_kvstore* prev_kv, const cdsp_sp_group* sp_group, int32_t layer,
                                      float softmax_scale, cdsp_tensor* out, float* lse, void* cuda_stream) {
+    return prefill_impl(q, k, v, prev_kv, sp_group, layer, softmax_scale, out, lse, cuda_stream);
+}
+
+cdsp_status cdsp_prefill_chunk_transfer(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v,
+                                        cdsp_kvstore* prev_kv, const cdsp_sp_group* sp_group, float softmax_scale,
+                                        cdsp_tensor* out, float* lse, const cdsp_decode_target* dst,
+                                        void* cuda_stream) {
+    CDSP_REQUIRE(dst != nullptr && sp_group && sp_group->comm, CDSP_ERR_INVALID, "NULL decode target / group");
+    cdsp_comm c = sp_group->comm;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    CDSP_CUDA(cudaEventRecord(c->ev_x0, st));  // this call's k / v are ready
+    // the attention first: its persistent grid takes every SM; the scatter, on the comm's
+    // transfer stream, fills SMs as the attention's tail frees them (enqueued first, its CTAs
+    // would hold SMs the attention needs)
+    CDSP_CHECK_STATUS(prefill_impl(q, k, v, prev_kv, sp_group, 0, softmax_scale, out, lse, cuda_stream));
+    CDSP_CUDA(cudaStreamWaitEvent(c->xfer_stream, c->ev_x0, 0));
+    CDSP_CHECK_STATUS(cdsp_kv_transfer_to_decode(k, v, sp_group, dst, c->xfer_stream));
+    CDSP_CUDA(cudaEventRecord(c->ev_x1, c->xfer_stream));
+    CDSP_CUDA(cudaStreamWaitEvent(st, c->ev_x1, 0));  // the caller's stream sees both
+    return CDSP_OK;
+}
+
+namespace cdsp {
+namespace {
+static cdsp_status prefill_impl(const cdsp_tensor* q, const cdsp_tensor* k, const cdsp_tensor* v, cdsp_kvstore* prev_kv,
+                                const cdsp_sp_group* sp_group, int32_t layer, float softmax_scale, cdsp_tensor* out,
+                                float* lse, void* cuda_stream) {
     CDSP_REQUIRE(sp_group && sp_group->comm && sp_group->plan && prev_kv, CDSP_ERR_INVALID,
                  "NULL sp_group/comm/plan/prev_kv");
     CDSP_CHECK_STATUS(check_tensor(q, "q"));
@@ -1089,6 +1145,8 @@ cdsp_status cdsp_prefill_chunk_layer(const cdsp_tensor* q, const cdsp_tensor* k,
     CDSP_CHECK_STATUS(phase_ring(c, ci, r, layer, q->ptr, Hq, out->ptr, lse, scale, st, nullptr));
     return prebalance_next(c, ci, r, layer, sp_group->plan, true);
 }
+}  // namespace
+}  // namespace cdsp
 
 // ------------------------------------------------------------------------------- merge
 cdsp_status cdsp_lse_merge(int32_t n, const cdsp_tensor* const* o_parts, const float* const* lse_parts,
@@ -1125,15 +1183,7 @@ cdsp_status cdsp_kv_transfer_to_decode(const cdsp_tensor* k, const cdsp_tensor* 
     CDSP_REQUIRE(k->dtype == v->dtype, CDSP_ERR_DTYPE, "k/v dtypes differ");
     CDSP_REQUIRE(k->T == 2 * ci.m && v->T == k->T && v->H == k->H && v->D == k->D, CDSP_ERR_SHAPE,
                  "k/v must be this rank's [2m, Hkv, D] shard");
-    CDSP_REQUIRE(dst->tp >= 1 && dst->tp <= 8, CDSP_ERR_INVALID, "decode tp %d not in [1,8]", dst->tp);
-    CDSP_REQUIRE(k->H % dst->tp == 0, CDSP_ERR_UNSUPPORTED,
-                 "Hkv=%lld not divisible by decode tp=%d (KV-head replication is not defined)",
-                 static_cast<long long>(k->H), dst->tp);
-    CDSP_REQUIRE(dst->block_size >= 1 && dst->num_blocks >= 1 && dst->block_table && dst->k_cache && dst->v_cache,
-                 CDSP_ERR_INVALID, "bad decode target");
-    CDSP_REQUIRE(dst->n_table * dst->block_size >= ci.C + ci.L, CDSP_ERR_CAPACITY,
-                 "block table covers %lld positions, chunk ends at %lld",
-                 static_cast<long long>(dst->n_table * dst->block_size), static_cast<long long>(ci.C + ci.L));
+    CDSP_CHECK_STATUS(check_decode_target(dst, k, ci));
     PagedArgs a;
     std::memset(&a, 0, sizeof(a));
     a.k = k->ptr;
@@ -1152,7 +1202,6 @@ cdsp_status cdsp_kv_transfer_to_decode(const cdsp_tensor* k, const cdsp_tensor* 
     a.n_table = dst->n_table;
     a.block_table = dst->block_table;
     for (int t = 0; t < dst->tp; ++t) {
-        CDSP_REQUIRE(dst->k_cache[t] && dst->v_cache[t], CDSP_ERR_INVALID, "NULL cache pointer for tp rank %d", t);
         a.k_cache[t] = dst->k_cache[t];
         a.v_cache[t] = dst->v_cache[t];
     }
