@@ -1,0 +1,6 @@
+O=gpurun_out/${TAG:-r4s}; mkdir -p $O
+timeout 300 python tools/sanitize_cases.py > $O/plain.log 2>&1; echo "rc=$?" >> $O/plain.log
+for t in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $t --print-limit 20 python tools/sanitize_cases.py > $O/$t.log 2>&1; echo "rc=$?" >> $O/$t.log
+done
+tail -n 4 $O/*.log

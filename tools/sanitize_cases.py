@@ -72,7 +72,31 @@ vc = [torch.zeros_like(x) for x in kc]
 tgt = api.DecodeTarget(kc, vc, B, bt)
 api.kv_transfer_to_decode(k, k, api.SpGroup(comm, plan, 0), tgt)
 qd = torch.randn(1, 2, 128, device=dev).to(torch.bfloat16)
-api.decode_attention(qd, tgt, 0, 1, 256)
+api.decode_attention(qd, tgt, 0, 1, 256)   # TMA-fed kernel (B >= 16), slice merge over its splits
+api.decode_attention(qd, tgt, 0, 1, 250)   # ragged last page (V rows past the range zeroed)
+torch.cuda.synchronize()
+comm.close()
+# decode with 8-token pages (cp.async kernel) and in fp32 (FFMA kernel)
+for dt, B8 in ((torch.bfloat16, 8), (torch.float32, 16)):
+    plan = api.Plan([(512, [0])])
+    comm = api.Comm(0, 1, 0, 512, 1, 128, dt)
+    k = torch.randn(512, 1, 128, device=dev).to(dt)
+    bt = block_table(512 // B8, 512 // B8 + 4, seed=5).to(dev)
+    kc = [torch.zeros(512 // B8 + 4, B8, 1, 128, dtype=dt, device=dev)]
+    vc = [torch.zeros_like(kc[0])]
+    tgt = api.DecodeTarget(kc, vc, B8, bt)
+    api.kv_transfer_to_decode(k, k, api.SpGroup(comm, plan, 0), tgt)
+    api.decode_attention(torch.randn(1, 4, 128, device=dev).to(dt), tgt, 0, 1, 509)
+    torch.cuda.synchronize()
+    comm.close()
+# prefill + transfer in one call (scatter on the communicator's transfer stream)
+plan = api.Plan([(256, [0])])
+comm = api.Comm(0, 1, 0, 256, 2, 128, torch.bfloat16)
+q, k, v = (t.to(dev) for t in qkv(256, 4, 2, 128, torch.bfloat16, seed=4))
+bt = block_table(16, 20, seed=2).to(dev)
+kc = [torch.zeros(20, 16, 1, 128, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+vc = [torch.zeros_like(x) for x in kc]
+api.prefill_chunk_transfer(q, k, v, comm.kvstore(), api.SpGroup(comm, plan, 0), api.DecodeTarget(kc, vc, 16, bt))
 torch.cuda.synchronize()
 comm.close()
 print("sanitize cases done")
