@@ -149,3 +149,50 @@ def test_prefill_transfer_two_chunks_with_history():
                                   rows=rows)
     assert_out_close(out.float().cpu().numpy()[rows], o_ref, True, "two chunks")
     comm.close()
+
+
+def test_prefill_transfer_loopback_ring():
+    """SP = 2 then SP = 4 chunks on loopback instances: every rank's call transfers its zigzag
+    shard (the group executes on the last rank's call; each rank's scatter only reads its own
+    k / v): the caches equal the oracle writer's over the whole prompt, the outputs the oracle's."""
+    from paper_2511_06247_b200.driver import make_loopback_comms
+    Hq, Hkv, D, tp, B = 8, 4, 128, 4, 16
+    plan_list = [(1024, [0, 1]), (2048, [0, 1, 2, 3])]
+    N = sum(L for L, _ in plan_list)
+    q, k, v = qkv(N, Hq, Hkv, D, torch.bfloat16, seed=21)
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    plan = api.Plan(plan_list)
+    comms = make_loopback_comms(plan, Hkv, D, torch.bfloat16, Hq=Hq)
+    n_logical = N // B
+    num_blocks = n_logical + 8
+    bt = block_table(n_logical, num_blocks, seed=8)
+    kc, vc = _caches(num_blocks, B, Hkv // tp, D, tp)
+    dst = api.DecodeTarget(kc, vc, B, bt.cuda())
+    out = torch.empty_like(qd)
+    for c, (L, ranks) in enumerate(plan_list):
+        C = plan.chunk_start(c)
+        s = len(ranks)
+        res = []
+        for r, inst in enumerate(ranks):
+            qs, ks, vs = (api.zigzag_gather(t[C:C + L].contiguous(), s, r) for t in (qd, kd, vd))
+            o = torch.empty_like(qs)
+            api.prefill_chunk_transfer(qs, ks, vs, comms[inst].kvstore(), api.SpGroup(comms[inst], plan, c), dst,
+                                       0.0, o)
+            res.append((qs, ks, vs, o))
+        torch.cuda.synchronize()
+        part = torch.empty(L, Hq, D, dtype=torch.bfloat16, device="cuda")
+        for r in range(s):
+            api.zigzag_scatter(res[r][3], s, r, part)
+        out[C:C + L] = part
+        for inst in ranks:
+            assert api.kv_transfer_errors(comms[inst]) == 0
+    torch.cuda.synchronize()
+    ok, ov = _expect(k, v, np.arange(N), tp, B, bt.numpy(), num_blocks, Hkv // tp, D)
+    for t in range(tp):
+        assert np.array_equal(_u16(kc[t]), ok[t]) and np.array_equal(_u16(vc[t]), ov[t])
+    rows = sample_rows(N, 64, seed=4, edges=[0, 1023, 1024, N - 1]).numpy()
+    o_ref, _ = oracle.causal_rows(q.float().numpy(), k.float().numpy(), v.float().numpy(), 1.0 / math.sqrt(D),
+                                  rows=rows)
+    assert_out_close(out.float().cpu().numpy()[rows], o_ref, True, str(plan_list))
+    for cm in comms:
+        cm.close()
