@@ -144,6 +144,28 @@ def test_bench_torchrun_two_ranks_one_gpu():
     assert d["gpu_launches"] == 2 * 9
 
 
+def test_bench_torchrun_eight_ranks_one_gpu():
+    """bench.py at N = 8 (the SCALE run's largest size): eight processes, an SP = 8 ring of
+    CUDA-IPC stores, device peer barriers and copy-engine pulls, max-over-ranks timing — all
+    pinned to GPU 0 (functional check only: the ranks time-slice one GPU)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CDSP_BENCH_DEVICE="0", CUDA_DEVICE_MAX_CONNECTIONS="32")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "8",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+           "--gpus", "8", "--steps", "2", "--warmup", "1", "--no-e2e"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 8 and d["config"]["sp"] == 8 and d["value"] > 0
+    assert d["ring"]["pulls_per_step"] == 7 and d["ring"]["pull_gbs"] > 0
+    assert d["roofline"]["launches_timed"] == 2 and d["roofline"]["traffic"] is not None
+
+
 def test_bench_weak_is_configs4_shape():
     """--weak: GQA 32/8 with 64K tokens per GPU (at N = 8 this is configs[4]'s 512K prompt)."""
     import json
