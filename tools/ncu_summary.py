@@ -31,12 +31,17 @@ def launches(path, out):
         name = r[ik].split("(")[0].replace("void ", "").strip()
         per[name].append(ns)
     total = sum(sum(v) for v in per.values())
-    lines = ["| kernel | launches | total ms | avg us | share |", "|---|---:|---:|---:|---:|"]
+    ours = {k: v for k, v in per.items() if k.startswith("cdsp::") or "attn" in k or "decode" in k}
+    t_ours = sum(sum(v) for v in ours.values())
+    lines = ["| kernel | launches | total ms | avg us | share of all | share of the library's |",
+             "|---|---:|---:|---:|---:|---:|"]
     for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
-        lines.append(f"| `{k}` | {len(v)} | {sum(v) / 1e6:.3f} | {sum(v) / len(v) / 1e3:.1f} | {sum(v) / total:.1%} |")
+        own = f"{sum(v) / t_ours:.1%}" if k in ours and t_ours else "— (torch: input setup)"
+        lines.append(f"| `{k}` | {len(v)} | {sum(v) / 1e6:.3f} | {sum(v) / len(v) / 1e3:.1f} | {sum(v) / total:.1%} | {own} |")
     open(out, "w").write(
         f"# ncu launch list (gpu__time_duration.sum, --clock-control none)\n\nSource: `{os.path.basename(path)}`. "
-        "Per-launch times under ncu are cold-cache and serialised: compare SHARES, not absolutes.\n\n"
+        "Per-launch times under ncu are cold-cache and serialised: compare SHARES, not absolutes. "
+        "torch kernels are the seeded input generation before the timed region.\n\n"
         + "\n".join(lines) + "\n")
     print("\n".join(lines))
 
