@@ -1,4 +1,7 @@
-O=gpurun_out/${TAG:-r4final}; mkdir -p $O
+#!/bin/bash
+# One gpurun call: build, every GPU test, smoke, the default bench line and its ncu launch list
+# (outputs under gpurun_out/$TAG).
+O=gpurun_out/${TAG:-validate}; mkdir -p $O
 python paper_2511_06247_b200/build.py --force > $O/build.log 2>&1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
 timeout 2000 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log
