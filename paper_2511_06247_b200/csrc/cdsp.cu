@@ -397,6 +397,55 @@ cdsp_status ring_launches(cdsp_comm c, const ChunkInfo& ci, int r, RingLaunches*
         acc_bytes += bytes;
     }
     out->first[out->n] = ci.s;
+    // Pull pacing (flag-gated rings: every peer on another GPU, or CDSP_RING_GATE_FLAGS).  Every
+    // unit of one fused launch walks all the blocks, so its first wave of units cannot finish
+    // before the last pull has landed: T_fused ~ T_pull + T_compute (1 - 1 / waves).  When the
+    // pulls are long against the compute (a short chunk at s = 8), launches of g blocks — each
+    // waiting for its own blocks' pulls, merged through the fp32 accumulators, ~4.4% of T_compute
+    // per extra launch (s = 8 stepwise vs fused, blocks resident) — finish earlier.  The model's
+    // rates: CDSP_RING_LINK_GBS (pull, default 700) and CDSP_RING_TFLOPS (attention, default 1200).
+    bool remote_all = true;
+    for (int k = 1; k < ci.s; ++k)
+        if (!c->peer_remote[ci.ranks[(r - k + ci.s) % ci.s]]) remote_all = false;
+    const bool flags = (c->ring_opts & CDSP_RING_GATE_FLAGS) || (remote_all && !(c->ring_opts & CDSP_RING_GATE_EVENTS));
+    if (fused && acc_ok && flags && out->n == 1 && ci.s > 2) {
+        static const double link = (getenv("CDSP_RING_LINK_GBS") ? atof(getenv("CDSP_RING_LINK_GBS")) : 700.0) * 1e9;
+        static const double rate = (getenv("CDSP_RING_TFLOPS") ? atof(getenv("CDSP_RING_TFLOPS")) : 1200.0) * 1e12;
+        double arrive[kMaxWorld + 1] = {}, comp[kMaxWorld] = {}, t_c = 0.0;
+        for (int k = 0; k < ci.s; ++k) {
+            const int src = (r - k + ci.s) % ci.s;
+            const double rows = static_cast<double>(ci.hist[src]) + 2.0 * ci.m;
+            // visible pairs: history rows fully, the shard's 2m rows about half (causal / zigzag)
+            const double pairs = 2.0 * ci.m * (static_cast<double>(ci.hist[src]) + 0.5 * 2.0 * ci.m);
+            comp[k] = 4.0 * c->D * Hq * pairs / rate;
+            t_c += comp[k];
+            arrive[k] = k == 0 ? 0.0 : arrive[k - 1] + 2.0 * rows * static_cast<double>(c->row_bytes) / link;
+        }
+        int sms = 148;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess || sms < 2) sms = 148;
+        const double units = std::ceil(2.0 * ci.m / 256.0) * Hq, waves = std::max(1.0, units / (sms / 2));
+        const double t_fused = std::max(arrive[ci.s - 1] + t_c * (1.0 - 1.0 / waves), t_c);
+        int best_g = ci.s;
+        double best_t = t_fused;
+        for (int g = 1; g < ci.s; ++g) {
+            double t = 0.0;
+            for (int k0 = 0, i = 0; k0 < ci.s; k0 += g, ++i) {
+                const int k1 = std::min(ci.s, k0 + g);
+                double cl = 0.0;
+                for (int k = k0; k < k1; ++k) cl += comp[k];
+                t = std::max(t, arrive[k1 - 1]) + cl + (i > 0 ? 0.044 * t_c : 0.0);
+            }
+            if (t < 0.9 * best_t) {
+                best_t = t;
+                best_g = g;
+            }
+        }
+        if (best_g < ci.s) {
+            out->n = 0;
+            for (int k0 = 0; k0 < ci.s; k0 += best_g) out->first[out->n++] = k0;
+            out->first[out->n] = ci.s;
+        }
+    }
     return CDSP_OK;
 }
 

@@ -227,3 +227,51 @@ def test_m2_shape_sp8_fused_and_flags_sampled():
         for c in comms:
             c.check()
             c.close()
+
+
+_PACING_CODE = """
+import sys, math, json
+sys.path.insert(0, 'tests')
+import numpy as np, torch, oracle
+from tolerances import assert_out_close
+from cdsp_inputs import qkv, sample_rows
+from paper_2511_06247_b200 import api
+from paper_2511_06247_b200.driver import make_loopback_comms, run_plan_loopback
+N, Hq, Hkv, D = 40960, 32, 8, 128
+plan = api.Plan([(N, list(range(8)))])
+q, k, v = qkv(N, Hq, Hkv, D, torch.bfloat16, seed=5)
+comms = make_loopback_comms(plan, Hkv, D, torch.bfloat16, Hq=Hq)
+for c in comms:
+    c.set_ring_options(api.RING_GATE_FLAGS)
+    c.profile(True)
+out, lse = run_plan_loopback(q.cuda(), k.cuda(), v.cuda(), plan, comms=comms)
+torch.cuda.synchronize()
+n = max(c.profile_read()[1] for c in comms)
+rows = sample_rows(N, 24, seed=1, edges=[0, N - 1]).numpy()
+o_ref, l_ref = oracle.causal_rows(q.float().numpy(), k.float().numpy(), v.float().numpy(), 1.0 / math.sqrt(D), rows=rows)
+assert_out_close(out.float().cpu().numpy()[rows], o_ref, True, 'paced ring')
+assert np.abs(lse.cpu().numpy()[:, rows] - l_ref).max() <= 1e-3
+print(json.dumps({'launches_per_rank': n}))
+"""
+
+
+@pytest.mark.parametrize("link_gbs,grouped", [(None, False), ("150", True)])
+def test_ring_pull_pacing(link_gbs, grouped):
+    """Flag-gated SP = 8 ring of a 40K-token chunk (8.6 waves of units per rank): at the default
+    link rate the pulls are short against the compute and the ring stays ONE fused launch; at
+    150 GB/s (CDSP_RING_LINK_GBS) the first wave of a fused launch would wait out most of the
+    pulls, so the blocks are grouped into several launches merged in fp32 — either way the
+    result matches the oracle."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("CDSP_RING_LINK_GBS", None)
+    if link_gbs:
+        env["CDSP_RING_LINK_GBS"] = link_gbs
+    out = subprocess.run([sys.executable, "-c", _PACING_CODE], cwd=root, capture_output=True, text=True, timeout=900,
+                         env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    n = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])["launches_per_rank"]
+    assert (n > 1) == grouped, n
