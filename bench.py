@@ -481,7 +481,7 @@ def main():
     achieved = per_launch_flops / (attn_avg * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_attn_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and abs(attn_n / args.steps - 1.0) < 1e-9:  # keyed captures are of one-launch rings
         try:
             traffic = json.load(open(prof)).get(f"L{L}_H{Hq}_KV{Hkv}_s{s}")
         except Exception:
