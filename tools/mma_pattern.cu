@@ -76,14 +76,17 @@ __global__ void __launch_bounds__(64, 1) pattern(int tiles, const uint8_t* gsrc,
         if (!(MODE & 32)) __syncwarp();
         const unsigned long long t0 = clock64();
         for (int t = 0; t < tiles; ++t) {
-            const uint32_t sb = 128 + 128 * (t % 3);
+            // bit 8: the CDSP_HALFSLOT placement (S in 64-column halves {0,1},{3,4},{1,2},{4,5}, P in 0/3/2/5)
+            const int hs_h[4] = {0, 3, 1, 4}, hs_p[4] = {0, 3, 2, 5};
+            const uint32_t sb = (MODE & 256) ? 128 + 64 * hs_h[t % 4] : 128 + 128 * (t % 3);
+            const uint32_t sp = (MODE & 256) ? 128 + 64 * hs_p[t % 4] : sb;
             mbar_wait(smem_u32(&bars[3]), 0);
             mbar_wait(smem_u32(&bars[3]), 0);
             if (!(MODE & 64)) tc_fence_after();
             if ((((MODE & 32) != 0) || elect_one())) {
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    mma_ts(tmem, tmem + sb + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4), idesc_pv, 1u);
+                    mma_ts(tmem, tmem + sp + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4), idesc_pv, 1u);
                 mma_commit(smem_u32(&bars[1]));
                 if (!(MODE & 128)) mma_commit(smem_u32(&bars[1]));
             }
@@ -113,7 +116,10 @@ __global__ void __launch_bounds__(64, 1) pattern(int tiles, const uint8_t* gsrc,
         const uint64_t dv = umma_desc_sw128(sV, kBox, 1024);
         const unsigned long long t0 = clock64();
         for (int t = 0; t < tiles; ++t) {
-            const uint32_t sb = 128 + 128 * (t % 3);
+            // bit 8: the CDSP_HALFSLOT placement (S in 64-column halves {0,1},{3,4},{1,2},{4,5}, P in 0/3/2/5)
+            const int hs_h[4] = {0, 3, 1, 4}, hs_p[4] = {0, 3, 2, 5};
+            const uint32_t sb = (MODE & 256) ? 128 + 64 * hs_h[t % 4] : 128 + 128 * (t % 3);
+            const uint32_t sp = (MODE & 256) ? 128 + 64 * hs_p[t % 4] : sb;
             if (MODE & 1) {
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
@@ -130,7 +136,7 @@ __global__ void __launch_bounds__(64, 1) pattern(int tiles, const uint8_t* gsrc,
             if (MODE & 2) {
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    mma_ts(tmem, tmem + sb + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4), idesc_pv, 1u);
+                    mma_ts(tmem, tmem + sp + kk * 8, dv + static_cast<uint64_t>((kk * 16 * 128) >> 4), idesc_pv, 1u);
                 mma_commit(smem_u32(&bars[1]));
                 if (delay) {
                     const unsigned long long d0 = clock64();
@@ -196,6 +202,8 @@ int main() {
     run<16 + 64>("warp loop, no tcgen05 fence", g, d);
     run<16 + 128>("warp loop, 2 commits / tile", g, d);
     run<16 + 32 + 64 + 128>("lane-0, no fence, 2 commits", g, d);
+    run<3 + 256>("S + PV, half-slot placement", g, d);
+    run<11 + 256>("S + PV, half-slot placement, random data", g, d);
     run<3>("S + PV, issuer +50 clk per group", g, d, 50);
     run<3>("S + PV, issuer +100 clk per group", g, d, 100);
     run<3>("S + PV, issuer +200 clk per group", g, d, 200);
