@@ -106,6 +106,10 @@
 #define CDSP_COLSPLIT 0
 #endif
 
+#ifndef CDSP_DBG_NO_KV  // debug probe (timing only, results garbage): 1 skip K tile loads, 2 skip V, 3 both
+#define CDSP_DBG_NO_KV 0
+#endif
+
 #ifndef CDSP_KV_POLICY  // L2 policy of the K / V tile loads: 0 evict_last, 1 evict_normal, 2 evict_first
 #define CDSP_KV_POLICY 0
 #endif
@@ -1068,7 +1072,9 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
                 // stage st last held tile it - 3: free once S(it - 3) is done (in both CTAs)
                 if (it >= L::KST) mbar_wait_backoff(bar(L::B_SF + st), ((it - L::KST) / L::KST) & 1);
                 if (lane == 0) KTRACE(15, it);
-                if (elect_one()) {
+                if (CDSP_DBG_NO_KV & 1) {  // debug probe: no K traffic (results garbage)
+                    if (leader && lane == 0) mbar_arrive(bar(L::B_KF + st));
+                } else if (elect_one()) {
                     if constexpr (PAIR) {
                         // this CTA's 64 keys of the tile, both d halves
                         if (leader) mbar_expect_tx(bar(L::B_KF + st), 2 * L::KTILE);
@@ -1125,7 +1131,9 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
                 const int st = it % L::VST;
                 if (it >= L::VST) mbar_wait_backoff(bar(L::B_VE + st), ((it - L::VST) / L::VST) & 1);
                 if (lane == 0) KTRACE(14, it);
-                if (elect_one()) {
+                if (CDSP_DBG_NO_KV & 2) {  // debug probe: no V traffic (results garbage)
+                    if (leader && lane == 0) mbar_arrive(bar(L::B_VF + st));
+                } else if (elect_one()) {
                     if constexpr (PAIR) {  // all 128 keys, this CTA's 64 d columns
                         if (leader) mbar_expect_tx(bar(L::B_VF + st), 2 * L::VTILE);
                         tma_load_3d_2sm(sV + st * L::VTILE, &tm.v[blk], lbar(L::B_VF + st), crank * 64, kvh, j * BN,
