@@ -99,13 +99,6 @@
 #define ARRIVERS (CDSP_ALL_LANE_ARRIVE ? 32 : 1)
 #define ARRIVE_LANE (CDSP_ALL_LANE_ARRIVE || lane == 0)
 
-// CDSP_COLSPLIT: both softmax groups work on EVERY tile, group g on keys [64 g, 64 g + 64) of its
-// rows; the two halves' row maxima meet once per tile (one named barrier), so a group's per-tile
-// chain is half as long and no row max travels from tile to tile between groups (PAIR, HD = 128).
-#ifndef CDSP_COLSPLIT
-#define CDSP_COLSPLIT 0
-#endif
-
 #ifndef CDSP_DBG_NO_KV  // debug probe (timing only, results garbage): 1 skip K tile loads, 2 skip V, 3 both
 #define CDSP_DBG_NO_KV 0
 #endif
@@ -183,8 +176,8 @@ struct Layout {
     // PAIR: bf16 output staging, 128 rows x 64 columns (128B-swizzled) per softmax group, TMA-stored
     static constexpr int STG = PAIR ? 2 * BM * 128 : 0;
     static constexpr int OFF_STG = OFF_V + VST * VTILE;
-    static constexpr int OFF_M = OFF_STG + STG;            // running row max m(n): [2][NG][128] float (COLSPLIT: per-tile partial maxima by tile parity)
-    static constexpr int OFF_L = OFF_M + 2 * NG * BM * 4;  // epilogue hand-over (m_used, l): [2 unit parity][NG][128] float2
+    static constexpr int OFF_M = OFF_STG + STG;            // running row max m(n): [NG (tile mod NG)][128] float
+    static constexpr int OFF_L = OFF_M + NG * BM * 4;      // epilogue hand-over (m_used, l): [2 unit parity][NG][128] float2
     static constexpr int OFF_QP = OFF_L + 2 * NG * BM * 8;  // query position per row: [2 unit buffer][128] int64
     static constexpr int OFF_BAR = OFF_QP + 2 * BM * 8;
     // Local: u_full[2] (unit buffer published), u_empty[2] (read by every consumer), q_empty[2],
@@ -664,7 +657,6 @@ template <int HD, bool PAIR>
 __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
     attn_tc_kernel(const __grid_constant__ TcMaps tm, const __grid_constant__ TcParams p) {
     using L = Layout<HD, PAIR>;
-    constexpr bool CS = CDSP_COLSPLIT && PAIR && HD == 128 && NG == 2 && !CDSP_EPI_WARPS;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
     const uint32_t raw_addr = smem_u32(smem_raw);
@@ -909,10 +901,10 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
             }
             for (int b = 0; b < NSB; ++b) {
                 mbar_init(bar(L::B_SF + b), 1);
-                mbar_init(bar(L::B_PF + b), (CS ? 8 : 4) * CL);  // the softmax warps of the tile (x CTAs of a pair)
+                mbar_init(bar(L::B_PF + b), 4 * CL);  // the softmax warps of the tile (x CTAs of a pair)
             }
             mbar_init(bar(L::B_OF), 1);
-            mbar_init(bar(L::B_OE), (CS ? 8 : 4) * CL);  // the finishing group's warps (x CTAs of a pair)
+            mbar_init(bar(L::B_OE), 4 * CL);  // the finishing group's 4 warps (x CTAs of a pair)
             for (int i = 0; i < 2; ++i) {
                 // row statistics hand-over: every softmax group to the epilogue group (CDSP_EPI_WARPS),
                 // else the other groups to the finishing one
@@ -1239,135 +1231,6 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
             }
             gn0 += N;
             ++n_units_done;
-        }
-    } else if (CS && warp < 4 * NG) {
-        // ========= column-split softmax (CDSP_COLSPLIT): group g = keys [64 g, 64 g + 64) of every
-        // tile; thread = one query row.  Per tile: both halves' S into registers, the half-row
-        // maxima exchanged through shared memory (one 256-thread barrier), the same lazy m in both
-        // groups, each group's own row-sum half and O half (rescale, epilogue) =========
-        const int g = warp >> 2;
-        const int quad = warp & 3;
-        const int r = quad * 32 + lane;
-        const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-        const uint32_t tO = tmem + lane_off + COL_O;
-        float* mxs = reinterpret_cast<float*>(smem + L::OFF_M);  // [2 tile parity][NG][BM]
-        volatile int* role_sh = reinterpret_cast<volatile int*>(smem + L::OFF_ROLE);
-        const float sl2 = p.scale_log2;
-        int gn0 = 0, n_units_done = 0;
-        for (int i = 0;; ++i) {
-            const int ub = i & 1;
-            mbar_wait(bar(L::B_UF + ub), (i >> 1) & 1);
-            const UnitInfo u = uinfo[ub];
-            if (u.x < 0) break;
-            const int N = u.n_used;
-            int head;
-            int64_t row0;
-            unit_rows(u.x, crank, head, row0);
-            const int64_t row = row0 + r;
-            const bool row_ok = row < nq;
-            const uint16_t* list = reinterpret_cast<const uint16_t*>(smem + L::OFF_SCHED) + ub * L::LISTMAX;
-            const int64_t* qp = reinterpret_cast<const int64_t*>(smem + L::OFF_QP) + ub * BM;
-            float m = -INFINITY, m_used = -INFINITY;
-            float2 lacc = make_float2(0.f, 0.f);
-            for (int n = 0; n < N; ++n) {
-                const int gn = gn0 + n;
-                const uint32_t e = list[n];
-                const int j = static_cast<int>(e & ~kPartialBit);
-                const bool partial = (e & kPartialBit) != 0;
-                const int b = gn % NSB;
-                const uint32_t tS = tmem + lane_off + col_s(b);
-                mbar_wait(bar(L::B_SF + b), (gn / NSB) & 1);
-                tc_fence_after();
-                uint32_t s[64];
-                tmem_ld32p(tS + 64 * g, s);
-                tmem_ld32p(tS + 64 * g + 32, s + 32);
-                tc_wait_ld();
-                reg_tie32(s);
-                reg_tie32(s + 32);
-                if (partial) mask_tile<2>(s, segs, toff, j, qp[r], 64 * g);
-                float mx = max64(s) * sl2;
-                mxs[((gn & 1) * NG + g) * BM + r] = mx;
-                // both halves' maxima are in, and both halves' S are in registers (P may now be
-                // written over S columns 0-63 by either group)
-                named_bar_sync(2, NG * BM);
-                mx = fmaxf(mx, mxs[((gn & 1) * NG + (1 - g)) * BM + r]);
-                const bool need = mx > m + 8.0f;
-                const float m_prev = m;
-                if (need) m = mx;
-                if (n > 0 && __any_sync(0xFFFFFFFFu, need)) {  // rescale this group's O half after PV(n-1)
-                    mbar_wait(bar(L::B_VE + (gn - 1) % L::VST), ((gn - 1) / L::VST) & 1);
-                    tc_fence_after();
-                    const float alpha = need ? ex2(m_prev - m) : 1.0f;
-#pragma unroll 1
-                    for (int c = 0; c < 4; ++c) {
-                        uint32_t o[16];
-                        tmem_ld16(tO + 64 * g + 16 * c, o);
-                        tc_wait_ld();
-                        reg_tie16(o);
-#pragma unroll
-                        for (int q = 0; q < 16; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha);
-                        tmem_st16(tO + 64 * g + 16 * c, o);
-                    }
-                }
-                reg_tie32(s);
-                reg_tie32(s + 32);
-                if (m != m_used) {
-                    const float beta = ex2(m_used - m);
-                    lacc.x *= beta;
-                    lacc.y *= beta;
-                    m_used = m;
-                }
-                const float m_use = (m == -INFINITY) ? 0.f : m;
-                const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m_use, -m_use);
-                exp32_store(s, sc, nm, lacc, tS + 32 * g);  // keys 64 g .. 64 g + 63 -> P columns 32 g ..
-                exp32_store(s + 32, sc, nm, lacc, tS + 32 * g + 16);
-                tc_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) arrive_leader(L::B_PF + b);
-            }
-            __syncwarp();
-            if (ARRIVE_LANE) mbar_arrive(bar(L::B_UE + ub));  // done with the unit's schedule / positions
-            int part = -1, ux = 0;
-            if (p.split) {
-                int xx = u.x, h2, b0, b1;
-                int64_t r2;
-                asm volatile("" : "+r"(xx));
-                unit_map(xx, crank, h2, r2, part, ux, b0, b1);
-            }
-            if (N == 0 && p.mode == CDSP_ATTN_MID && part < 0) continue;  // merging an empty block is the identity
-            float l = 0.f;
-            if (N > 0) {  // the row sum: both halves, relative to the same max
-                float* lsh = reinterpret_cast<float*>(smem + L::OFF_L) + (n_units_done & 1) * NG * BM;
-                lsh[g * BM + r] = lacc.x + lacc.y;
-                named_bar_sync(13, NG * BM);
-                if (m != -INFINITY) l = lsh[r] + lsh[BM + r];
-                gn0 += N;
-                ++n_units_done;
-            }
-            asm volatile("griddepcontrol.wait;" ::: "memory");
-            bool split_first = false;
-            int* scnt = nullptr;
-            if (part >= 0) {
-                scnt = p.split_cnt + 2 * (2 * ux + crank);
-                split_first = split_role(scnt, role_sh, 12, NG * BM, g == 0 && r == 0) != 0;
-            }
-            const int stage_bar = 8 + g;
-            const unsigned stage_lead = static_cast<unsigned>(g * BM);
-            if (part < 0)
-                run_epilogue(IntC<2>{}, IntC<2>{}, head, row0, row, row_ok, r, quad, N, l, m, n_units_done, tO,
-                             stage_bar, stage_lead, g, g + 1, false, g == 0);
-            else if (split_first)
-                run_epilogue(IntC<0>{}, IntC<1>{}, head, row0, row, row_ok, r, quad, N, l, m, n_units_done, tO,
-                             stage_bar, stage_lead, g, g + 1, false, g == 0);
-            else
-                run_epilogue(IntC<1>{}, IntC<0>{}, head, row0, row, row_ok, r, quad, N, l, m, n_units_done, tO,
-                             stage_bar, stage_lead, g, g + 1, false, g == 0);
-            if (split_first) {  // publish the partial (both groups' stores, then one release)
-                __threadfence();
-                named_bar_sync(12, NG * BM);
-                if (g == 0 && r == 0) asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(scnt + 1), "r"(1) : "memory");
-            }
         }
     } else if (warp < 4 * NG) {
         // ========= softmax group g (tiles gn = g, g+2, ... over all units): thread = one query row =========
