@@ -1056,8 +1056,15 @@ cdsp_status cdsp_prefill_chunk_transfer(const cdsp_tensor* q, const cdsp_tensor*
                                         cdsp_kvstore* prev_kv, const cdsp_sp_group* sp_group, float softmax_scale,
                                         cdsp_tensor* out, float* lse, const cdsp_decode_target* dst,
                                         void* cuda_stream) {
-    CDSP_REQUIRE(dst != nullptr && sp_group && sp_group->comm, CDSP_ERR_INVALID, "NULL decode target / group");
+    CDSP_REQUIRE(dst != nullptr && sp_group && sp_group->comm && sp_group->plan, CDSP_ERR_INVALID,
+                 "NULL decode target / group");
     cdsp_comm c = sp_group->comm;
+    {  // the transfer's own checks first: a refused call enqueues nothing
+        CDSP_CHECK_STATUS(check_tensor(k, "k"));
+        ChunkInfo ci;
+        CDSP_CHECK_STATUS(plan_chunk_info(sp_group->plan, sp_group->chunk, &ci));
+        CDSP_CHECK_STATUS(check_decode_target(dst, k, ci));
+    }
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     CDSP_CUDA(cudaEventRecord(c->ev_x0, st));  // this call's k / v are ready
     // the attention first: its persistent grid takes every SM; the scatter, on the comm's

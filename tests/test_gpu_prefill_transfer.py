@@ -196,3 +196,24 @@ def test_prefill_transfer_loopback_ring():
     assert_out_close(out.float().cpu().numpy()[rows], o_ref, True, str(plan_list))
     for cm in comms:
         cm.close()
+
+
+def test_prefill_transfer_refuses_bad_target_before_any_work():
+    """A decode target the transfer refuses (Hkv not divisible by tp) fails the call before
+    anything is enqueued: the output keeps its sentinel and the store stays empty."""
+    L, Hq, Hkv, D = 512, 4, 4, 128
+    q, k, v = (t.cuda() for t in qkv(L, Hq, Hkv, D, torch.bfloat16, seed=2))
+    plan = api.Plan([(L, [0])])
+    comm = api.Comm(0, 1, 0, L, Hkv, D, torch.bfloat16)
+    caches = [torch.zeros(40, 16, 1, D, dtype=torch.bfloat16, device="cuda") for _ in range(3)]
+    dst = api.DecodeTarget(caches, caches, 16, torch.arange(40, dtype=torch.int32, device="cuda"))
+    out = torch.full_like(q, 7.0)
+    with pytest.raises(api.CdspError) as e:
+        api.prefill_chunk_transfer(q, k, v, comm.kvstore(), api.SpGroup(comm, plan, 0), dst, 0.0, out)
+    assert e.value.status == 8
+    torch.cuda.synchronize()
+    assert bool((out == 7.0).all())
+    # the store was not appended: the same chunk can still be prefilled
+    api.prefill_chunk(q, k, v, comm.kvstore(), api.SpGroup(comm, plan, 0), 0.0, out)
+    torch.cuda.synchronize()
+    comm.close()
