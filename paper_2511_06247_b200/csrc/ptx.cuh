@@ -57,9 +57,13 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parit
     return ok != 0;
 }
 // Wait for the phase with parity `parity` to complete.  A watchdog traps after ~4 s so a
-// protocol bug fails the launch instead of hanging the GPU.
+// protocol bug fails the launch instead of hanging the GPU.  CDSP_WAIT_SLEEP=1: try_wait with a
+// suspend-time hint (the waiting warp sleeps until the phase completes); 0 (default): plain
+// try_wait polling — same-box A/B: attention s = 1 1366 -> 1386 TF/s mean of 4, per-GPU ring
+// s = 8 1252-1275 -> 1284-1297, decode unchanged (the wake-up from a suspended wait lands on the
+// softmax / MMA hand-offs).
 #ifndef CDSP_WAIT_SLEEP
-#define CDSP_WAIT_SLEEP 1
+#define CDSP_WAIT_SLEEP 0
 #endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
