@@ -77,14 +77,14 @@ __global__ void __launch_bounds__(512, 1) exp_rate(int iters, const float* in, u
 }
 
 template <int MASK, bool PACKED>
-void run(const char* name, const float* in, uint32_t* out, unsigned long long* d) {
-    const int iters = 2000;
-    exp_rate<MASK, PACKED><<<148, 512>>>(iters, in, out, d);
-    exp_rate<MASK, PACKED><<<148, 512>>>(iters, in, out, d);
+void run(const char* name, const float* in, uint32_t* out, unsigned long long* d, int wps = 4) {
+    const int iters = 2000;  // wps: warps per SMSP (1: one warp's latency-bound stream, as a softmax group's)
+    exp_rate<MASK, PACKED><<<148, 128 * wps>>>(iters, in, out, d);
+    exp_rate<MASK, PACKED><<<148, 128 * wps>>>(iters, in, out, d);
     unsigned long long h;
     cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-    printf("%-40s %7.1f clk per 32-score block per SMSP (4 warps)  [%s]\n", name, double(h) / iters,
-           cudaGetErrorString(cudaGetLastError()));
+    printf("%-40s %7.1f clk per 32-score block per SMSP (%d warp%s)  [%s]\n", name, double(h) / iters, wps,
+           wps > 1 ? "s" : "", cudaGetErrorString(cudaGetLastError()));
 }
 
 int main() {
@@ -102,5 +102,10 @@ int main() {
     run<0xFF, true>("all FMA cubic, packed", in, out, d);
     run<0x00, false>("all MUFU, scalar FFMA/FADD", in, out, d);
     run<0x52, false>("3/8 FMA cubic, scalar", in, out, d);
+    for (int w = 1; w <= 4; w *= 2) {  // latency vs throughput of the kernel's 1/8 mix
+        run<0x02, true>("1/8 FMA cubic, packed", in, out, d, w);
+        run<0x00, true>("all MUFU, packed", in, out, d, w);
+        run<0x22, true>("1/4 FMA cubic, packed", in, out, d, w);
+    }
     return 0;
 }
