@@ -19,11 +19,13 @@
 //    arrivals land on the even CTA's barriers.  HD = 64 (and CDSP_ATTN_1SM=1) run the same
 //    code on one SM per unit (PAIR = false).
 //  * Persistent: one CTA per SM, work units (a pair of 128-row blocks x one head) claimed from
-//    an atomic counter, head-major and heaviest first; the producer warp publishes each unit's
-//    compacted list of used KV tiles one unit ahead (double-buffered u_full / u_empty).
-//  * 11 warps: 0-3 and 4-7 two softmax groups (one thread = one query row = one TMEM lane)
-//    taking alternate KV tiles; 8 unit scheduler + TMA producer of Q (2 buffers in PAIR) and K
-//    (3 stages); 9 TMA producer of V (3 stages in PAIR); 10 TMEM allocator + MMA issuer.
+//    an atomic counter, head-major and heaviest first; a scheduler warp publishes each unit's
+//    compacted list of used KV tiles and loads its Q (double-buffered u_full / u_empty), cued
+//    by the K producer a few tiles before the current unit's end.
+//  * 12 warps: 0-3 and 4-7 two softmax groups (one thread = one query row = one TMEM lane)
+//    taking alternate KV tiles; 8 TMA producer of K (3 stages); 9 TMA producer of V (3 stages
+//    in PAIR); 10 TMEM allocator + MMA issuer; 11 unit scheduler + TMA producer of Q (2
+//    buffers in PAIR).  3 warps per sub-partition x 168 registers.
 //  * TMEM (512 cols): O [0,128), S/P triple buffer [128,256) [256,384) [384,512); P (bf16) is
 //    written over its own S columns and is PV's A operand straight from TMEM.  MMA order
 //    S(0) S(1) S(2) | PV(0) S(3) | PV(1) S(4) | ...: scores run two tiles ahead.
@@ -70,11 +72,17 @@
 #define MMA_WAIT mbar_wait
 #endif
 
+// unit scheduler: the next unit is claimed when the K producer is this many tiles from the end of
+// the current one
+#ifndef CDSP_PREP_LEAD
+#define CDSP_PREP_LEAD 6
+#endif
+constexpr int kPrepLead = CDSP_PREP_LEAD;
 #ifndef CDSP_VST  // V shared-memory stages (K has one per S buffer)
 #define CDSP_VST 2
 #endif
 
-#ifndef CDSP_MAXNREG  // 11 warps: 3 per sub-partition x 168 regs x 32 lanes fills its 16K registers
+#ifndef CDSP_MAXNREG  // 12 warps: 3 per sub-partition x 168 regs x 32 lanes fills its 16K registers
 #define CDSP_MAXNREG 168
 #endif
 
@@ -137,10 +145,10 @@ constexpr int NG = CDSP_NGROUPS;
 #define CDSP_EPI_WARPS 0
 #endif
 constexpr int NEPI = CDSP_EPI_WARPS ? 4 : 0;
-// register redistribution (setmaxnreg) whenever the CTA outgrows 11 warps at 168 registers:
+// register redistribution (setmaxnreg) whenever the CTA outgrows 12 warps at 168 registers:
 // softmax / epilogue / producers+MMA+idle; 16 warps launched at 128 registers each
 #define CDSP_REGSPLIT (CDSP_EPI_WARPS || CDSP_NGROUPS > 2)
-constexpr int kThreads = 32 * (4 * NG + NEPI + 3 + (CDSP_REGSPLIT ? 1 : 0));  // softmax, epilogue, K / V producers, MMA (+ idle)
+constexpr int kThreads = 32 * (4 * NG + NEPI + 4);  // softmax, epilogue, K / V producers, MMA, scheduler
 static_assert(!CDSP_REGSPLIT || kThreads == 512, "register split assumes 16 warps");
 static_assert(NG == 2 || (NG == 3 && !CDSP_EPI_WARPS), "NG = 3 runs without the epilogue group");
 #define CDSP_SOFTMAX_REGS (NG == 3 ? 152 : 168)
@@ -154,7 +162,7 @@ constexpr int kMaxBlk = CDSP_MAX_SP;    // KV blocks one launch walks (a rank's 
 // roles are warpgroup-aligned (setmaxnreg acts per warpgroup): softmax 0..4NG-1, epilogue
 // 4NG..4NG+3 (TMEM quadrants 0..3), then K producer, V producer, MMA
 constexpr int W_EPI0 = 4 * NG;
-constexpr int W_K = 4 * NG + NEPI, W_V = W_K + 1, W_MMA = W_K + 2;
+constexpr int W_K = 4 * NG + NEPI, W_V = W_K + 1, W_MMA = W_K + 2, W_SCH = W_K + 3;
 
 // PAIR: 2-SM variant (HD = 128).  A CTA pair (cluster of 2) runs M = 256 MMAs (cta_group::2):
 // each CTA holds its own 128 query rows of Q and of S / P / O in its TMEM, and HALF of every
@@ -194,7 +202,7 @@ struct Layout {
     // tile, the Q buffer); v_empty[s] (PV(n) done) also tells a rescaling group that O is stable.
     static constexpr int B_UF = 0, B_UE = 2, B_QF = 4, B_QE = 6, B_KF = 8, B_VF = B_KF + KST, B_VE = B_VF + VST,
                          B_SF = B_VE + VST, B_PF = B_SF + NSB, B_OF = B_PF + NSB, B_OE = B_OF + 1, B_CF = B_OE + 1,
-                         B_CE = B_CF + 2, B_LF = B_CE + 2, B_LE = B_LF + 2, NBAR = B_LE + 2;
+                         B_CE = B_CF + 2, B_LF = B_CE + 2, B_LE = B_LF + 2, B_PR = B_LE + 2, NBAR = B_PR + 2;
     static_assert(KST == NSB, "K stages are released through s_full");
     static constexpr int OFF_TMEM_SLOT = OFF_BAR + NBAR * 8;
     static constexpr int OFF_CLAIM = OFF_TMEM_SLOT + 8;     // [2] next unit id (odd CTA of a pair)
@@ -886,7 +894,7 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
         if (lane == 0) {
             for (int i = 0; i < 2; ++i) {
                 mbar_init(bar(L::B_UF + i), ARRIVERS);  // the scheduler warp (its list / position writes)
-                mbar_init(bar(L::B_UE + i), ARRIVERS * (4 * NG + NEPI + 2));  // softmax, epilogue, V producer, MMA warps
+                mbar_init(bar(L::B_UE + i), ARRIVERS * (4 * NG + NEPI + 3));  // softmax, epilogue, K / V producers, MMA warps
                 mbar_init(bar(L::B_CF + i), 1);
                 mbar_init(bar(L::B_CE + i), 1);
             }
@@ -910,6 +918,7 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
                 // else the other groups to the finishing one
                 mbar_init(bar(L::B_LF + i), ARRIVERS * 4 * (CDSP_EPI_WARPS ? NG : NG - 1));
                 mbar_init(bar(L::B_LE + i), ARRIVERS * 4);
+                mbar_init(bar(L::B_PR + i), 1);  // the K producer is kPrepLead tiles from the unit's end
             }
             fence_barrier_init();
             tma_prefetch_desc(&tm.q);
@@ -943,27 +952,41 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
 #if CDSP_REGSPLIT
     if (warp >= W_K) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CDSP_PRODUCER_REGS) : "memory");  // producers, MMA issuer
 #endif
-    if (warp == W_K) {
-        // ======== unit scheduler + TMA producer of Q and K: for each unit, list its used KV
-        // tiles in order (empty ones skipped), publish the unit (u_full[i&1]) and stream its
-        // Q tile and K tiles (3 stages) ========
-        const uint64_t pol_kv = kv_policy();
+    if (warp == W_SCH) {
+        // ======== unit scheduler: claim each unit, list its used KV tiles in order (empty ones
+        // skipped), publish it (u_full[i&1]) as soon as every consumer (the K producer included)
+        // is done with the unit two back, and load its Q tile once the Q buffer is free.  Its own
+        // warp: list building and the claim round trip stay off the K stream ========
         const uint64_t pol_q = policy_evict_first();
         int x = static_cast<int>(blockIdx.x) / CL;
         int x_pre = 0;  // leader lane 0: the unit after x, claimed one unit ahead
         if (leader && lane == 0) x_pre = G + atomicAdd(p.claim, 1);
-        int it = 0;        // used tiles loaded so far (all units)
         int n_ne = 0;      // non-empty units so far
         int* claim_slot = reinterpret_cast<int*>(smem + L::OFF_CLAIM);
-        for (int i = 0;; ++i) {
+        // prepare unit i (its id in x): list, publish, Q; returns its tile count (-1: no more
+        // units) and its KV head in *kvh_out
+        auto prepare = [&](int i, int* kvh_out) -> int {
             const int ub = i & 1;
-            if constexpr (PAIR) {
-                if (!leader && i >= 1) {  // unit id from the even CTA (message i)
-                    const int s = (i - 1) & 1, use = (i - 1) >> 1;
-                    mbar_wait_acq_cluster(bar(L::B_CF + s), use & 1);  // pairs with the even CTA's release.cluster
-                    x = *reinterpret_cast<volatile int*>(claim_slot + s);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_remote(mapa_shared(bar(L::B_CE + s), 0));
+            if (i >= 1) {  // unit id: the even CTA claims one unit ahead and tells the odd CTA
+                x = __shfl_sync(0xFFFFFFFFu, x_pre, 0);
+                if (leader && lane == 0) {
+                    if (x < p.n_units) x_pre = G + atomicAdd(p.claim, 1);
+                    if constexpr (PAIR) {  // message i to the odd CTA: the unit it runs next
+                        const int s = (i - 1) & 1, use = (i - 1) >> 1;
+                        if (use >= 1) mbar_wait(bar(L::B_CE + s), (use - 1) & 1);  // slot consumed
+                        st_cluster_u32(mapa_shared(smem_u32(claim_slot + s), 1), static_cast<uint32_t>(x));
+                        mbar_arrive_cluster(mapa_shared(bar(L::B_CF + s), 1));
+                    }
+                }
+                __syncwarp();
+                if constexpr (PAIR) {
+                    if (!leader) {  // unit id from the even CTA (message i)
+                        const int s = (i - 1) & 1, use = (i - 1) >> 1;
+                        mbar_wait_acq_cluster(bar(L::B_CF + s), use & 1);  // pairs with the even CTA's release.cluster
+                        x = *reinterpret_cast<volatile int*>(claim_slot + s);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_remote(mapa_shared(bar(L::B_CE + s), 0));
+                    }
                 }
             }
             if (i >= 2) mbar_wait(bar(L::B_UE + ub), ((i - 2) >> 1) & 1);  // every consumer is done with unit i-2
@@ -974,12 +997,12 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
                 // no more units here: a programmatically dependent launch (the next ring step)
                 // may start on the SMs this grid frees from now on
                 if (lane == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-                break;
+                return -1;
             }
             int head, part, ux, blo, bhi;
             int64_t row0;
             unit_map(x, crank, head, row0, part, ux, blo, bhi);
-            const int kvh = head / p.g;
+            *kvh_out = head / p.g;
             uint16_t* list = reinterpret_cast<uint16_t*>(smem + L::OFF_SCHED) + ub * L::LISTMAX;
             int64_t qlo, qhi, plo = 0, phi = 0;
             bool qany, pany = false;
@@ -1049,9 +1072,37 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
                 ++n_ne;
             }
             __syncwarp();
+            return cnt;
+        };
+        // unit i is claimed and prepared once the K producer is kPrepLead tiles from the end of
+        // unit i - 1: late enough that the claim order still balances the launch's tail, early
+        // enough that the list, the publication and the Q load are done when its first S is due
+        int kvh_unused = 0;
+        for (int i = 0;; ++i) {
+            if (i >= 1) mbar_wait(bar(L::B_PR + ((i - 1) & 1)), ((i - 1) >> 1) & 1);
+            if (prepare(i, &kvh_unused) < 0) break;
+        }
+    } else if (warp == W_K) {
+        // ======== TMA producer of K (3 stages), following the published units ========
+        const uint64_t pol_kv = kv_policy();
+        int it = 0;
+        for (int i = 0;; ++i) {
+            const int ub = i & 1;
+            mbar_wait(bar(L::B_UF + ub), (i >> 1) & 1);
+            const UnitInfo u = uinfo[ub];
+            if (u.x < 0) break;
+            int head;
+            int64_t row0_unused;
+            unit_rows(u.x, crank, head, row0_unused);
+            const int kvh = head / p.g;
+            const int cnt = u.n_used;
+            const uint16_t* list = reinterpret_cast<const uint16_t*>(smem + L::OFF_SCHED) + ub * L::LISTMAX;
+            const int n_prep = cnt > kPrepLead ? cnt - kPrepLead : 0;  // the scheduler's cue for the next unit
+            if (n_prep == 0 && lane == 0) mbar_arrive(bar(L::B_PR + ub));
             int blk = 0;  // block of the current list entry (the list runs through blocks in order)
             uint32_t gated = 0;  // gated blocks already seen arrived (this unit)
             for (int n = 0; n < cnt; ++n) {
+                if (n == n_prep && n > 0 && lane == 0) mbar_arrive(bar(L::B_PR + ub));
                 const int gt = list[n] & ~kPartialBit;
                 while (gt >= toff[blk + 1]) ++blk;
                 const int j = gt - toff[blk];
@@ -1083,17 +1134,8 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
                 __syncwarp();
                 ++it;
             }
-            x = __shfl_sync(0xFFFFFFFFu, x_pre, 0);
-            if (leader && lane == 0) {
-                if (x < p.n_units) x_pre = G + atomicAdd(p.claim, 1);
-                if constexpr (PAIR) {  // message i+1 to the odd CTA: the unit it runs next
-                    const int s = i & 1, use = i >> 1;
-                    if (use >= 1) mbar_wait(bar(L::B_CE + s), (use - 1) & 1);  // slot consumed
-                    st_cluster_u32(mapa_shared(smem_u32(claim_slot + s), 1), static_cast<uint32_t>(x));
-                    mbar_arrive_cluster(mapa_shared(bar(L::B_CF + s), 1));
-                }
-            }
             __syncwarp();
+            if (ARRIVE_LANE) mbar_arrive(bar(L::B_UE + ub));  // done with the unit's list
         }
     } else if (warp == W_V) {
         // ======== TMA producer of V, following the published units ========
@@ -1157,7 +1199,7 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
             else mma_commit(bar(b));
         };
         // S(b) = Q K^T: M=128 (x2), N=128, K=HD in steps of 16 (32 B inside a 128-B swizzle row)
-        auto issue_qk = [&](int ks, int b) {
+        auto issue_qk = [&](int ks, int b, uint64_t dq) {
             const uint64_t dk = dk0 + static_cast<uint64_t>((ks * L::KTILE) >> 4);
 #pragma unroll
             for (int kk = 0; kk < HD / 16; ++kk) {
@@ -1181,13 +1223,14 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
                            idesc_pv, (acc || kk > 0) ? 1u : 0u);
             }
         };
-        auto issue_s = [&](int gn, int q_release) {  // S(gn) into buffer gn % NSB; K stage gn % KST
+        // S(gn) into buffer gn % NSB; K stage gn % KST; Q of the tile's unit at dq_u
+        auto issue_s = [&](int gn, int q_release, uint64_t dq_u) {
             const int ks = gn % L::KST;
             MMA_WAIT(bar(L::B_KF + ks), (gn / L::KST) & 1);
             tc_fence_after();
             if (elect_one()) {
                 KTRACE(9, gn);
-                issue_qk(ks, gn % NSB);
+                issue_qk(ks, gn % NSB, dq_u);
                 commit(L::B_SF + gn % NSB);  // S(gn) ready; K stage ks free
                 if (q_release >= 0) commit(L::B_QE + q_release);  // the unit's last S: Q buffer free
             }
@@ -1208,9 +1251,11 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
             MMA_WAIT(bar(L::B_QF + qb), (n_units_done / L::QST) & 1);  // Q tile(s) landed
             tc_fence_after();
             dq = dq0 + static_cast<uint64_t>((qb * L::TILE) >> 4);
-            // this unit's first S tiles go in only after the previous unit's last PV: its
-            // buffers are the ones those PVs read
-            for (int n = 0; n < NSB && n < N; ++n) issue_s(gn0 + n, n == N - 1 ? qb : -1);
+            // this unit's first S tiles go in only after the previous unit's last PV (their buffers
+            // are the ones those PVs read).  Issuing each as soon as its buffer's PV is issued, i.e.
+            // between the previous unit's last PVs, was measured slower (DESIGN 6.1): that unit's O
+            // then completes later and its finishing group reaches its next tile later.
+            for (int n = 0; n < NSB && n < N; ++n) issue_s(gn0 + n, n == N - 1 ? qb : -1, dq);
             for (int n = 0; n < N; ++n) {
                 const int gn = gn0 + n;
                 const int b = gn % NSB, vs = gn % L::VST;
@@ -1227,7 +1272,9 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
                     if (n == N - 1) commit(L::B_OF);
                 }
                 __syncwarp();
-                if (n + NSB < N) issue_s(gn + NSB, n + NSB == N - 1 ? qb : -1);  // into the buffer P(gn) just left
+                if (n + NSB < N) {
+                    issue_s(gn + NSB, n + NSB == N - 1 ? qb : -1, dq);  // into the buffer P(gn) just left
+                }
             }
             gn0 += N;
             ++n_units_done;
