@@ -45,7 +45,7 @@ extern "C" {
 #define CDSP_API
 #endif
 
-#define CDSP_ABI_VERSION 4
+#define CDSP_ABI_VERSION 5
 #define CDSP_IPC_HANDLE_BYTES 64   /* one cudaIpcMemHandle_t */
 #define CDSP_MAX_SP 8
 
@@ -388,6 +388,26 @@ CDSP_API cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_deco
                                            int32_t hkv_local, int64_t n_ctx, float softmax_scale,
                                            cdsp_tensor* out, float* lse, void* workspace,
                                            size_t workspace_bytes, void* cuda_stream);
+
+/* The same decode step for a batch of requests in one launch (a decode instance steps every
+ * running request at once).  Request b's newest token attends to its positions
+ * 0 .. ctx_lens[b]-1 through row b of the block table.
+ *   q / out [batch, Hq_t, D] bf16 (request-major); lse fp32 [batch, Hq_t] or NULL;
+ *   cache->block_table: device int32 [batch][n_table / batch] (row b = request b's pages);
+ *   ctx_lens: device int32 [batch], each in 1 .. max_ctx; max_ctx / total_ctx: host copies of
+ *     their maximum and sum (total_ctx <= 0: batch x max_ctx); the splits are sized so that
+ *     all requests' splits fill one wave, a shorter request's surplus split CTAs exit at once;
+ *   workspace: >= cdsp_decode_workspace_bytes(batch * Hq_t, batch * Hkv_t, D), zero-filled once
+ *     (left zero-filled), one call at a time per workspace.
+ * Errors: as cdsp_decode_attention; CDSP_ERR_UNSUPPORTED unless bf16 with block_size >= 16 (the
+ * TMA kernel); CDSP_ERR_SHAPE if n_table is not a multiple of batch; CDSP_ERR_CAPACITY if a row
+ * covers fewer than max_ctx positions or batch * Hkv_t > 65535.  ctx_lens outside 1 .. max_ctx:
+ * undefined (not read on the host). */
+CDSP_API cdsp_status cdsp_decode_attention_batch(const cdsp_tensor* q, const cdsp_decode_target* cache, int32_t t,
+                                                 int32_t hkv_local, int32_t batch, const int32_t* ctx_lens,
+                                                 int64_t max_ctx, int64_t total_ctx, float softmax_scale,
+                                                 cdsp_tensor* out, float* lse, void* workspace,
+                                                 size_t workspace_bytes, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------------
  * Building blocks, exported for tests and benches (same kernels the path uses)

@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "cdsp_comm_create_layers", "cdsp_kvstore_get_layer", "cdsp_prefill_chunk_layer",
     "cdsp_striped_gather", "cdsp_striped_scatter", "cdsp_fit_latency_model", "cdsp_schedule_prefill",
     "cdsp_comm_reserve", "cdsp_comm_set_ring_options", "cdsp_attention_fwd_blocks", "cdsp_prefill_chunk_transfer",
+    "cdsp_decode_attention_batch",
 )
 
 
@@ -159,6 +160,8 @@ def lib():
                                        ctypes.POINTER(i64), ctypes.POINTER(i32)],
             "cdsp_decode_attention": [ctypes.POINTER(Tensor), ctypes.POINTER(DecodeTargetC), i32, i32, i64, f32,
                                       ctypes.POINTER(Tensor), P, P, ctypes.c_size_t, P],
+            "cdsp_decode_attention_batch": [ctypes.POINTER(Tensor), ctypes.POINTER(DecodeTargetC), i32, i32, i32, P,
+                                            i64, i64, f32, ctypes.POINTER(Tensor), P, P, ctypes.c_size_t, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -492,6 +495,23 @@ def decode_attention(q, cache: DecodeTarget, t: int, hkv_local: int, n_ctx: int,
     _check(lib().cdsp_decode_attention(ctypes.byref(tq), ctypes.byref(cache.c), t, hkv_local, n_ctx, softmax_scale,
                                        ctypes.byref(to), _ptr(lse), workspace.data_ptr(), workspace.numel(),
                                        _stream(stream)))
+    return out, lse
+
+
+def decode_attention_batch(q, cache: DecodeTarget, t: int, hkv_local: int, ctx_lens, max_ctx: int,
+                           total_ctx: int = 0, softmax_scale: float = 0.0, out=None, lse=None, workspace=None,
+                           stream=None):
+    """Decode step for a batch on decode TP rank t: q [batch, Hq_t, D], request b over row b of
+    cache.block_table ([batch, pages]) up to ctx_lens[b] (device int32) -> (out, lse [batch, Hq_t])."""
+    batch, Hq_t, D = q.shape
+    out = out if out is not None else torch.empty_like(q)
+    if workspace is None:
+        workspace = decode_workspace(batch * Hq_t, batch * hkv_local, D, q.device)
+    tq, to = as_tensor(q), as_tensor(out)
+    _check(lib().cdsp_decode_attention_batch(ctypes.byref(tq), ctypes.byref(cache.c), t, hkv_local, batch,
+                                             ctx_lens.data_ptr(), int(max_ctx), int(total_ctx), softmax_scale,
+                                             ctypes.byref(to),
+                                             _ptr(lse), workspace.data_ptr(), workspace.numel(), _stream(stream)))
     return out, lse
 
 

@@ -75,10 +75,14 @@ constexpr int kMaxSplit = 512;  // splits per KV head
 constexpr int kMaxGroups = kMaxSplit / kGroup;
 
 struct DecodeParams {
-    const void* q;   // [Hq_t, D]
+    const void* q;   // [Hq_t, D] ([batch, Hq_t, D] for a batch)
     const void* kc;  // [num_blocks, B, Hkv_t, D]
     const void* vc;
     const int32_t* bt;
+    // batch (TMA kernel): request b = blockIdx.y / Hkv_t reads block-table row b (bt_stride
+    // entries apart) up to ctx_lens[b]; n_ctx / n_split / n_groups are then the longest request's
+    const int32_t* ctx_lens;  // device [batch], or NULL (one request of n_ctx)
+    int64_t bt_stride;
     int64_t num_blocks, n_ctx, tok_per_split;
     int b_shift, Hkv_t, n_split, n_groups;
     float scale_log2;
@@ -851,7 +855,17 @@ template <int HD, int G>
 __global__ void __launch_bounds__((kTW + 1) * 32) decode_tma_kernel(const __grid_constant__ DecTmaArgs a) {
     using L = TmaDecLayout<HD>;
     constexpr int KS = HD / 16, ND = HD / 8;
-    const DecodeParams& p = a.p;
+    // blockIdx.y = virtual head (request, KV head): the merge state, q, out and lse are indexed by
+    // it as for one request of batch x Hkv_t heads; the cache by the request's table row and kvh
+    DecodeParams p = a.p;
+    const int req = static_cast<int>(blockIdx.y) / p.Hkv_t;
+    if (p.ctx_lens) {
+        p.n_ctx = __ldg(p.ctx_lens + req);
+        p.bt += static_cast<int64_t>(req) * p.bt_stride;
+        p.n_split = static_cast<int>((p.n_ctx + p.tok_per_split - 1) / p.tok_per_split);
+        p.n_groups = (p.n_split + kGroup - 1) / kGroup;
+        if (static_cast<int>(blockIdx.x) >= p.n_split) return;  // a shorter request: no split here
+    }
     extern __shared__ uint8_t dsm_t[];
     __shared__ __align__(8) uint64_t full_b[kTNst], empty_b[kTNst];
     __shared__ int s_last;
@@ -859,7 +873,7 @@ __global__ void __launch_bounds__((kTW + 1) * 32) decode_tma_kernel(const __grid
     uint8_t* sm = dsm_t + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(dsm_t)) & 1023u)) & 1023u);
     const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int kvh = blockIdx.y, split = blockIdx.x;
+    const int vh = blockIdx.y, kvh = vh - req * p.Hkv_t, split = blockIdx.x;
     const int64_t t0 = static_cast<int64_t>(split) * p.tok_per_split;
     const int64_t t1 = min(p.n_ctx, t0 + p.tok_per_split);
     const int n_st = static_cast<int>((t1 - t0 + kTStage - 1) / kTStage);
@@ -918,7 +932,7 @@ __global__ void __launch_bounds__((kTW + 1) * 32) decode_tma_kernel(const __grid
         // ===== consumer warp w: sub-tile w of every stage
         uint32_t qa[KS][2];
         {
-            const __nv_bfloat16* qp = static_cast<const __nv_bfloat16*>(p.q) + (static_cast<size_t>(kvh) * G + g) * HD;
+            const __nv_bfloat16* qp = static_cast<const __nv_bfloat16*>(p.q) + (static_cast<size_t>(vh) * G + g) * HD;
 #pragma unroll
             for (int kk = 0; kk < KS; ++kk) {
                 qa[kk][0] = g < G ? *reinterpret_cast<const uint32_t*>(qp + 16 * kk + 2 * t) : 0u;
@@ -1140,16 +1154,22 @@ cdsp_status cdsp_decode_workspace_bytes(int32_t hq_local, int32_t hkv_local, int
     return CDSP_OK;
 }
 
-cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_decode_target* cache, int32_t t,
-                                  int32_t hkv_local, int64_t n_ctx, float softmax_scale, cdsp_tensor* out,
-                                  float* lse, void* workspace, size_t workspace_bytes, void* cuda_stream) {
+}  // extern "C"
+
+namespace {
+// One decode step for `batch` requests (batch == 1, ctx_lens == NULL: cdsp_decode_attention);
+// n_ctx is the longest request's context (sizes the splits and checks the table capacity).
+cdsp_status decode_impl(const cdsp_tensor* q, const cdsp_decode_target* cache, int32_t t, int32_t hkv_local,
+                        int32_t batch, const int32_t* ctx_lens, int64_t n_ctx, int64_t total_ctx, float softmax_scale,
+                        cdsp_tensor* out,
+                        float* lse, void* workspace, size_t workspace_bytes, void* cuda_stream) {
     CDSP_REQUIRE(q && cache && out && workspace, CDSP_ERR_INVALID, "NULL argument");
     CDSP_REQUIRE(dtype_ok(q->dtype) && q->dtype == out->dtype, CDSP_ERR_DTYPE, "q/out dtype");
     CDSP_REQUIRE(q->ptr && out->ptr && (reinterpret_cast<uintptr_t>(q->ptr) & 15u) == 0 &&
                      (reinterpret_cast<uintptr_t>(out->ptr) & 15u) == 0,
                  CDSP_ERR_INVALID, "q/out must be non-NULL and 16-byte aligned");
-    CDSP_REQUIRE(q->T == 1 && out->T == 1 && out->H == q->H && out->D == q->D, CDSP_ERR_SHAPE,
-                 "q and out must be [1, Hq_t, D]");
+    CDSP_REQUIRE(batch >= 1 && q->T == batch && out->T == batch && out->H == q->H && out->D == q->D,
+                 CDSP_ERR_SHAPE, "q and out must be [%d, Hq_t, D]", batch);
     const int D = static_cast<int>(q->D);
     CDSP_REQUIRE(D == 64 || D == 128, CDSP_ERR_SHAPE, "head dim %d not in {64,128}", D);
     CDSP_REQUIRE(hkv_local >= 1 && q->H % hkv_local == 0, CDSP_ERR_SHAPE, "Hq_t=%lld not a multiple of Hkv_t=%d",
@@ -1164,9 +1184,14 @@ cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_decode_target
     CDSP_REQUIRE(B >= 1 && B <= 4096 && (B & (B - 1)) == 0, CDSP_ERR_UNSUPPORTED,
                  "block size %d must be a power of two <= 4096", B);
     CDSP_REQUIRE(n_ctx >= 1, CDSP_ERR_SHAPE, "n_ctx must be >= 1");
-    CDSP_REQUIRE(cache->n_table * B >= n_ctx, CDSP_ERR_CAPACITY, "block table covers %lld positions < n_ctx %lld",
-                 static_cast<long long>(cache->n_table * B), static_cast<long long>(n_ctx));
-    const WsLayout w = ws_layout(hkv_local, G, D);
+    CDSP_REQUIRE(cache->n_table % batch == 0, CDSP_ERR_SHAPE, "block table of %lld entries is not %d rows",
+                 static_cast<long long>(cache->n_table), batch);
+    const int64_t row_len = cache->n_table / batch;  // block-table entries per request
+    CDSP_REQUIRE(row_len * B >= n_ctx, CDSP_ERR_CAPACITY, "block table row covers %lld positions < n_ctx %lld",
+                 static_cast<long long>(row_len * B), static_cast<long long>(n_ctx));
+    const int vheads = batch * hkv_local;  // (request, KV head) pairs: the merge's heads
+    CDSP_REQUIRE(vheads <= 65535, CDSP_ERR_CAPACITY, "batch x KV heads %d exceeds 65535", vheads);
+    const WsLayout w = ws_layout(vheads, G, D);
     CDSP_REQUIRE(workspace_bytes >= w.total, CDSP_ERR_CAPACITY, "workspace %zu < %zu bytes", workspace_bytes,
                  w.total);
     CDSP_REQUIRE((reinterpret_cast<uintptr_t>(workspace) & 255u) == 0, CDSP_ERR_INVALID,
@@ -1178,6 +1203,8 @@ cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_decode_target
     p.kc = cache->k_cache[t];
     p.vc = cache->v_cache[t];
     p.bt = cache->block_table;
+    p.ctx_lens = ctx_lens;
+    p.bt_stride = row_len;
     p.num_blocks = cache->num_blocks;
     p.n_ctx = n_ctx;
     int sh = 0;
@@ -1188,11 +1215,23 @@ cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_decode_target
     p.scale_log2 = scale * 1.4426950408889634f;
     // split sizing: one wave of resident CTAs over all KV heads, whole warp-steps per split
     const Sel k = select(q->dtype, D, G, B >= 16);
+    CDSP_REQUIRE(batch == 1 || k.tma, CDSP_ERR_UNSUPPORTED,
+                 "a batch of requests needs the bf16 TMA kernel (block size >= 16)");
     const int occ = prepare(k);
     const int64_t steps = (n_ctx + k.step - 1) / k.step;
-    int64_t want = (static_cast<int64_t>(occ) * sm_count() + hkv_local - 1) / hkv_local;
+    // (rounded down: a split more per head than one wave holds would put a few CTAs in a second
+    // wave, doubling the launch)
+    int64_t want = static_cast<int64_t>(occ) * sm_count() / vheads;
     want = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, kMaxSplit), steps));
-    const int64_t steps_per = (steps + want - 1) / want;
+    int64_t steps_per = (steps + want - 1) / want;
+    if (total_ctx > 0 && total_ctx < static_cast<int64_t>(batch) * n_ctx) {
+        // a batch of mixed lengths: splits sized for the AVERAGE request, want - 1 of them (each
+        // request's count rounds up by < 1, so all of them still fit one wave), instead of the
+        // longest request's want; a shorter request's surplus split CTAs exit at once
+        const int64_t avg_steps = (total_ctx / batch + k.step - 1) / k.step;
+        const int64_t w1 = std::max<int64_t>(1, static_cast<int64_t>(occ) * sm_count() / vheads - 1);
+        steps_per = std::max<int64_t>((avg_steps + w1 - 1) / w1, (steps + kMaxSplit - 1) / kMaxSplit);
+    }
     p.tok_per_split = steps_per * k.step;
     p.n_split = static_cast<int>((n_ctx + p.tok_per_split - 1) / p.tok_per_split);
     p.n_groups = (p.n_split + kGroup - 1) / kGroup;
@@ -1217,7 +1256,7 @@ cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_decode_target
         ta.p = p;
         ta.oob_row = rows;
         void* targs[] = {&ta};
-        CDSP_CUDA(cudaLaunchKernel(k.fn, dim3(static_cast<unsigned>(p.n_split), static_cast<unsigned>(hkv_local)),
+        CDSP_CUDA(cudaLaunchKernel(k.fn, dim3(static_cast<unsigned>(p.n_split), static_cast<unsigned>(vheads)),
                                    dim3(static_cast<unsigned>(k.threads)), targs, k.smem, st));
         return CDSP_OK;
     }
@@ -1225,6 +1264,27 @@ cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_decode_target
     CDSP_CUDA(cudaLaunchKernel(k.fn, dim3(static_cast<unsigned>(p.n_split), static_cast<unsigned>(hkv_local)),
                                dim3(static_cast<unsigned>(k.threads)), args, k.smem, st));
     return CDSP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_decode_target* cache, int32_t t,
+                                  int32_t hkv_local, int64_t n_ctx, float softmax_scale, cdsp_tensor* out,
+                                  float* lse, void* workspace, size_t workspace_bytes, void* cuda_stream) {
+    return decode_impl(q, cache, t, hkv_local, 1, nullptr, n_ctx, 0, softmax_scale, out, lse, workspace,
+                       workspace_bytes, cuda_stream);
+}
+
+cdsp_status cdsp_decode_attention_batch(const cdsp_tensor* q, const cdsp_decode_target* cache, int32_t t,
+                                        int32_t hkv_local, int32_t batch, const int32_t* ctx_lens, int64_t max_ctx,
+                                        int64_t total_ctx, float softmax_scale, cdsp_tensor* out, float* lse,
+                                        void* workspace, size_t workspace_bytes, void* cuda_stream) {
+    CDSP_REQUIRE(ctx_lens != nullptr, CDSP_ERR_INVALID, "ctx_lens is NULL");
+    CDSP_REQUIRE(total_ctx <= static_cast<int64_t>(batch) * max_ctx, CDSP_ERR_SHAPE,
+                 "total_ctx %lld exceeds batch x max_ctx", static_cast<long long>(total_ctx));
+    return decode_impl(q, cache, t, hkv_local, batch, ctx_lens, max_ctx, total_ctx, softmax_scale, out, lse, workspace,
+                       workspace_bytes, cuda_stream);
 }
 
 #ifdef CDSP_DTRACE

@@ -30,7 +30,7 @@ def test_exports_every_declared_symbol(lib):
     for n in names:
         assert hasattr(lib, n), f"libcdsp.so does not export {n}"
     assert set(names) == set(api.EXPORTED_SYMBOLS)
-    assert api.abi_version() == 4
+    assert api.abi_version() == 5
 
 
 def test_no_oracle_in_product():
