@@ -1071,6 +1071,9 @@ cdsp_status cdsp_prefill_chunk_transfer(const cdsp_tensor* q, const cdsp_tensor*
     // transfer stream, fills SMs as the attention's tail frees them (enqueued first, its CTAs
     // would hold SMs the attention needs)
     CDSP_CHECK_STATUS(prefill_impl(q, k, v, prev_kv, sp_group, 0, softmax_scale, out, lse, cuda_stream));
+    // measurement control CDSP_XFER_SERIAL=1: the scatter after the attention on the caller's stream
+    static const bool serial = getenv("CDSP_XFER_SERIAL") != nullptr && getenv("CDSP_XFER_SERIAL")[0] == '1';
+    if (serial) return cdsp_kv_transfer_to_decode(k, v, sp_group, dst, cuda_stream);
     CDSP_CUDA(cudaStreamWaitEvent(c->xfer_stream, c->ev_x0, 0));
     CDSP_CHECK_STATUS(cdsp_kv_transfer_to_decode(k, v, sp_group, dst, c->xfer_stream));
     CDSP_CUDA(cudaEventRecord(c->ev_x1, c->xfer_stream));
