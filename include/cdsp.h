@@ -394,19 +394,19 @@ CDSP_API cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_deco
  * 0 .. ctx_lens[b]-1 through row b of the block table.
  *   q / out [batch, Hq_t, D] bf16 (request-major); lse fp32 [batch, Hq_t] or NULL;
  *   cache->block_table: device int32 [batch][n_table / batch] (row b = request b's pages);
- *   ctx_lens: device int32 [batch], each in 1 .. max_ctx; max_ctx / total_ctx: host copies of
- *     their maximum and sum (total_ctx <= 0: batch x max_ctx); the splits are sized so that
- *     all requests' splits fill one wave, a shorter request's surplus split CTAs exit at once;
+ *   ctx_lens: HOST int32 [batch] (the decode instance's own record of its requests' lengths),
+ *     each >= 1; the splits are sized so that all requests' splits together fill at most one
+ *     wave, and laid out back to back on a 1D grid (a request of c tokens gets ceil(c / split)
+ *     per KV head); batch <= 1024;
  *   workspace: >= cdsp_decode_workspace_bytes(batch * Hq_t, batch * Hkv_t, D), zero-filled once
  *     (left zero-filled), one call at a time per workspace.
  * Errors: as cdsp_decode_attention; CDSP_ERR_UNSUPPORTED unless bf16 with block_size >= 16 (the
- * TMA kernel); CDSP_ERR_SHAPE if n_table is not a multiple of batch; CDSP_ERR_CAPACITY if a row
- * covers fewer than max_ctx positions or batch * Hkv_t > 65535.  ctx_lens outside 1 .. max_ctx:
- * undefined (not read on the host). */
+ * TMA kernel); CDSP_ERR_SHAPE if n_table is not a multiple of batch or a length is < 1;
+ * CDSP_ERR_CAPACITY if a row covers fewer positions than the longest request, batch > 1024 or
+ * batch * Hkv_t > 65535. */
 CDSP_API cdsp_status cdsp_decode_attention_batch(const cdsp_tensor* q, const cdsp_decode_target* cache, int32_t t,
                                                  int32_t hkv_local, int32_t batch, const int32_t* ctx_lens,
-                                                 int64_t max_ctx, int64_t total_ctx, float softmax_scale,
-                                                 cdsp_tensor* out, float* lse, void* workspace,
+                                                 float softmax_scale, cdsp_tensor* out, float* lse, void* workspace,
                                                  size_t workspace_bytes, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------------

@@ -161,7 +161,7 @@ def lib():
             "cdsp_decode_attention": [ctypes.POINTER(Tensor), ctypes.POINTER(DecodeTargetC), i32, i32, i64, f32,
                                       ctypes.POINTER(Tensor), P, P, ctypes.c_size_t, P],
             "cdsp_decode_attention_batch": [ctypes.POINTER(Tensor), ctypes.POINTER(DecodeTargetC), i32, i32, i32, P,
-                                            i64, i64, f32, ctypes.POINTER(Tensor), P, P, ctypes.c_size_t, P],
+                                            f32, ctypes.POINTER(Tensor), P, P, ctypes.c_size_t, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -498,19 +498,18 @@ def decode_attention(q, cache: DecodeTarget, t: int, hkv_local: int, n_ctx: int,
     return out, lse
 
 
-def decode_attention_batch(q, cache: DecodeTarget, t: int, hkv_local: int, ctx_lens, max_ctx: int,
-                           total_ctx: int = 0, softmax_scale: float = 0.0, out=None, lse=None, workspace=None,
-                           stream=None):
+def decode_attention_batch(q, cache: DecodeTarget, t: int, hkv_local: int, ctx_lens: Sequence[int],
+                           softmax_scale: float = 0.0, out=None, lse=None, workspace=None, stream=None):
     """Decode step for a batch on decode TP rank t: q [batch, Hq_t, D], request b over row b of
-    cache.block_table ([batch, pages]) up to ctx_lens[b] (device int32) -> (out, lse [batch, Hq_t])."""
+    cache.block_table ([batch, pages]) up to ctx_lens[b] (host lengths) -> (out, lse [batch, Hq_t])."""
     batch, Hq_t, D = q.shape
+    lens = (ctypes.c_int32 * batch)(*[int(x) for x in ctx_lens])
     out = out if out is not None else torch.empty_like(q)
     if workspace is None:
         workspace = decode_workspace(batch * Hq_t, batch * hkv_local, D, q.device)
     tq, to = as_tensor(q), as_tensor(out)
     _check(lib().cdsp_decode_attention_batch(ctypes.byref(tq), ctypes.byref(cache.c), t, hkv_local, batch,
-                                             ctx_lens.data_ptr(), int(max_ctx), int(total_ctx), softmax_scale,
-                                             ctypes.byref(to),
+                                             lens, softmax_scale, ctypes.byref(to),
                                              _ptr(lse), workspace.data_ptr(), workspace.numel(), _stream(stream)))
     return out, lse
 

@@ -79,10 +79,7 @@ struct DecodeParams {
     const void* kc;  // [num_blocks, B, Hkv_t, D]
     const void* vc;
     const int32_t* bt;
-    // batch (TMA kernel): request b = blockIdx.y / Hkv_t reads block-table row b (bt_stride
-    // entries apart) up to ctx_lens[b]; n_ctx / n_split / n_groups are then the longest request's
-    const int32_t* ctx_lens;  // device [batch], or NULL (one request of n_ctx)
-    int64_t bt_stride;
+    int64_t bt_stride;  // batch (TMA kernel): request b reads block-table row b, bt_stride entries apart
     int64_t num_blocks, n_ctx, tok_per_split;
     int b_shift, Hkv_t, n_split, n_groups;
     float scale_log2;
@@ -318,9 +315,9 @@ __device__ void merge_slice(const DecodeParams& p, int kvh, int sl) {
 // shared memory; merge them (R3), then write the output (one split) or this split's partial
 // and run the in-kernel two-level split merge.
 template <typename T, int HD, int G>
-__device__ void finish_cta(const DecodeParams& p, const int NS, const float* sm_o, const float* sm_ml, float* w_sh,
+__device__ void finish_cta(const DecodeParams& p, const int kvh, const int split, const int NS, const float* sm_o,
+                           const float* sm_ml, float* w_sh,
                            float* lse_sh, int* s_last) {
-    const int kvh = blockIdx.y, split = blockIdx.x;
     __syncthreads();
     if (threadIdx.x < G) {
         const int h = threadIdx.x;
@@ -575,7 +572,7 @@ __global__ void __launch_bounds__(kThreads) decode_attn_kernel(const DecodeParam
             sm_ml[(slot * G + h) * 2 + 1] = l[h];
         }
     }
-    finish_cta<T, HD, G>(p, kWarps * TPI, sm_o, sm_ml, w_sh, lse_sh, &s_last);
+    finish_cta<T, HD, G>(p, blockIdx.y, blockIdx.x, kWarps * TPI, sm_o, sm_ml, w_sh, lse_sh, &s_last);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -802,7 +799,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32) decode_mma_kernel(const Decode
             sm_ml[(warp * G + g) * 2 + 1] = l;
         }
     }
-    finish_cta<__nv_bfloat16, HD, G>(p, kMmaWarps, sm_o, sm_ml, w_sh, lse_sh, &s_last);
+    finish_cta<__nv_bfloat16, HD, G>(p, blockIdx.y, blockIdx.x, kMmaWarps, sm_o, sm_ml, w_sh, lse_sh, &s_last);
     dstamp(3);
 }
 
@@ -836,6 +833,15 @@ struct DecTmaArgs {
     DecodeParams p;
     int64_t oob_row;   // a row coordinate past the tensor (zero-filled box)
 };
+// A batch of requests: a 1D grid over every request's (KV head, split) pairs back to back; CTA
+// i belongs to request b with pre[b] <= i < pre[b + 1] (n_split_b = (pre[b + 1] - pre[b]) /
+// Hkv_t splits of each of its KV heads), found by a binary search in kernel-parameter space.
+constexpr int kMaxBatch = 1024;
+struct DecTmaBatchArgs : DecTmaArgs {
+    int32_t nb;
+    int32_t pre[kMaxBatch + 1];
+    int32_t ctx[kMaxBatch];
+};
 
 template <int HD>
 struct TmaDecLayout {
@@ -851,21 +857,33 @@ __device__ __forceinline__ uint32_t tdec_chunk(uint32_t sub, int tok, int ch) { 
     return sub + static_cast<uint32_t>((ch >> 3) * TmaDecLayout<HD>::BOX + tok * 128 + (((ch & 7) ^ (tok & 7)) << 4));
 }
 
-template <int HD, int G>
-__global__ void __launch_bounds__((kTW + 1) * 32) decode_tma_kernel(const __grid_constant__ DecTmaArgs a) {
+template <int HD, int G, typename Args>
+__global__ void __launch_bounds__((kTW + 1) * 32) decode_tma_kernel(const __grid_constant__ Args a) {
     using L = TmaDecLayout<HD>;
     constexpr int KS = HD / 16, ND = HD / 8;
-    // blockIdx.y = virtual head (request, KV head): the merge state, q, out and lse are indexed by
-    // it as for one request of batch x Hkv_t heads; the cache by the request's table row and kvh
+    // virtual head vh = (request, KV head): the merge state, q, out and lse are indexed by it as
+    // for one request of batch x Hkv_t heads; the cache by the request's table row and kvh.
+    // One request: grid (split, KV head).  A batch (DecTmaBatchArgs): 1D grid, see there.
     DecodeParams p = a.p;
-    const int req = static_cast<int>(blockIdx.y) / p.Hkv_t;
-    if (p.ctx_lens) {
-        p.n_ctx = __ldg(p.ctx_lens + req);
-        p.bt += static_cast<int64_t>(req) * p.bt_stride;
-        p.n_split = static_cast<int>((p.n_ctx + p.tok_per_split - 1) / p.tok_per_split);
-        p.n_groups = (p.n_split + kGroup - 1) / kGroup;
-        if (static_cast<int>(blockIdx.x) >= p.n_split) return;  // a shorter request: no split here
+    int vh = blockIdx.y, split = blockIdx.x;
+    if constexpr (sizeof(Args) == sizeof(DecTmaBatchArgs)) {
+        const int i = static_cast<int>(blockIdx.x);
+        int lo = 0, hi = a.nb;  // pre[lo] <= i < pre[hi]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (a.pre[mid] <= i) lo = mid;
+            else hi = mid;
+        }
+        const int ns = (a.pre[lo + 1] - a.pre[lo]) / p.Hkv_t;
+        const int rr = i - a.pre[lo];
+        p.n_ctx = a.ctx[lo];
+        p.bt += static_cast<int64_t>(lo) * p.bt_stride;
+        p.n_split = ns;
+        p.n_groups = (ns + kGroup - 1) / kGroup;
+        vh = lo * p.Hkv_t + rr / ns;
+        split = rr % ns;
     }
+    const int req = vh / p.Hkv_t;
     extern __shared__ uint8_t dsm_t[];
     __shared__ __align__(8) uint64_t full_b[kTNst], empty_b[kTNst];
     __shared__ int s_last;
@@ -873,7 +891,7 @@ __global__ void __launch_bounds__((kTW + 1) * 32) decode_tma_kernel(const __grid
     uint8_t* sm = dsm_t + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(dsm_t)) & 1023u)) & 1023u);
     const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int vh = blockIdx.y, kvh = vh - req * p.Hkv_t, split = blockIdx.x;
+    const int kvh = vh - req * p.Hkv_t;
     const int64_t t0 = static_cast<int64_t>(split) * p.tok_per_split;
     const int64_t t1 = min(p.n_ctx, t0 + p.tok_per_split);
     const int n_st = static_cast<int>((t1 - t0 + kTStage - 1) / kTStage);
@@ -1033,7 +1051,7 @@ __global__ void __launch_bounds__((kTW + 1) * 32) decode_tma_kernel(const __grid
             sm_ml[(warp * G + g) * 2 + 1] = l;
         }
     }
-    finish_cta<__nv_bfloat16, HD, G>(p, kTW, sm_o, sm_ml, w_sh, lse_sh, &s_last);
+    finish_cta<__nv_bfloat16, HD, G>(p, vh, split, kTW, sm_o, sm_ml, w_sh, lse_sh, &s_last);
     dstamp(3);
 }
 
@@ -1074,11 +1092,17 @@ struct Sel {
     bool tma;
 };
 template <int HD>
-Sel select_tma(int G) {
-    const void* fn = G == 1 ? reinterpret_cast<const void*>(decode_tma_kernel<HD, 1>)
-                   : G == 2 ? reinterpret_cast<const void*>(decode_tma_kernel<HD, 2>)
-                   : G == 4 ? reinterpret_cast<const void*>(decode_tma_kernel<HD, 4>)
-                            : reinterpret_cast<const void*>(decode_tma_kernel<HD, 8>);
+Sel select_tma(int G, bool batch) {
+    using A = DecTmaArgs;
+    using BA = DecTmaBatchArgs;
+    const void* fn = G == 1 ? (batch ? reinterpret_cast<const void*>(decode_tma_kernel<HD, 1, BA>)
+                                     : reinterpret_cast<const void*>(decode_tma_kernel<HD, 1, A>))
+                   : G == 2 ? (batch ? reinterpret_cast<const void*>(decode_tma_kernel<HD, 2, BA>)
+                                     : reinterpret_cast<const void*>(decode_tma_kernel<HD, 2, A>))
+                   : G == 4 ? (batch ? reinterpret_cast<const void*>(decode_tma_kernel<HD, 4, BA>)
+                                     : reinterpret_cast<const void*>(decode_tma_kernel<HD, 4, A>))
+                            : (batch ? reinterpret_cast<const void*>(decode_tma_kernel<HD, 8, BA>)
+                                     : reinterpret_cast<const void*>(decode_tma_kernel<HD, 8, A>));
     return {fn, (kTW + 1) * 32, static_cast<size_t>(TmaDecLayout<HD>::SMEM), kTStage, true};
 }
 template <typename T, int HD, int G>
@@ -1102,8 +1126,9 @@ Sel select_g(int G, bool ps) {
         default: return select_t<T, HD, 8>(ps);
     }
 }
-Sel select(int32_t dtype, int D, int G, bool ps) {
-    if (CDSP_DEC_TMA && dtype == CDSP_BF16 && ps) return D == 128 ? select_tma<128>(G) : select_tma<64>(G);
+Sel select(int32_t dtype, int D, int G, bool ps, bool batch) {
+    if ((CDSP_DEC_TMA || batch) && dtype == CDSP_BF16 && ps)
+        return D == 128 ? select_tma<128>(G, batch) : select_tma<64>(G, batch);
     if (dtype == CDSP_BF16) return D == 128 ? select_g<__nv_bfloat16, 128>(G, ps) : select_g<__nv_bfloat16, 64>(G, ps);
     return D == 128 ? select_g<float, 128>(G, ps) : select_g<float, 64>(G, ps);
 }
@@ -1157,11 +1182,10 @@ cdsp_status cdsp_decode_workspace_bytes(int32_t hq_local, int32_t hkv_local, int
 }  // extern "C"
 
 namespace {
-// One decode step for `batch` requests (batch == 1, ctx_lens == NULL: cdsp_decode_attention);
-// n_ctx is the longest request's context (sizes the splits and checks the table capacity).
+// One decode step for `batch` requests (ctx_lens: host [batch]) or for one request of n_ctx
+// (ctx_lens == NULL, batch == 1: cdsp_decode_attention).
 cdsp_status decode_impl(const cdsp_tensor* q, const cdsp_decode_target* cache, int32_t t, int32_t hkv_local,
-                        int32_t batch, const int32_t* ctx_lens, int64_t n_ctx, int64_t total_ctx, float softmax_scale,
-                        cdsp_tensor* out,
+                        int32_t batch, const int32_t* ctx_lens, int64_t n_ctx, float softmax_scale, cdsp_tensor* out,
                         float* lse, void* workspace, size_t workspace_bytes, void* cuda_stream) {
     CDSP_REQUIRE(q && cache && out && workspace, CDSP_ERR_INVALID, "NULL argument");
     CDSP_REQUIRE(dtype_ok(q->dtype) && q->dtype == out->dtype, CDSP_ERR_DTYPE, "q/out dtype");
@@ -1183,6 +1207,17 @@ cdsp_status decode_impl(const cdsp_tensor* q, const cdsp_decode_target* cache, i
     const int B = cache->block_size;
     CDSP_REQUIRE(B >= 1 && B <= 4096 && (B & (B - 1)) == 0, CDSP_ERR_UNSUPPORTED,
                  "block size %d must be a power of two <= 4096", B);
+    int64_t total_ctx = n_ctx;
+    if (ctx_lens) {
+        CDSP_REQUIRE(batch <= kMaxBatch, CDSP_ERR_CAPACITY, "batch %d exceeds %d", batch, kMaxBatch);
+        n_ctx = 0;
+        total_ctx = 0;
+        for (int b = 0; b < batch; ++b) {
+            CDSP_REQUIRE(ctx_lens[b] >= 1, CDSP_ERR_SHAPE, "ctx_lens[%d] = %d must be >= 1", b, ctx_lens[b]);
+            n_ctx = std::max<int64_t>(n_ctx, ctx_lens[b]);
+            total_ctx += ctx_lens[b];
+        }
+    }
     CDSP_REQUIRE(n_ctx >= 1, CDSP_ERR_SHAPE, "n_ctx must be >= 1");
     CDSP_REQUIRE(cache->n_table % batch == 0, CDSP_ERR_SHAPE, "block table of %lld entries is not %d rows",
                  static_cast<long long>(cache->n_table), batch);
@@ -1203,7 +1238,6 @@ cdsp_status decode_impl(const cdsp_tensor* q, const cdsp_decode_target* cache, i
     p.kc = cache->k_cache[t];
     p.vc = cache->v_cache[t];
     p.bt = cache->block_table;
-    p.ctx_lens = ctx_lens;
     p.bt_stride = row_len;
     p.num_blocks = cache->num_blocks;
     p.n_ctx = n_ctx;
@@ -1214,7 +1248,7 @@ cdsp_status decode_impl(const cdsp_tensor* q, const cdsp_decode_target* cache, i
     const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(static_cast<float>(D));
     p.scale_log2 = scale * 1.4426950408889634f;
     // split sizing: one wave of resident CTAs over all KV heads, whole warp-steps per split
-    const Sel k = select(q->dtype, D, G, B >= 16);
+    const Sel k = select(q->dtype, D, G, B >= 16, ctx_lens != nullptr);
     CDSP_REQUIRE(batch == 1 || k.tma, CDSP_ERR_UNSUPPORTED,
                  "a batch of requests needs the bf16 TMA kernel (block size >= 16)");
     const int occ = prepare(k);
@@ -1224,13 +1258,20 @@ cdsp_status decode_impl(const cdsp_tensor* q, const cdsp_decode_target* cache, i
     int64_t want = static_cast<int64_t>(occ) * sm_count() / vheads;
     want = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, kMaxSplit), steps));
     int64_t steps_per = (steps + want - 1) / want;
-    if (total_ctx > 0 && total_ctx < static_cast<int64_t>(batch) * n_ctx) {
-        // a batch of mixed lengths: splits sized for the AVERAGE request, want - 1 of them (each
-        // request's count rounds up by < 1, so all of them still fit one wave), instead of the
-        // longest request's want; a shorter request's surplus split CTAs exit at once
-        const int64_t avg_steps = (total_ctx / batch + k.step - 1) / k.step;
-        const int64_t w1 = std::max<int64_t>(1, static_cast<int64_t>(occ) * sm_count() / vheads - 1);
-        steps_per = std::max<int64_t>((avg_steps + w1 - 1) / w1, (steps + kMaxSplit - 1) / kMaxSplit);
+    if (ctx_lens && total_ctx < static_cast<int64_t>(batch) * n_ctx) {
+        // a batch of mixed lengths: the smallest split size whose splits, over all requests and
+        // KV heads, fill at most one wave (each request gets ceil(steps_b / split) of them).  A few
+        // slots are left free: a grid of exactly occupancy x SMs CTAs measured as two waves
+        // (one CTA waiting makes its request's merge, and the launch, twice as long)
+        const int64_t slots = static_cast<int64_t>(occ) * sm_count() - std::max(8, sm_count() / 16);
+        int64_t sp = std::max<int64_t>(1, ((total_ctx + k.step - 1) / k.step * hkv_local + slots - 1) / slots);
+        sp = std::max<int64_t>(sp, (steps + kMaxSplit - 1) / kMaxSplit);
+        for (;; ++sp) {
+            int64_t n = 0;
+            for (int b = 0; b < batch; ++b) n += ((ctx_lens[b] + k.step - 1) / k.step + sp - 1) / sp;
+            if (n * hkv_local <= slots || sp >= steps) break;
+        }
+        steps_per = sp;
     }
     p.tok_per_split = steps_per * k.step;
     p.n_split = static_cast<int>((n_ctx + p.tok_per_split - 1) / p.tok_per_split);
@@ -1255,6 +1296,21 @@ cdsp_status decode_impl(const cdsp_tensor* q, const cdsp_decode_target* cache, i
         CDSP_CHECK_STATUS(make_tile_map(&ta.v, cache->v_cache[t], rows, hkv_local, D, 16));
         ta.p = p;
         ta.oob_row = rows;
+        if (ctx_lens) {  // every request's (KV head, split) pairs back to back on a 1D grid
+            static thread_local DecTmaBatchArgs tb;  // (8 KB: off the stack)
+            static_cast<DecTmaArgs&>(tb) = ta;
+            tb.nb = batch;
+            tb.pre[0] = 0;
+            for (int b = 0; b < batch; ++b) {
+                tb.ctx[b] = ctx_lens[b];
+                const int64_t ns = (ctx_lens[b] + p.tok_per_split - 1) / p.tok_per_split;
+                tb.pre[b + 1] = tb.pre[b] + static_cast<int32_t>(ns * hkv_local);
+            }
+            void* bargs[] = {&tb};
+            CDSP_CUDA(cudaLaunchKernel(k.fn, dim3(static_cast<unsigned>(tb.pre[batch])),
+                                       dim3(static_cast<unsigned>(k.threads)), bargs, k.smem, st));
+            return CDSP_OK;
+        }
         void* targs[] = {&ta};
         CDSP_CUDA(cudaLaunchKernel(k.fn, dim3(static_cast<unsigned>(p.n_split), static_cast<unsigned>(vheads)),
                                    dim3(static_cast<unsigned>(k.threads)), targs, k.smem, st));
@@ -1272,18 +1328,16 @@ extern "C" {
 cdsp_status cdsp_decode_attention(const cdsp_tensor* q, const cdsp_decode_target* cache, int32_t t,
                                   int32_t hkv_local, int64_t n_ctx, float softmax_scale, cdsp_tensor* out,
                                   float* lse, void* workspace, size_t workspace_bytes, void* cuda_stream) {
-    return decode_impl(q, cache, t, hkv_local, 1, nullptr, n_ctx, 0, softmax_scale, out, lse, workspace,
+    return decode_impl(q, cache, t, hkv_local, 1, nullptr, n_ctx, softmax_scale, out, lse, workspace,
                        workspace_bytes, cuda_stream);
 }
 
 cdsp_status cdsp_decode_attention_batch(const cdsp_tensor* q, const cdsp_decode_target* cache, int32_t t,
-                                        int32_t hkv_local, int32_t batch, const int32_t* ctx_lens, int64_t max_ctx,
-                                        int64_t total_ctx, float softmax_scale, cdsp_tensor* out, float* lse,
-                                        void* workspace, size_t workspace_bytes, void* cuda_stream) {
+                                        int32_t hkv_local, int32_t batch, const int32_t* ctx_lens, float softmax_scale,
+                                        cdsp_tensor* out, float* lse, void* workspace, size_t workspace_bytes,
+                                        void* cuda_stream) {
     CDSP_REQUIRE(ctx_lens != nullptr, CDSP_ERR_INVALID, "ctx_lens is NULL");
-    CDSP_REQUIRE(total_ctx <= static_cast<int64_t>(batch) * max_ctx, CDSP_ERR_SHAPE,
-                 "total_ctx %lld exceeds batch x max_ctx", static_cast<long long>(total_ctx));
-    return decode_impl(q, cache, t, hkv_local, batch, ctx_lens, max_ctx, total_ctx, softmax_scale, out, lse, workspace,
+    return decode_impl(q, cache, t, hkv_local, batch, ctx_lens, 0, softmax_scale, out, lse, workspace,
                        workspace_bytes, cuda_stream);
 }
 

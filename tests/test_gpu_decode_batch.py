@@ -52,11 +52,10 @@ def _batch(lens, Hq, Hkv, D, tp, B=16, seed=3):
 def _check(lens, Hq, Hkv, D, tp, ranks, B=16):
     dst, reqs = _batch(lens, Hq, Hkv, D, tp, B)
     hq_t, hkv_t = Hq // tp, Hkv // tp
-    ctx = torch.tensor(lens, dtype=torch.int32, device="cuda")
     for t in ranks:
         q = torch.cat([r[0][:, t * hq_t:(t + 1) * hq_t] for r in reqs]).contiguous().cuda()
         lse = torch.empty((len(lens), hq_t), dtype=torch.float32, device="cuda")
-        out, _ = api.decode_attention_batch(q, dst, t, hkv_t, ctx, max(lens), total_ctx=sum(lens), lse=lse)
+        out, _ = api.decode_attention_batch(q, dst, t, hkv_t, lens, lse=lse)
         torch.cuda.synchronize()
         for b, (qb, k, v) in enumerate(reqs):
             n = lens[b]
@@ -81,12 +80,19 @@ def test_batch_equal_lengths_many_requests():
     _check([2048] * 12, 32, 8, 128, 8, [0, 3])
 
 
+def test_batch_many_short_and_one_long():
+    """300 requests of 16..700 tokens and one of 20000: the split search and the 1D grid's
+    binary search over 301 request offsets."""
+    g = torch.Generator().manual_seed(9)
+    lens = [int(x) for x in torch.randint(16, 701, (300,), generator=g)] + [20000]
+    _check(lens, 32, 8, 128, 8, [0])
+
+
 def test_batch_of_one_equals_single_call():
     """batch = 1 through the batch entry point == cdsp_decode_attention (same kernel, same splits)."""
     dst, reqs = _batch([3001], 32, 8, 128, 8)
     q = reqs[0][0][:, :4].contiguous().cuda()
-    ctx = torch.tensor([3001], dtype=torch.int32, device="cuda")
-    ob, _ = api.decode_attention_batch(q, dst, 0, 1, ctx, 3001)
+    ob, _ = api.decode_attention_batch(q, dst, 0, 1, [3001])
     single = api.DecodeTarget(dst.k_caches, dst.v_caches, 16, dst.block_table[0])
     os_, _ = api.decode_attention(q, single, 0, 1, 3001)
     torch.cuda.synchronize()
@@ -95,13 +101,14 @@ def test_batch_of_one_equals_single_call():
 
 def test_batch_refusals():
     dst, reqs = _batch([64, 64], 32, 8, 128, 8)
-    ctx = torch.tensor([64, 64], dtype=torch.int32, device="cuda")
     q = torch.zeros((2, 4, 128), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(api.CdspError, match="SHAPE"):  # out rows != batch
-        api.decode_attention_batch(q, dst, 0, 1, ctx, 64, out=torch.empty_like(q[:1]))
+        api.decode_attention_batch(q, dst, 0, 1, [64, 64], out=torch.empty_like(q[:1]))
+    with pytest.raises(api.CdspError, match="SHAPE"):  # an empty request
+        api.decode_attention_batch(q, dst, 0, 1, [64, 0])
     with pytest.raises(api.CdspError, match="CAPACITY"):  # a table row covers 64 positions
-        api.decode_attention_batch(q, dst, 0, 1, ctx, 65)
+        api.decode_attention_batch(q, dst, 0, 1, [64, 65])
     small = api.DecodeTarget([x.view(-1, 8, 1, 128) for x in dst.k_caches],
                              [x.view(-1, 8, 1, 128) for x in dst.v_caches], 8, dst.block_table)
     with pytest.raises(api.CdspError, match="UNSUPPORTED"):  # block 8: not the TMA kernel
-        api.decode_attention_batch(q, small, 0, 1, torch.tensor([16, 16], dtype=torch.int32, device="cuda"), 16)
+        api.decode_attention_batch(q, small, 0, 1, [16, 16])

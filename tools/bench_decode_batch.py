@@ -30,7 +30,6 @@ def main():
     ap.add_argument("--mixed", action="store_true")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--no-total", action="store_true", help="size the splits by batch x max_ctx (dev)")
     args = ap.parse_args()
     Hq, Hkv, D, B, tp = 32, 8, 128, 16, 8
     hq_t, hkv_t = Hq // tp, Hkv // tp
@@ -60,16 +59,13 @@ def main():
     q = torch.randn((nb_req, hq_t, D), generator=gd, device=dev).to(torch.bfloat16)
     out = torch.empty_like(q)
     lse = torch.empty((nb_req, hq_t), dtype=torch.float32, device=dev)
-    ctx_d = lens.to(torch.int32).to(dev)
-    max_ctx = int(lens.max())
+    lens_h = [int(x) for x in lens]
     tot = int(lens.sum())
-    tot_arg = 0 if args.no_total else tot
     ws = api.decode_workspace(nb_req * hq_t, nb_req * hkv_t, D, dev)
     st = torch.cuda.current_stream(dev)
 
     def step():
-        api.decode_attention_batch(q, dst, 0, hkv_t, ctx_d, max_ctx, total_ctx=tot_arg, out=out, lse=lse, workspace=ws,
-                                   stream=st)
+        api.decode_attention_batch(q, dst, 0, hkv_t, lens_h, out=out, lse=lse, workspace=ws, stream=st)
 
     for _ in range(args.warmup):
         step()
@@ -86,7 +82,7 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     gbs = bytes_launch / (avg * 1e-3) / 1e9
     line = {"metric": "batched decode attention over paged caches (GB/s)", "value": gbs, "unit": "GB/s",
-            "batch": nb_req, "ctx": args.ctx, "mixed": args.mixed, "sized_by": "max" if args.no_total else "total", "tokens": tot, "tp": tp, "rank": 0,
+            "batch": nb_req, "ctx": args.ctx, "mixed": args.mixed, "tokens": tot, "tp": tp, "rank": 0,
             "q_heads": Hq, "kv_heads": Hkv, "head_dim": D, "block": B, "dtype": "bf16",
             "avg_launch_us": avg * 1e3, "min_launch_us": min(ms) * 1e3, "bytes_per_launch": bytes_launch,
             "hbm_peak_gbs": peaks["hbm_gbs"], "frac_of_hbm": gbs / peaks["hbm_gbs"], "steps": args.steps,
