@@ -31,6 +31,10 @@
 //  * partials: the CTA merges its 8 x TPI lane-group states in shared memory; splits merge
 //    inside the same launch (merge_slice: the last finishers, column slices in parallel):
 //    no second kernel, no host round trip.  Weights 2^(m_j - M) (R3 in base 2).
+//  * a batch of requests (cdsp_decode_attention_batch, TMA kernel only): virtual heads =
+//    (request, KV head) carry the merge state exactly as one request's KV heads do; the grid is
+//    1D over every request's splits back to back (DecTmaBatchArgs: request offsets and lengths in
+//    kernel-parameter space, found by binary search), sized to one wave over the whole batch.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
