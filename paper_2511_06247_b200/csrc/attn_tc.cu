@@ -954,18 +954,17 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
 #endif
     if (warp == W_SCH) {
         // ======== unit scheduler: claim each unit, list its used KV tiles in order (empty ones
-        // skipped), publish it (u_full[i&1]) as soon as every consumer (the K producer included)
-        // is done with the unit two back, and load its Q tile once the Q buffer is free.  Its own
-        // warp: list building and the claim round trip stay off the K stream ========
+        // skipped), publish it (u_full[i&1]; its slot is free once every consumer, the K producer
+        // included, is done with the unit two back) and load its Q tile once the Q buffer is
+        // free.  Its own warp: list building and the claim round trip stay off the K stream ========
         const uint64_t pol_q = policy_evict_first();
         int x = static_cast<int>(blockIdx.x) / CL;
         int x_pre = 0;  // leader lane 0: the unit after x, claimed one unit ahead
         if (leader && lane == 0) x_pre = G + atomicAdd(p.claim, 1);
         int n_ne = 0;      // non-empty units so far
         int* claim_slot = reinterpret_cast<int*>(smem + L::OFF_CLAIM);
-        // prepare unit i (its id in x): list, publish, Q; returns its tile count (-1: no more
-        // units) and its KV head in *kvh_out
-        auto prepare = [&](int i, int* kvh_out) -> int {
+        // prepare unit i (its id in x): list, publish, Q; returns its tile count (-1: no more units)
+        auto prepare = [&](int i) -> int {
             const int ub = i & 1;
             if (i >= 1) {  // unit id: the even CTA claims one unit ahead and tells the odd CTA
                 x = __shfl_sync(0xFFFFFFFFu, x_pre, 0);
@@ -1002,7 +1001,6 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
             int head, part, ux, blo, bhi;
             int64_t row0;
             unit_map(x, crank, head, row0, part, ux, blo, bhi);
-            *kvh_out = head / p.g;
             uint16_t* list = reinterpret_cast<uint16_t*>(smem + L::OFF_SCHED) + ub * L::LISTMAX;
             int64_t qlo, qhi, plo = 0, phi = 0;
             bool qany, pany = false;
@@ -1077,10 +1075,9 @@ __global__ void __maxnreg__(CDSP_REGSPLIT ? 128 : CDSP_MAXNREG)
         // unit i is claimed and prepared once the K producer is kPrepLead tiles from the end of
         // unit i - 1: late enough that the claim order still balances the launch's tail, early
         // enough that the list, the publication and the Q load are done when its first S is due
-        int kvh_unused = 0;
         for (int i = 0;; ++i) {
             if (i >= 1) mbar_wait(bar(L::B_PR + ((i - 1) & 1)), ((i - 1) >> 1) & 1);
-            if (prepare(i, &kvh_unused) < 0) break;
+            if (prepare(i) < 0) break;
         }
     } else if (warp == W_K) {
         // ======== TMA producer of K (3 stages), following the published units ========
