@@ -1840,8 +1840,12 @@ cdsp_status launch_tc(const AttnArgs& a, cudaStream_t st) {
         // group's share, in the heads of the last ~1.5 waves, at the block boundary that halves
         // the heaviest unit
         const double share = static_cast<double>(W) * a.Hq / max_groups;
+        // only where units are few per CTA group (the tail is a large part of the launch): 32K MHA
+        // ring proxy, s = 8 (7 units per group) 1292-1294 split vs 1232-1237 TF/s; s = 4 (14) even;
+        // s = 2 (28) no gain (profiles/r02_split_rule_ab.md)
+        const bool few_units = static_cast<int64_t>(p.n_pb) * a.Hq < 10ll * max_groups;
         int n = 0;
-        if (split_env && a.split_ok && a.nblk >= 2 && a.mode == CDSP_ATTN_ONLY && a.o_acc && a.lse_acc)
+        if (split_env && few_units && a.split_ok && a.nblk >= 2 && a.mode == CDSP_ATTN_ONLY && a.o_acc && a.lse_acc)
             while (n < p.n_pb - p.n_light && w[p.n_pb - 1 - n] * 6.0 > share && w[p.n_pb - 1 - n] >= 32) ++n;
         if (n > 0) {
             // region B + C (pieces no larger than half the heaviest unit) carries at least 1.5
