@@ -318,3 +318,31 @@ def test_kv_block_at_capacity_512k_keys():
     rows = sample_rows(nq, 24, seed=3, edges=[0, 127, 128, nq - 1])
     o_ref, l_ref = oracle.causal_rows(_np(q), _np(k), _np(v), scale, rows=(rows + nkv - nq).numpy())
     _check(out[rows], lse[:, rows], o_ref, l_ref, torch.bfloat16, "512K keys")
+
+
+def test_one_sm_kernel_d128_subprocess():
+    """CDSP_ATTN_1SM=1 (read once per process) runs D = 128 on the 1-SM kernel instead of CTA
+    pairs (the measurement control of DESIGN 6.1): a ragged causal launch, every row vs the
+    oracle, in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import math, numpy as np, torch, oracle
+from cdsp_inputs import qkv
+from paper_2511_06247_b200 import api
+N, Hq, Hkv, D = 1500, 4, 2, 128
+q, k, v = qkv(N, Hq, Hkv, D, torch.bfloat16, seed=77)
+s = 1.0 / math.sqrt(D)
+out = torch.empty_like(q.cuda()); lse = torch.empty((Hq, N), dtype=torch.float32, device="cuda")
+api.attention_fwd(q.cuda(), k.cuda(), v.cuda(), api.causal_segments(N, N), s, api.ATTN_ONLY, out=out, lse=lse)
+torch.cuda.synchronize()
+o_ref, l_ref = oracle.causal_rows(q.float().numpy(), k.float().numpy(), v.float().numpy(), s)
+print("ERR", float(np.abs(out.float().cpu().numpy() - o_ref).max()), float(np.abs(lse.cpu().numpy() - l_ref).max()))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CDSP_ATTN_1SM="1", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    err, lerr = [float(x) for x in [l for l in r.stdout.splitlines() if l.startswith("ERR")][0].split()[1:]]
+    assert err <= 2e-2 and lerr <= 1e-3, (err, lerr)
