@@ -57,7 +57,9 @@ def analyze(path, n_units):
     p_arr = d[np.arange(n), 4 * g + 3]
     for name, x in (("S seen->m ready", m_ready - s_seen), ("m ready->exps done", exps - m_ready),
                     ("exps->P arrive", p_arr - exps), ("P arrive->PV issue", pv - p_arr),
-                    ("S issue->S seen", s_seen[3:] - d[3:n, 9])):
+                    ("S issue->S seen", s_seen[3:] - d[3:n, 9]), ("MMA V wait", d[:n, 11] - d[:n, 10]),
+                    ("MMA P wait (after V)", pv - d[:n, 11]), ("K load->S issue", d[3:n, 9] - d[3:n, 15]),
+                    ("V load->PV issue", pv[3:] - d[3:n, 14])):
         print(f"  {name:20s} median {np.median(x):7.0f}  p90 {np.percentile(x, 90):7.0f}")
     big = np.nonzero(dpv > 2 * med)[0][:6]
     for k in big:
