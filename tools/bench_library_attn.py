@@ -1,7 +1,7 @@
 """Context numbers (not the product, not the target): the installed libraries' causal prefill
 attention on the bench's s = 1 workload (32K MHA 32/32, d = 128, bf16), same box, CUDA events.
 
-    python tools/bench_library_attn.py --backend {cudnn,flash2,fi_cutlass,fi_trtllm,fi_fa2,ours}
+    python tools/bench_library_attn.py --backend {cudnn,flash2,fi_fa2,ours}
 
 One JSON line per call: TFLOP/s = 4·d·Hq·L(L+1)/2 (the visible causal pairs, the same count
 bench.py uses) / average launch time over `--iters` back-to-back launches after warm-up.  Run each
@@ -66,7 +66,7 @@ def main():
                                                       enable_gqa=Hq != Hkv)
     elif b.startswith("fi_"):
         import flashinfer
-        be = {"fi_cutlass": "cutlass", "fi_fa2": "fa2", "fi_trtllm": "trtllm-gen"}[b]
+        be = {"fi_fa2": "fa2"}[b]  # (the installed flashinfer's single-prefill API offers fa2 / fa3 only)
         note = f"flashinfer {flashinfer.__version__} single_prefill_with_kv_cache backend={be}"
 
         def fn():
