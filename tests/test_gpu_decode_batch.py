@@ -112,3 +112,21 @@ def test_batch_refusals():
                              [x.view(-1, 8, 1, 128) for x in dst.v_caches], 8, dst.block_table)
     with pytest.raises(api.CdspError, match="UNSUPPORTED"):  # block 8: not the TMA kernel
         api.decode_attention_batch(q, small, 0, 1, [16, 16])
+
+
+def test_batch_bench_shape_32x32k():
+    """The bench's launch configuration (tools/bench_decode_batch.py, 32 requests x 32K on a rank
+    with 4 query heads / 1 KV head: 32 virtual heads x 9 splits, one wave): sampled requests vs
+    the oracle."""
+    lens = [32768] * 32
+    dst, reqs = _batch(lens, 4, 1, 128, 1)
+    q = torch.cat([r[0] for r in reqs]).contiguous().cuda()
+    lse = torch.empty((32, 4), dtype=torch.float32, device="cuda")
+    out, _ = api.decode_attention_batch(q, dst, 0, 1, lens, lse=lse)
+    torch.cuda.synchronize()
+    for b in (0, 13, 31):
+        qb, k, v = reqs[b]
+        o_ref, l_ref = oracle.attention(qb.float().numpy(), np.array([32767]), k.float().numpy(), v.float().numpy(),
+                                        np.arange(32768), 1.0 / math.sqrt(128))
+        assert float(np.abs(out[b:b + 1].float().cpu().numpy() - o_ref).max()) <= TOL, b
+        assert float(np.abs(lse[b].cpu().numpy() - l_ref[:, 0]).max()) <= LSE_TOL, b
